@@ -1,0 +1,186 @@
+/*
+ * cg.h -- C ABI of the B200-native cell-graph builder (arXiv 1503.06029).
+ *
+ * Citations "P:n" are lines of the paper's text (reference PAPER.md); "G.."
+ * are the readings listed in DESIGN.md.  No torch or CUDA-runtime types appear
+ * in these signatures: pointers are plain (device unless stated), sizes are
+ * int64, streams are passed as the opaque cudaStream_t handle value.
+ *
+ * The problem.  X = {x_0..x_{n-1}} is a multiset of n binary
+ * vectors of length ell (a cell signature: bit i = 1 iff the sampled point
+ * satisfies constraint c_i).  The cell graph G_X has the distinct
+ * vectors as vertices and an edge between every pair at Hamming distance
+ * exactly 1.  cg_build returns
+ *   cells: the distinct vectors in canonical order -- lexicographic, bit 0
+ *          first, 0 < 1 (the order "sort X" gives; pinned by
+ *          Fig. 2; G1) -- and
+ *   edges: every pair (i, j), i < j, of canonical indices with
+ *          dist(cells[i], cells[j]) = 1, each pair once, ascending by (i, j)
+ *          (G3, G4).
+ *
+ * Packed word format (cells, cg_query inputs): W = ceil(ell/64) u64 words per
+ * vector, bit k in word k/64 at bit position 63-(k%64) (MSB-first), so that
+ * comparing rows word by word as unsigned integers IS the canonical order.
+ * The unused low bits of the last word are zero (G6).
+ *
+ * Errors: every entry point returns CG_OK (0) or a negative code; details
+ * for the calling thread are in cg_last_error().  On error all output structs
+ * are zeroed and nothing is leaked.
+ */
+#ifndef CG_H_
+#define CG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cg_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+enum {
+  CG_OK = 0,
+  CG_EINVAL = -1,   /* bad argument: n < 1, ell not in [1, CG_MAX_ELL], NULL or host pointer where a device pointer is required */
+  CG_EINPUT = -2,   /* an input byte is not 0 or 1 (G5), or set pad bits in packed input */
+  CG_ENOMEM = -3,   /* device (or pinned host) allocation failed */
+  CG_ECUDA = -4,    /* a CUDA runtime error (kernel launch, sticky error) */
+  CG_ETOOBIG = -5,  /* n >= 2^32 (cell and edge indices are u32, G11) */
+  CG_EARCH = -6,    /* the current device is not sm_100 (B200) */
+  CG_ENOTIMPL = -7  /* option not implemented */
+};
+
+#define CG_MAX_ELL 4096
+
+/* Cell table: words[n_cells][words_per_cell] (device, owned by the caller,
+ * release with cg_cells_free).  Rows strictly increasing. */
+typedef struct {
+  uint64_t* words;
+  int64_t n_cells;
+  int32_t ell;
+  int32_t words_per_cell;
+} cg_cells;
+
+/* Edge list: ij[n_edges][2] u32 (device, owned by the caller, release with
+ * cg_edges_free).  ij[2e] < ij[2e+1]; ascending by (i, j); each pair once. */
+typedef struct {
+  uint32_t* ij;
+  int64_t n_edges;
+} cg_edges;
+
+/* Opaque, immutable dictionary over a cell table (the popcount-layered,
+ * prefix-indexed sorted array built by cg_build_ex, see DESIGN.md a4-a5). */
+typedef struct cg_index cg_index;
+
+/* Per-stage device times (CUDA events on the build stream, microseconds)
+ * and counters; filled when cg_opts.stats != NULL. */
+typedef struct {
+  double us_total, us_pack, us_sort, us_dedupe, us_layers, us_dict, us_probe, us_edges;
+  int64_t n_in, n_cells, n_edges;
+  int64_t logical_probes; /* n_cells * ell: the paper's one probe per (cell, bit) */
+  int64_t issued_probes;  /* lookups actually issued (0->1 flips, <= lcp when pruning) */
+  int32_t sort_passes;    /* radix passes executed by the cell sort */
+  int32_t probe_reruns;   /* probe stage reruns because the edge buffer was too small */
+} cg_stats;
+
+enum {
+  CG_DICT_SORTED = 0, /* per-layer sorted array + 2^b prefix index, then binary search (default) */
+  CG_DICT_BSEARCH = 1 /* per-layer sorted array, plain binary search (no prefix index) */
+};
+
+typedef struct {
+  cg_stream_t stream;   /* stream all work is ordered on (NULL = legacy default) */
+  int32_t dict_kind;    /* CG_DICT_* */
+  int32_t lcp_prune;    /* 1: probe bit k only if k <= lcp(V_i, V_{i+1}) (exact, DESIGN a6) */
+  int32_t bucket_log2;  /* prefix index: target log2(cells per bucket); -1 = default (2) */
+  int32_t reserved;
+  cg_index** index_out; /* if non-NULL, receives the dictionary (release with cg_index_free) */
+  cg_stats* stats;      /* if non-NULL, stage times and counters */
+} cg_opts;
+
+/* Fill *o with defaults: stream NULL, CG_DICT_SORTED, lcp_prune 1,
+ * bucket_log2 -1, no index, no stats. */
+void cg_opts_init(cg_opts* o);
+
+/* Build the cell graph of vecs = uint8[n][ell] (device, row-major,
+ * contiguous; byte k of row r is bit k of x_r and must be 0 or 1, G5).
+ * Input is borrowed read-only.  Blocks until cells/edges are complete (it
+ * must learn n_cells and n_edges).  Errors: CG_EINVAL (n < 1, ell out of
+ * range, NULL/host vecs), CG_ETOOBIG (n >= 2^32), CG_EINPUT (a byte > 1),
+ * CG_ENOMEM, CG_ECUDA. */
+int cg_build(const uint8_t* vecs, int64_t n, int32_t ell, cg_cells* cells, cg_edges* edges);
+
+/* As cg_build with options (stream, dictionary kind, index and stats out). */
+int cg_build_ex(const uint8_t* vecs, int64_t n, int32_t ell, const cg_opts* o, cg_cells* cells,
+                cg_edges* edges);
+
+/* As cg_build_ex from already packed vectors words = u64[n][ceil(ell/64)]
+ * (device) in the packed word format; set pad bits -> CG_EINPUT. */
+int cg_build_packed_ex(const uint64_t* words, int64_t n, int32_t ell, const cg_opts* o,
+                       cg_cells* cells, cg_edges* edges);
+
+/* End-to-end entry with HOST buffers.  h_vecs = uint8[n][ell] in host memory
+ * (pinned for full PCIe speed, pageable accepted).  The library copies it to
+ * the device (chunked, overlapped with the pack kernel), builds, and copies
+ * the results back into host arrays it allocates (pinned; release with
+ * cg_host_free).  *h_cells = u64[*n_cells][W], *h_edges = u32[*n_edges][2].
+ * Same error codes as cg_build_ex (CG_EINVAL for a NULL host pointer). */
+int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* o,
+                  uint64_t** h_cells, int64_t* n_cells, uint32_t** h_edges, int64_t* n_edges);
+void cg_host_free(void* p);
+
+/* Streaming query against a built index.  q = u64[nq][W] packed cells
+ * (device; pad bits ignored, G19).  Writes (device)
+ *   self_idx[r]        = canonical index of q_r, or -1 if q_r is not a cell;
+ *   nbr_idx[r*ell + k] = canonical index of q_r with bit k negated, or -1.
+ * Asynchronous on stream s (no host sync); nq == 0 is a no-op.
+ * Errors: CG_EINVAL (NULL index, NULL pointers with nq > 0, nq < 0). */
+int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_idx,
+             int32_t* nbr_idx, cg_stream_t s);
+
+/* Index metadata (host). */
+int cg_index_info(const cg_index* idx, int64_t* n_cells, int32_t* ell);
+
+/* Allocator hook for every device allocation the library makes (outputs and
+ * workspace).  alloc(bytes, stream, ctx) returns a device pointer or NULL;
+ * dealloc(ptr, stream, ctx).  Passing NULLs restores the default
+ * (cudaMallocAsync / cudaFreeAsync on the stream's device memory pool).
+ * Must not be changed while outputs allocated by the previous allocator are
+ * alive. */
+int cg_set_allocator(void* (*alloc)(size_t, cg_stream_t, void*),
+                     void (*dealloc)(void*, cg_stream_t, void*), void* ctx);
+
+void cg_cells_free(cg_cells* c); /* frees c->words, zeroes *c; NULL-safe */
+void cg_edges_free(cg_edges* e); /* frees e->ij, zeroes *e; NULL-safe */
+void cg_index_free(cg_index* idx);
+
+const char* cg_strerror(int code);
+const char* cg_last_error(void); /* thread-local detail of the last failure */
+int cg_version(void);            /* (major << 16) | minor */
+
+/* ---- distributed phases (one process per GPU; the caller runs the NCCL
+ * collectives between them) ----------------- */
+
+/* Phase 1: pack + sort + dedupe this rank's rows: a sorted unique run. */
+int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_opts* o,
+                  cg_cells* run);
+
+/* Phase 2: merge G gathered runs (device buffer runs = u64[G][stride][W],
+ * run g holding counts[g] (host array) valid rows) into the global canonical
+ * table (identical on every rank), then probe this rank's share of the
+ * queries: the cells of the (popcount, canonical index) order between the
+ * cut points at equal issued-probe weight r/G and (r+1)/G.  Returns the
+ * table and this rank's edges (canonical (i, j), ascending). */
+int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, int64_t stride,
+                        int32_t ell, int32_t rank, const cg_opts* o, cg_cells* table,
+                        cg_edges* local_edges);
+
+/* Phase 3: merge G gathered edge lists (device buffer u32[G][stride][2],
+ * list g holding counts[g] (host) valid pairs) into the canonical list. */
+int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G, int64_t stride,
+                     const cg_opts* o, cg_edges* edges);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CG_H_ */

@@ -1,0 +1,13 @@
+"""B200-native cell-graph construction (arXiv 1503.06029): the data-parallel
+hot path -- pack, radix sort, dedupe, popcount layering, prefix-indexed
+sorted dictionary, single-bit-flip probes, canonical edge sort -- as
+hand-written sm_100a CUDA behind the C ABI of include/cg.h.
+
+    from paper_1503_06029_b200 import build
+    res = build(vecs_uint8_cuda)      # res.cells int64 [nc, W], res.edges int32 [m, 2]
+"""
+from .cg import (BuildResult, CgError, Index, build, build_host, build_packed, lib,  # noqa: F401
+                 version)
+
+__all__ = ["build", "build_packed", "build_host", "BuildResult", "Index", "CgError", "lib",
+           "version"]

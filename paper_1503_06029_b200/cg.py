@@ -1,0 +1,340 @@
+"""Thin Python binding of the C ABI in include/cg.h (ctypes; marshalling only).
+
+Every step of the path runs in the CUDA kernels of ``lib/libcg.so``; this
+module only passes device pointers, sizes and the stream handle, and wraps
+the returned device buffers as torch tensors without copying (through
+``__cuda_array_interface__``; the tensor owns the buffer and frees it with
+``cg_cells_free`` / ``cg_edges_free`` when collected).  There is no CPU
+fallback: if the library is missing or the device is not a B200 the calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libcg.so")
+
+CG_OK, CG_EINVAL, CG_EINPUT, CG_ENOMEM, CG_ECUDA, CG_ETOOBIG, CG_EARCH, CG_ENOTIMPL = (
+    0, -1, -2, -3, -4, -5, -6, -7)
+CG_DICT_SORTED, CG_DICT_BSEARCH = 0, 1
+DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH}
+
+
+class CgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"cg error {code}: {msg}")
+        self.code = code
+
+
+class cg_cells(ctypes.Structure):
+    _fields_ = [("words", ctypes.c_void_p), ("n_cells", ctypes.c_int64),
+                ("ell", ctypes.c_int32), ("words_per_cell", ctypes.c_int32)]
+
+
+class cg_edges(ctypes.Structure):
+    _fields_ = [("ij", ctypes.c_void_p), ("n_edges", ctypes.c_int64)]
+
+
+class cg_stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in
+                ("us_total", "us_pack", "us_sort", "us_dedupe", "us_layers", "us_dict",
+                 "us_probe", "us_edges")] + \
+               [(k, ctypes.c_int64) for k in
+                ("n_in", "n_cells", "n_edges", "logical_probes", "issued_probes")] + \
+               [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32)]
+
+
+class cg_opts(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_void_p), ("dict_kind", ctypes.c_int32),
+                ("lcp_prune", ctypes.c_int32), ("bucket_log2", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("index_out", ctypes.c_void_p),
+                ("stats", ctypes.POINTER(cg_stats))]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcg.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise CgError(CG_ENOTIMPL, f"{LIB_PATH} not built (run __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    L.cg_opts_init.argtypes = [ctypes.POINTER(cg_opts)]
+    L.cg_opts_init.restype = None
+    for name in ("cg_build_ex",):
+        f = getattr(L, name)
+        f.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells),
+                      ctypes.POINTER(cg_edges)]
+        f.restype = ctypes.c_int
+    L.cg_build.argtypes = [P, i64, i32, ctypes.POINTER(cg_cells), ctypes.POINTER(cg_edges)]
+    L.cg_build.restype = ctypes.c_int
+    L.cg_build_packed_ex.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts),
+                                     ctypes.POINTER(cg_cells), ctypes.POINTER(cg_edges)]
+    L.cg_build_packed_ex.restype = ctypes.c_int
+    L.cg_build_host.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts),
+                                ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64),
+                                ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64)]
+    L.cg_build_host.restype = ctypes.c_int
+    L.cg_host_free.argtypes = [P]
+    L.cg_host_free.restype = None
+    L.cg_query.argtypes = [P, P, i64, P, P, P]
+    L.cg_query.restype = ctypes.c_int
+    L.cg_index_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.cg_index_info.restype = ctypes.c_int
+    L.cg_cells_free.argtypes = [ctypes.POINTER(cg_cells)]
+    L.cg_cells_free.restype = None
+    L.cg_edges_free.argtypes = [ctypes.POINTER(cg_edges)]
+    L.cg_edges_free.restype = None
+    L.cg_index_free.argtypes = [P]
+    L.cg_index_free.restype = None
+    L.cg_strerror.argtypes = [ctypes.c_int]
+    L.cg_strerror.restype = ctypes.c_char_p
+    L.cg_last_error.argtypes = []
+    L.cg_last_error.restype = ctypes.c_char_p
+    L.cg_version.argtypes = []
+    L.cg_version.restype = ctypes.c_int
+    L.cg_dist_local.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells)]
+    L.cg_dist_local.restype = ctypes.c_int
+    L.cg_dist_merge_probe.argtypes = [P, ctypes.POINTER(i64), i32, i64, i32, i32,
+                                      ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells),
+                                      ctypes.POINTER(cg_edges)]
+    L.cg_dist_merge_probe.restype = ctypes.c_int
+    L.cg_dist_finalize.argtypes = [P, ctypes.POINTER(i64), i32, i64, ctypes.POINTER(cg_opts),
+                                   ctypes.POINTER(cg_edges)]
+    L.cg_dist_finalize.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg_build_host",
+            "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
+            "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
+            "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
+
+
+def _check(rc: int):
+    if rc != CG_OK:
+        L = lib()
+        raise CgError(rc, f"{L.cg_strerror(rc).decode()}: {L.cg_last_error().decode()}")
+
+
+class _DevBlock:
+    """Owner of one device buffer returned by the library; exposes it through
+    __cuda_array_interface__ so torch.as_tensor wraps it without a copy."""
+
+    def __init__(self, kind: str, struct, ptr: int, shape, typestr: str):
+        self._kind, self._struct = kind, struct
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+            "version": 3, "strides": None, "stream": None}
+
+    def __del__(self):
+        try:
+            L = lib()
+            if self._kind == "cells":
+                L.cg_cells_free(ctypes.byref(self._struct))
+            else:
+                L.cg_edges_free(ctypes.byref(self._struct))
+        except Exception:
+            pass
+
+
+def _wrap_cells(c: cg_cells, device) -> torch.Tensor:
+    W = max(1, c.words_per_cell)
+    if c.n_cells == 0:
+        return torch.zeros((0, W), dtype=torch.int64, device=device)
+    blk = _DevBlock("cells", c, c.words, (c.n_cells, W), "<i8")
+    return torch.as_tensor(blk, device=device)
+
+
+def _wrap_edges(e: cg_edges, device) -> torch.Tensor:
+    if e.n_edges == 0:
+        L = lib()
+        L.cg_edges_free(ctypes.byref(e))
+        return torch.zeros((0, 2), dtype=torch.int32, device=device)
+    blk = _DevBlock("edges", e, e.ij, (e.n_edges, 2), "<i4")
+    return torch.as_tensor(blk, device=device)
+
+
+class Index:
+    """Dictionary over a cell table (cg_index); immutable, for cg_query."""
+
+    def __init__(self, handle: int, device):
+        self.handle = handle
+        self.device = device
+        n = ctypes.c_int64()
+        ell = ctypes.c_int32()
+        _check(lib().cg_index_info(ctypes.c_void_p(handle), ctypes.byref(n), ctypes.byref(ell)))
+        self.n_cells, self.ell = n.value, ell.value
+        self.words = (self.ell + 63) // 64
+
+    def query(self, q: torch.Tensor, stream: torch.cuda.Stream | None = None):
+        """q: int64 [nq, W] packed cells (device).  Returns (self_idx int32 [nq],
+        nbr_idx int32 [nq, ell]); asynchronous on the stream."""
+        if q.dim() != 2 or q.shape[1] != self.words or q.dtype != torch.int64 or not q.is_cuda:
+            raise CgError(CG_EINVAL, "q must be a CUDA int64 tensor [nq, ceil(ell/64)]")
+        q = q.contiguous()
+        nq = q.shape[0]
+        self_idx = torch.empty(nq, dtype=torch.int32, device=q.device)
+        nbr = torch.empty((nq, self.ell), dtype=torch.int32, device=q.device)
+        st = stream or torch.cuda.current_stream(q.device)
+        _check(lib().cg_query(ctypes.c_void_p(self.handle), ctypes.c_void_p(q.data_ptr()), nq,
+                              ctypes.c_void_p(self_idx.data_ptr()),
+                              ctypes.c_void_p(nbr.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+        return self_idx, nbr
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().cg_index_free(ctypes.c_void_p(self.handle))
+                self.handle = 0
+        except Exception:
+            pass
+
+
+@dataclass
+class BuildResult:
+    cells: torch.Tensor          # int64 [n_cells, W] (u64 bit patterns, canonical order)
+    edges: torch.Tensor          # int32 [n_edges, 2] (u32 values, i < j, ascending)
+    stats: dict = field(default_factory=dict)
+    index: Index | None = None
+
+
+def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats):
+    L = lib()
+    o = cg_opts()
+    L.cg_opts_init(ctypes.byref(o))
+    o.stream = ctypes.c_void_p(stream.cuda_stream)
+    o.dict_kind = DICT_KINDS[dict_kind] if isinstance(dict_kind, str) else int(dict_kind)
+    o.lcp_prune = int(bool(lcp_prune))
+    o.bucket_log2 = int(bucket_log2)
+    ih = ctypes.c_void_p()
+    st = cg_stats()
+    if want_index:
+        o.index_out = ctypes.cast(ctypes.byref(ih), ctypes.c_void_p)
+    if want_stats:
+        o.stats = ctypes.pointer(st)
+    return o, ih, st
+
+
+def _stats_dict(st: cg_stats) -> dict:
+    return {k: getattr(st, k) for k, _ in cg_stats._fields_}
+
+
+def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
+          dict_kind="sorted", lcp_prune: bool = True, bucket_log2: int = -1,
+          want_index: bool = False, want_stats: bool = False) -> BuildResult:
+    """cg_build_ex on a CUDA uint8 tensor [n, ell] of 0/1 bytes."""
+    if not isinstance(vecs, torch.Tensor) or vecs.dim() != 2:
+        raise CgError(CG_EINVAL, "vecs must be a 2-D tensor [n, ell]")
+    if vecs.dtype != torch.uint8:
+        raise CgError(CG_EINVAL, "vecs must be uint8")
+    if not vecs.is_cuda:
+        raise CgError(CG_EINVAL, "vecs must be a CUDA tensor (no CPU fallback)")
+    vecs = vecs.contiguous()
+    n, ell = vecs.shape
+    stream = stream or torch.cuda.current_stream(vecs.device)
+    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats)
+    c, e = cg_cells(), cg_edges()
+    with torch.cuda.device(vecs.device):
+        _check(lib().cg_build_ex(ctypes.c_void_p(vecs.data_ptr()), n, ell, ctypes.byref(o),
+                                 ctypes.byref(c), ctypes.byref(e)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    res = BuildResult(_wrap_cells(c, vecs.device), _wrap_edges(e, vecs.device))
+    if want_stats:
+        res.stats = _stats_dict(st)
+    if want_index and ih.value:
+        res.index = Index(ih.value, vecs.device)
+    return res
+
+
+def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="sorted",
+                 lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False):
+    """cg_build_packed_ex on CUDA int64 [n, ceil(ell/64)] MSB-first words."""
+    if words.dim() != 2 or words.dtype != torch.int64 or not words.is_cuda:
+        raise CgError(CG_EINVAL, "words must be a CUDA int64 tensor [n, W]")
+    words = words.contiguous()
+    n = words.shape[0]
+    stream = stream or torch.cuda.current_stream(words.device)
+    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats)
+    c, e = cg_cells(), cg_edges()
+    with torch.cuda.device(words.device):
+        _check(lib().cg_build_packed_ex(ctypes.c_void_p(words.data_ptr()), n, ell,
+                                        ctypes.byref(o), ctypes.byref(c), ctypes.byref(e)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    res = BuildResult(_wrap_cells(c, words.device), _wrap_edges(e, words.device))
+    if want_stats:
+        res.stats = _stats_dict(st)
+    if want_index and ih.value:
+        res.index = Index(ih.value, words.device)
+    return res
+
+
+def build_host(vecs_host: torch.Tensor, *, device=None, stream=None, dict_kind="sorted",
+               lcp_prune=True, bucket_log2=-1, want_stats=False):
+    """cg_build_host: uint8 [n, ell] HOST tensor (pinned for full speed) in,
+    numpy-compatible host results out: (cells int64 [nc, W], edges int32 [m, 2],
+    stats).  Host<->device copies happen inside the library call."""
+    import numpy as np
+
+    if vecs_host.is_cuda or vecs_host.dtype != torch.uint8 or vecs_host.dim() != 2:
+        raise CgError(CG_EINVAL, "vecs_host must be a CPU uint8 tensor [n, ell]")
+    vecs_host = vecs_host.contiguous()
+    n, ell = vecs_host.shape
+    device = torch.device(device or "cuda")
+    with torch.cuda.device(device):
+        stream = stream or torch.cuda.current_stream(device)
+        o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, False, want_stats)
+        hc, he = ctypes.c_void_p(), ctypes.c_void_p()
+        nc, ne = ctypes.c_int64(), ctypes.c_int64()
+        L = lib()
+        _check(L.cg_build_host(ctypes.c_void_p(vecs_host.data_ptr()), n, ell, ctypes.byref(o),
+                               ctypes.byref(hc), ctypes.byref(nc), ctypes.byref(he),
+                               ctypes.byref(ne)))
+    W = (ell + 63) // 64
+    try:
+        cells = np.ctypeslib.as_array(ctypes.cast(hc.value, ctypes.POINTER(ctypes.c_int64)),
+                                      shape=(nc.value * W,)).reshape(nc.value, W).copy()
+        edges = (np.ctypeslib.as_array(ctypes.cast(he.value, ctypes.POINTER(ctypes.c_int32)),
+                                       shape=(ne.value * 2,)).reshape(ne.value, 2).copy()
+                 if ne.value else np.zeros((0, 2), np.int32))
+    finally:
+        L.cg_host_free(hc)
+        L.cg_host_free(he)
+    return cells, edges, (_stats_dict(st) if want_stats else {})
+
+
+def build_host_raw(vecs_host: torch.Tensor, *, stream=None, want_stats=False):
+    """As build_host but returns the library's pinned host pointers and counts
+    without copying (caller must release with release_host); used by the e2e
+    bench leg so the timed region holds exactly the library call."""
+    n, ell = vecs_host.shape
+    device = torch.device("cuda")
+    stream = stream or torch.cuda.current_stream(device)
+    o, ih, st = _opts(stream, "sorted", True, -1, False, want_stats)
+    hc, he = ctypes.c_void_p(), ctypes.c_void_p()
+    nc, ne = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().cg_build_host(ctypes.c_void_p(vecs_host.data_ptr()), n, ell, ctypes.byref(o),
+                               ctypes.byref(hc), ctypes.byref(nc), ctypes.byref(he),
+                               ctypes.byref(ne)))
+    return hc.value, nc.value, he.value, ne.value, (_stats_dict(st) if want_stats else {})
+
+
+def release_host(*ptrs):
+    L = lib()
+    for p in ptrs:
+        if p:
+            L.cg_host_free(ctypes.c_void_p(p))
+
+
+def version() -> int:
+    return lib().cg_version()

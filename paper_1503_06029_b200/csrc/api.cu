@@ -1,0 +1,634 @@
+// api.cu -- the C ABI (include/cg.h): argument checks, allocation, and the
+// host pipeline that runs the hot path on one stream:
+//   a1 pack -> a2 sort -> a3 dedupe (read back n_c) -> a4 layers (read back
+//   layer offsets) -> a5 prefix index -> a6 probes + a7 append (read back m)
+//   -> a7 canonical edge sort.
+// See DESIGN.md for the data layout and the paper passages of each step.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+
+struct cg_index {
+  cgk::DictView view;
+  // owned device buffers
+  uint64_t* keys = nullptr;
+  uint32_t* idx = nullptr;
+  uint32_t* layer_off = nullptr;
+  uint32_t* T = nullptr;
+  uint64_t* tbase = nullptr;
+  uint8_t* tbits = nullptr;
+  int device = 0;
+};
+
+namespace cgk {
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+// ---------------------------------------------------------------- allocator
+static void* (*g_alloc)(size_t, cg_stream_t, void*) = nullptr;
+static void (*g_dealloc)(void*, cg_stream_t, void*) = nullptr;
+static void* g_alloc_ctx = nullptr;
+static std::once_flag g_pool_once;
+
+static void init_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~uint64_t(0);  // keep freed blocks cached in the pool
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (g_alloc) {
+    p = g_alloc(bytes, reinterpret_cast<cg_stream_t>(s), g_alloc_ctx);
+    if (!p) throw CgError{CG_ENOMEM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes"};
+    return p;
+  }
+  std::call_once(g_pool_once, init_pool);
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CgError{CG_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e)};
+  }
+  return p;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+  if (!p) return;
+  if (g_dealloc) {
+    g_dealloc(p, reinterpret_cast<cg_stream_t>(s), g_alloc_ctx);
+    return;
+  }
+  cudaFreeAsync(p, s);
+}
+
+void* host_stage(size_t bytes) {
+  static thread_local void* buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 16);
+    CG_CUDA(cudaMallocHost(&buf, want));
+    cap = want;
+  }
+  return buf;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+// ---------------------------------------------------------------- pinned host pool (cg_build_host)
+static std::mutex g_host_mu;
+static std::multimap<size_t, void*> g_host_free;
+static std::map<void*, size_t> g_host_size;
+
+static void* host_pool_alloc(size_t bytes) {
+  bytes = std::max<size_t>(bytes, 64);
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  auto it = g_host_free.lower_bound(bytes);
+  if (it != g_host_free.end() && it->first <= 2 * bytes) {
+    void* p = it->second;
+    g_host_free.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    throw CgError{CG_ENOMEM, "cudaHostAlloc(" + std::to_string(bytes) + ") failed"};
+  }
+  g_host_size[p] = bytes;
+  return p;
+}
+
+static void host_pool_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  auto it = g_host_size.find(p);
+  if (it == g_host_size.end()) return;
+  g_host_free.emplace(it->second, p);
+}
+
+// ---------------------------------------------------------------- stage timer
+struct StageTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;
+  void start(bool enable, cudaStream_t st) {
+    on = enable;
+    s = st;
+    if (on) mark();
+  }
+  void mark() {
+    if (!on) return;
+    cudaEvent_t e;
+    CG_CUDA(cudaEventCreate(&e));
+    CG_CUDA(cudaEventRecord(e, s));
+    ev.push_back(e);
+  }
+  double us(int a, int b) const {
+    if (!on || b >= int(ev.size())) return 0.0;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return double(ms) * 1e3;
+  }
+  ~StageTimer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+static int bits_for(uint32_t v) {
+  int b = 0;
+  while ((uint64_t(1) << b) <= v) ++b;
+  return std::max(b, 1);
+}
+
+static void check_device_ptr(const void* p, const char* what) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CgError{CG_EINVAL, std::string(what) + ": not a CUDA pointer"};
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    throw CgError{CG_EINVAL, std::string(what) + ": host pointer where a device pointer is required"};
+}
+
+static void check_arch() {
+  int dev = 0, major = 0;
+  CG_CUDA(cudaGetDevice(&dev));
+  CG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw CgError{CG_EARCH, "cg is built for sm_100a (B200); device major = " + std::to_string(major)};
+}
+
+// ---------------------------------------------------------------- the pipeline
+struct Built {
+  uint64_t* cells = nullptr;
+  int64_t n_cells = 0;
+  uint32_t* edges = nullptr;  // (i, j) u32 pairs
+  int64_t n_edges = 0;
+  cg_index* index = nullptr;
+};
+
+// Runs a2..a7 given packed keys (u64[n][W], consumed as scratch).
+static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
+                            uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+  const int W = (ell + 63) / 64;
+  SortStats sst;
+  // ---- a2 sort
+  DevBuf<uint64_t> alt(size_t(n) * W, s);
+  const uint64_t* sorted = nullptr;
+  if (W == 1) {
+    uint64_t* ko = nullptr;
+    radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, n, 64, &ko, nullptr, s,
+                         &sst);
+    sorted = ko;
+  } else {
+    sort_rows_multiword(keys.p, n, W, alt.p, s, &sst);
+    sorted = alt.p;
+  }
+  tm.mark();  // 2: sort
+  // ---- a3 dedupe + compaction
+  DevBuf<uint64_t> cellbuf(size_t(n) * W, s);
+  DevBuf<uint32_t> popc(size_t(n), s);
+  DevBuf<uint16_t> lcp(size_t(n), s);
+  launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+  uint32_t* hf = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(hf, d_flags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  if (hf[0]) throw CgError{CG_EINPUT, "input byte not in {0,1} (or pad bit set in packed input)"};
+  const int64_t nc = hf[1];
+  tm.mark();  // 3: dedupe
+  keys.reset();
+  alt.reset();
+  // ---- a4 popcount layering: stable sort of (popc, canonical index)
+  DevBuf<uint32_t> popc_alt(size_t(nc), s), lidx(size_t(nc), s), lidx_alt(size_t(nc), s);
+  uint32_t* sp = nullptr;
+  uint32_t* li = nullptr;
+  radix_sort<uint32_t>(popc.p, popc_alt.p, nullptr, lidx.p, lidx_alt.p, true, nc,
+                       bits_for(uint32_t(ell)), &sp, &li, s, nullptr);
+  DevBuf<uint32_t> loff(size_t(ell) + 2, s);
+  launch_layer_offsets(sp, nc, ell, loff.p, s);
+  uint32_t* hoff = static_cast<uint32_t*>(host_stage((ell + 2) * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(hoff, loff.p, (ell + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> h_off(hoff, hoff + ell + 2);
+  DevBuf<uint64_t> lkeys(size_t(nc) * W, s);
+  launch_gather_rows(cellbuf.p, li, nc, W, lkeys.p, s);
+  DevBuf<uint16_t> llcp(size_t(nc), s);
+  launch_gather_u16(lcp.p, li, nc, llcp.p, s);
+  tm.mark();  // 4: layers
+  // ---- a5 dictionary: per-layer prefix index sizes
+  const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 2;
+  std::vector<uint8_t> h_bits(ell + 1);
+  std::vector<uint64_t> h_base(ell + 1);
+  uint64_t tot = 0;
+  for (int p = 0; p <= ell; ++p) {
+    const uint64_t sz = h_off[p + 1] - h_off[p];
+    int b = 0;
+    if (o.dict_kind == CG_DICT_SORTED)
+      while (b < 28 && (sz >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
+    h_bits[p] = uint8_t(b);
+    h_base[p] = tot;
+    tot += (uint64_t(1) << b) + 1;
+  }
+  DevBuf<uint8_t> tbits(size_t(ell) + 1, s);
+  DevBuf<uint64_t> tbase(size_t(ell) + 1, s);
+  DevBuf<uint32_t> T(size_t(tot), s);
+  CG_CUDA(cudaMemcpyAsync(tbits.p, h_bits.data(), h_bits.size(), cudaMemcpyHostToDevice, s));
+  CG_CUDA(cudaMemcpyAsync(tbase.p, h_base.data(), h_base.size() * 8, cudaMemcpyHostToDevice, s));
+  DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, W, ell, nc};
+  launch_build_prefix_index(dv, sp, T.p, s);
+  tm.mark();  // 5: dict
+  // ---- a6 probes + a7 warp-aggregated append
+  DevBuf<unsigned long long> ctr(2, s);
+  uint64_t cap = std::max<uint64_t>(4 * uint64_t(nc), 1 << 16);
+  DevBuf<uint64_t> eb(cap, s);
+  unsigned long long* hc = static_cast<unsigned long long*>(host_stage(2 * sizeof(unsigned long long)));
+  int reruns = 0;
+  uint64_t m = 0, issued = 0;
+  while (true) {
+    CG_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * sizeof(unsigned long long), s));
+    launch_probe(dv, llcp.p, sp, o.lcp_prune, 0, nc, eb.p, cap, ctr.p, ctr.p + 1, s);
+    CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    m = hc[0];
+    issued = hc[1];
+    if (m <= cap) break;
+    cap = m;
+    eb.alloc(cap, s);
+    ++reruns;
+  }
+  tm.mark();  // 6: probe
+  // ---- a7 canonical sort of (i << 32 | j), then (i, j) pairs
+  uint64_t* eo = eb.p;
+  DevBuf<uint64_t> eb_alt(std::max<uint64_t>(m, 1), s);
+  if (m > 1) radix_sort<uint64_t>(eb.p, eb_alt.p, nullptr, nullptr, nullptr, false, int64_t(m), 64, &eo, nullptr, s, nullptr);
+  uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
+  launch_rotate_edges(eo, int64_t(m), eout, s);
+  tm.mark();  // 7: edges
+  // ---- outputs
+  uint64_t* cout = nullptr;
+  if (nc * 2 < n) {
+    cout = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
+    CG_CUDA(cudaMemcpyAsync(cout, cellbuf.p, size_t(nc) * W * 8, cudaMemcpyDeviceToDevice, s));
+  } else {
+    cout = cellbuf.release();
+  }
+  if (o.index_out) {
+    cg_index* ix = new cg_index();
+    ix->keys = lkeys.release();
+    if (li == lidx.p) ix->idx = lidx.release();
+    else ix->idx = lidx_alt.release();
+    ix->layer_off = loff.release();
+    ix->T = T.release();
+    ix->tbase = tbase.release();
+    ix->tbits = tbits.release();
+    cudaGetDevice(&ix->device);
+    ix->view = DictView{ix->keys, ix->idx, ix->layer_off, ix->T, ix->tbase, ix->tbits, W, ell, nc};
+    out->index = ix;
+  }
+  CG_CUDA(cudaStreamSynchronize(s));
+  out->cells = cout;
+  out->n_cells = nc;
+  out->edges = reinterpret_cast<uint32_t*>(eout);
+  out->n_edges = int64_t(m);
+  if (st) {
+    st->n_cells = nc;
+    st->n_edges = int64_t(m);
+    st->logical_probes = nc * int64_t(ell);
+    st->issued_probes = int64_t(issued);
+    st->sort_passes = sst.passes;
+    st->probe_reruns = reruns;
+  }
+}
+
+static void fill_stats(const StageTimer& tm, int64_t n, cg_stats* st) {
+  if (!st) return;
+  st->n_in = n;
+  st->us_pack = tm.us(0, 1);
+  st->us_sort = tm.us(1, 2);
+  st->us_dedupe = tm.us(2, 3);
+  st->us_layers = tm.us(3, 4);
+  st->us_dict = tm.us(4, 5);
+  st->us_probe = tm.us(5, 6);
+  st->us_edges = tm.us(6, 7);
+  st->us_total = tm.us(0, 7);
+}
+
+static int finish(int rc, const Built& b, cg_cells* cells, cg_edges* edges, const cg_opts& o,
+                  int ell) {
+  if (rc == CG_OK) {
+    cells->words = b.cells;
+    cells->n_cells = b.n_cells;
+    cells->ell = ell;
+    cells->words_per_cell = (ell + 63) / 64;
+    edges->ij = b.edges;
+    edges->n_edges = b.n_edges;
+    if (o.index_out) *o.index_out = b.index;
+  }
+  return rc;
+}
+
+static int validate_common(int64_t n, int32_t ell, const void* p, cg_cells* cells, cg_edges* edges) {
+  if (!cells || !edges) throw CgError{CG_EINVAL, "cells/edges out-pointers must not be NULL"};
+  if (!p) throw CgError{CG_EINVAL, "input pointer is NULL"};
+  if (n < 1) throw CgError{CG_EINVAL, "n must be >= 1"};
+  if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+  if (n > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n must be < 2^32"};
+  return CG_OK;
+}
+
+static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, int32_t ell,
+                       const cg_opts* o_in, cg_cells* cells, cg_edges* edges) {
+  if (cells) std::memset(cells, 0, sizeof(*cells));
+  if (edges) std::memset(edges, 0, sizeof(*edges));
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  if (o.index_out) *o.index_out = nullptr;
+  Built b;
+  try {
+    validate_common(n, ell, vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words),
+                    cells, edges);
+    if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH)
+      throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
+    check_arch();
+    check_device_ptr(vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words), "input");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    StageTimer tm;
+    tm.start(o.stats != nullptr, s);  // 0
+    DevBuf<uint32_t> flags(4, s);
+    CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
+    DevBuf<uint64_t> keys(size_t(n) * W, s);
+    if (vecs) {
+      launch_pack(vecs, n, ell, keys.p, flags.p, s);
+    } else {
+      CG_CUDA(cudaMemcpyAsync(keys.p, words, size_t(n) * W * 8, cudaMemcpyDeviceToDevice, s));
+      launch_check_pad(keys.p, n, ell, flags.p, s);
+    }
+    tm.mark();  // 1: pack
+    build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b);
+    fill_stats(tm, n, o.stats);
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (b.cells) dev_free(b.cells, nullptr);
+    if (b.edges) dev_free(b.edges, nullptr);
+    if (b.index) cg_index_free(b.index);
+    if (cells) std::memset(cells, 0, sizeof(*cells));
+    if (edges) std::memset(edges, 0, sizeof(*edges));
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return CG_ECUDA;
+  }
+  return finish(CG_OK, b, cells, edges, o, ell);
+}
+
+}  // namespace cgk
+
+using namespace cgk;
+
+extern "C" {
+
+void cg_opts_init(cg_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dict_kind = CG_DICT_SORTED;
+  o->lcp_prune = 1;
+  o->bucket_log2 = -1;
+}
+
+int cg_build(const uint8_t* vecs, int64_t n, int32_t ell, cg_cells* cells, cg_edges* edges) {
+  return build_entry(vecs, nullptr, n, ell, nullptr, cells, edges);
+}
+
+int cg_build_ex(const uint8_t* vecs, int64_t n, int32_t ell, const cg_opts* o, cg_cells* cells,
+                cg_edges* edges) {
+  return build_entry(vecs, nullptr, n, ell, o, cells, edges);
+}
+
+int cg_build_packed_ex(const uint64_t* words, int64_t n, int32_t ell, const cg_opts* o,
+                       cg_cells* cells, cg_edges* edges) {
+  return build_entry(nullptr, words, n, ell, o, cells, edges);
+}
+
+int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* o_in,
+                  uint64_t** h_cells, int64_t* n_cells, uint32_t** h_edges, int64_t* n_edges) {
+  if (h_cells) *h_cells = nullptr;
+  if (h_edges) *h_edges = nullptr;
+  if (n_cells) *n_cells = 0;
+  if (n_edges) *n_edges = 0;
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  if (o.index_out) *o.index_out = nullptr;
+  uint64_t* hc = nullptr;
+  uint32_t* he = nullptr;
+  Built b;
+  try {
+    if (!h_vecs || !h_cells || !h_edges || !n_cells || !n_edges)
+      throw CgError{CG_EINVAL, "NULL pointer argument"};
+    cg_cells dummy_c;
+    cg_edges dummy_e;
+    validate_common(n, ell, h_vecs, &dummy_c, &dummy_e);
+    check_arch();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    StageTimer tm;
+    tm.start(o.stats != nullptr, s);
+    DevBuf<uint32_t> flags(4, s);
+    CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
+    DevBuf<uint64_t> keys(size_t(n) * W, s);
+    // H2D in row chunks, each packed as soon as it lands (copy/compute overlap
+    // through two staging buffers and a copy stream).
+    const int64_t row_bytes = ell;
+    const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(64) << 20) / row_bytes);
+    DevBuf<uint8_t> stage[2];
+    const int64_t nchunk_rows = std::min<int64_t>(chunk_rows, n);
+    stage[0].alloc(size_t(nchunk_rows * row_bytes), s);
+    stage[1].alloc(size_t(nchunk_rows * row_bytes), s);
+    cudaStream_t cs;
+    CG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t ev_copied[2], ev_packed[2];
+    for (int i = 0; i < 2; ++i) {
+      CG_CUDA(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&ev_packed[i], cudaEventDisableTiming));
+    }
+    // the stage buffers were allocated on s: make the copy stream wait for that
+    CG_CUDA(cudaEventRecord(ev_packed[0], s));
+    CG_CUDA(cudaEventRecord(ev_packed[1], s));
+    int64_t r0 = 0;
+    int k = 0;
+    while (r0 < n) {
+      const int64_t r1 = std::min<int64_t>(n, r0 + chunk_rows);
+      const int sb = k & 1;
+      CG_CUDA(cudaStreamWaitEvent(cs, ev_packed[sb], 0));
+      CG_CUDA(cudaMemcpyAsync(stage[sb].p, h_vecs + r0 * row_bytes, size_t((r1 - r0) * row_bytes),
+                              cudaMemcpyHostToDevice, cs));
+      CG_CUDA(cudaEventRecord(ev_copied[sb], cs));
+      CG_CUDA(cudaStreamWaitEvent(s, ev_copied[sb], 0));
+      launch_pack(stage[sb].p, r1 - r0, ell, keys.p + r0 * W, flags.p, s);
+      CG_CUDA(cudaEventRecord(ev_packed[sb], s));
+      r0 = r1;
+      ++k;
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(ev_copied[i]);
+      cudaEventDestroy(ev_packed[i]);
+    }
+    cudaStreamDestroy(cs);
+    stage[0].reset();
+    stage[1].reset();
+    tm.mark();  // 1: H2D + pack
+    build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b);
+    fill_stats(tm, n, o.stats);
+    const size_t cb = size_t(b.n_cells) * W * 8, ebytes = size_t(b.n_edges) * 8;
+    hc = static_cast<uint64_t*>(host_pool_alloc(cb));
+    he = static_cast<uint32_t*>(host_pool_alloc(ebytes));
+    CG_CUDA(cudaMemcpyAsync(hc, b.cells, cb, cudaMemcpyDeviceToHost, s));
+    if (ebytes) CG_CUDA(cudaMemcpyAsync(he, b.edges, ebytes, cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    dev_free(b.cells, s);
+    dev_free(b.edges, s);
+    b.cells = nullptr;
+    b.edges = nullptr;
+    *h_cells = hc;
+    *h_edges = he;
+    *n_cells = b.n_cells;
+    *n_edges = b.n_edges;
+    if (o.index_out) *o.index_out = b.index;
+    else if (b.index) cg_index_free(b.index);
+    return CG_OK;
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (b.cells) dev_free(b.cells, nullptr);
+    if (b.edges) dev_free(b.edges, nullptr);
+    if (b.index) cg_index_free(b.index);
+    host_pool_free(hc);
+    host_pool_free(he);
+    return e.code;
+  }
+}
+
+void cg_host_free(void* p) { host_pool_free(p); }
+
+int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_idx,
+             int32_t* nbr_idx, cg_stream_t s) {
+  try {
+    if (!idx) throw CgError{CG_EINVAL, "NULL index"};
+    if (nq < 0) throw CgError{CG_EINVAL, "nq < 0"};
+    if (nq == 0) return CG_OK;
+    if (!q || !self_idx || !nbr_idx) throw CgError{CG_EINVAL, "NULL query/output pointer"};
+    launch_query(idx->view, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
+    return CG_OK;
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  }
+}
+
+int cg_index_info(const cg_index* idx, int64_t* n_cells, int32_t* ell) {
+  if (!idx) return CG_EINVAL;
+  if (n_cells) *n_cells = idx->view.n_cells;
+  if (ell) *ell = idx->view.ell;
+  return CG_OK;
+}
+
+int cg_set_allocator(void* (*alloc)(size_t, cg_stream_t, void*),
+                     void (*dealloc)(void*, cg_stream_t, void*), void* ctx) {
+  if ((alloc == nullptr) != (dealloc == nullptr)) return CG_EINVAL;
+  g_alloc = alloc;
+  g_dealloc = dealloc;
+  g_alloc_ctx = alloc ? ctx : nullptr;
+  return CG_OK;
+}
+
+void cg_cells_free(cg_cells* c) {
+  if (!c) return;
+  if (c->words) dev_free(c->words, nullptr);
+  std::memset(c, 0, sizeof(*c));
+}
+
+void cg_edges_free(cg_edges* e) {
+  if (!e) return;
+  if (e->ij) dev_free(e->ij, nullptr);
+  std::memset(e, 0, sizeof(*e));
+}
+
+void cg_index_free(cg_index* idx) {
+  if (!idx) return;
+  dev_free(idx->keys, nullptr);
+  dev_free(idx->idx, nullptr);
+  dev_free(idx->layer_off, nullptr);
+  dev_free(idx->T, nullptr);
+  dev_free(idx->tbase, nullptr);
+  dev_free(idx->tbits, nullptr);
+  delete idx;
+}
+
+const char* cg_strerror(int code) {
+  switch (code) {
+    case CG_OK: return "ok";
+    case CG_EINVAL: return "invalid argument";
+    case CG_EINPUT: return "input byte not in {0,1} / pad bit set";
+    case CG_ENOMEM: return "out of memory";
+    case CG_ECUDA: return "CUDA error";
+    case CG_ETOOBIG: return "too many vectors (n >= 2^32)";
+    case CG_EARCH: return "unsupported GPU architecture (need sm_100)";
+    case CG_ENOTIMPL: return "not implemented";
+    default: return "unknown error";
+  }
+}
+
+const char* cg_last_error(void) { return g_last_error.c_str(); }
+
+int cg_version(void) { return (0 << 16) | 1; }
+
+int cg_dist_local(const uint8_t*, int64_t, int32_t, const cg_opts*, cg_cells* run) {
+  if (run) std::memset(run, 0, sizeof(*run));
+  set_last_error("cg_dist_local: not implemented yet");
+  return CG_ENOTIMPL;
+}
+
+int cg_dist_merge_probe(const uint64_t*, const int64_t*, int32_t, int64_t, int32_t, int32_t,
+                        const cg_opts*, cg_cells* table, cg_edges* local_edges) {
+  if (table) std::memset(table, 0, sizeof(*table));
+  if (local_edges) std::memset(local_edges, 0, sizeof(*local_edges));
+  set_last_error("cg_dist_merge_probe: not implemented yet");
+  return CG_ENOTIMPL;
+}
+
+int cg_dist_finalize(const uint32_t*, const int64_t*, int32_t, int64_t, const cg_opts*,
+                     cg_edges* edges) {
+  if (edges) std::memset(edges, 0, sizeof(*edges));
+  set_last_error("cg_dist_finalize: not implemented yet");
+  return CG_ENOTIMPL;
+}
+
+}  // extern "C"

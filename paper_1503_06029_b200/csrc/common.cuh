@@ -1,0 +1,160 @@
+// common.cuh -- shared plumbing of the sm_100a cell-graph kernels (product path).
+// Nothing here is shared with oracle/ (DESIGN "Oracle independence").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/cg.h"
+
+namespace cgk {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- errors
+struct CgError {
+  int code;
+  std::string msg;
+};
+void set_last_error(const std::string& s);
+
+#define CG_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      throw ::cgk::CgError{e_ == cudaErrorMemoryAllocation ? CG_ENOMEM : CG_ECUDA, \
+                           std::string(#call) + ": " + cudaGetErrorString(e_)};    \
+    }                                                                              \
+  } while (0)
+
+#define CG_LAUNCH_CHECK() CG_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- allocation
+void* dev_alloc(size_t bytes, cudaStream_t s);  // throws CG_ENOMEM
+void dev_free(void* p, cudaStream_t s);
+
+// RAII device buffer, stream-ordered free.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    reset();
+    s = st;
+    n = count;
+    p = static_cast<T*>(dev_alloc(count ? count * sizeof(T) : 16, st));
+  }
+  T* release() {
+    T* r = p;
+    p = nullptr;
+    n = 0;
+    return r;
+  }
+  void reset() {
+    if (p) dev_free(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { reset(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { reset(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+};
+
+// pinned host staging for small read-backs (per thread, grows)
+void* host_stage(size_t bytes);
+
+int num_sms();
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back status word: [flag:2 | epoch:30 | value:32].
+// flag 1 = tile aggregate only, 2 = inclusive prefix.  Epochs make a status
+// buffer reusable across passes without clearing it (cleared once per sort).
+__device__ __forceinline__ uint64_t lb_pack(uint32_t flag, uint32_t epoch, uint32_t value) {
+  return (uint64_t(flag) << 62) | (uint64_t(epoch & 0x3fffffffu) << 32) | value;
+}
+
+// Publish `agg` for (tile, slot) and return the exclusive prefix over all
+// earlier tiles of that slot.  Tiles are numbered in start order (atomic
+// ticket), so every tile waited on has already published its aggregate.
+__device__ __forceinline__ uint32_t lookback(uint64_t* status, int64_t tile, int nslots, int slot,
+                                             uint32_t agg, uint32_t epoch) {
+  uint64_t* me = status + tile * nslots + slot;
+  if (tile == 0) {
+    st_relaxed_u64(me, lb_pack(2, epoch, agg));
+    return 0;
+  }
+  st_relaxed_u64(me, lb_pack(1, epoch, agg));
+  uint32_t excl = 0;
+  int64_t j = tile - 1;
+  const uint32_t ep = epoch & 0x3fffffffu;
+  while (true) {
+    uint64_t s = ld_relaxed_u64(status + j * nslots + slot);
+    uint32_t flag = uint32_t(s >> 62);
+    uint32_t sep = uint32_t(s >> 32) & 0x3fffffffu;
+    if (flag == 0 || sep != ep) continue;  // not yet published in this epoch
+    excl += uint32_t(s);
+    if (flag == 2) break;
+    --j;
+  }
+  st_relaxed_u64(me, lb_pack(2, epoch, excl + agg));
+  return excl;
+}
+
+// Block-wide exclusive scan of one u32 per thread (blockDim.x multiple of 32,
+// <= 1024).  `tmp` needs 33 words of shared memory.  Returns the total in *total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = lane < nw ? tmp[lane] : 0;
+    uint32_t u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, u, o);
+      if (lane >= o) u += y;
+    }
+    if (lane < nw) tmp[lane] = u - t;
+    if (lane == 31) tmp[32] = u;
+  }
+  __syncthreads();
+  uint32_t r = tmp[wid] + x - v;
+  *total = tmp[32];
+  __syncthreads();
+  return r;
+}
+
+}  // namespace cgk

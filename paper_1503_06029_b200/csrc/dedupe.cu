@@ -1,0 +1,134 @@
+// dedupe.cu -- a3: duplicate removal and compaction into the cell table.
+//
+// "During this step we also remove all duplicates in X"; X may be a
+// multiset and only unique pairs may be output.  Over the
+// canonically sorted rows, row g starts a new cell iff g == 0 or it differs
+// from row g-1.  Flags are counted per warp with __ballot_sync/__popc,
+// scanned per block, and the block's base is found by decoupled look-back,
+// so cells are written in one pass straight to their final position.
+// The same pass records per cell
+//   popc[c] = popcount of the cell (its layer, a4) and
+//   lcp[c]  = number of leading bits shared with the next cell (0xffff for
+//             the last cell): the exact probe-pruning bound of a6.
+#include "kernels.cuh"
+
+namespace cgk {
+namespace {
+
+constexpr int kDedupThreads = 256;
+constexpr int kDedupIPT = 8;  // rows per thread (contiguous run)
+
+template <int WC>
+struct Row {
+  // compile-time W when WC > 0, else runtime
+  __device__ static __forceinline__ bool equal(const uint64_t* a, const uint64_t* b, int W) {
+    const int n = WC > 0 ? WC : W;
+    for (int w = 0; w < n; ++w)
+      if (a[w] != b[w]) return false;
+    return true;
+  }
+  __device__ static __forceinline__ int lcp(const uint64_t* a, const uint64_t* b, int W) {
+    const int n = WC > 0 ? WC : W;
+    for (int w = 0; w < n; ++w) {
+      const uint64_t x = a[w] ^ b[w];
+      if (x) return 64 * w + __clzll(x);
+    }
+    return 64 * n;
+  }
+  __device__ static __forceinline__ uint32_t popc(const uint64_t* a, int W) {
+    const int n = WC > 0 ? WC : W;
+    uint32_t c = 0;
+    for (int w = 0; w < n; ++w) c += __popcll(a[w]);
+    return c;
+  }
+};
+
+template <int WC>
+__global__ void __launch_bounds__(kDedupThreads)
+    k_dedupe(const uint64_t* __restrict__ sorted, int64_t n, int W, uint64_t* __restrict__ cells,
+             uint32_t* __restrict__ popc, uint16_t* __restrict__ lcp_out, uint64_t* status,
+             uint32_t* tile_counter, uint32_t* n_cells) {
+  constexpr int TILE = kDedupThreads * kDedupIPT;
+  constexpr int NWARP = kDedupThreads / 32;
+  __shared__ uint32_t s_warp[NWARP];
+  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  // warp `wid` owns rows [wb, wb + 32*IPT): step i covers 32 consecutive rows
+  const int64_t wb = tile * TILE + int64_t(wid) * 32 * kDedupIPT;
+  using R = Row<WC>;
+  uint32_t ball[kDedupIPT];
+  uint32_t wcount = 0;
+#pragma unroll
+  for (int i = 0; i < kDedupIPT; ++i) {
+    const int64_t g = wb + i * 32 + lane;
+    bool f = false;
+    if (g < n) f = (g == 0) || !R::equal(sorted + g * W, sorted + (g - 1) * W, W);
+    ball[i] = __ballot_sync(kFull, f);
+    wcount += __popc(ball[i]);
+  }
+  if (lane == 0) s_warp[wid] = wcount;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < NWARP; ++w) {
+      const uint32_t c = s_warp[w];
+      s_warp[w] = run;
+      run += c;
+    }
+    const uint32_t base = lookback(status, tile, 1, 0, run, 1);
+    s_base = base;
+    if (tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
+  }
+  __syncthreads();
+  uint32_t c0 = s_base + s_warp[wid];  // first cell index of this warp's flags
+  const uint32_t lt = lanemask_lt();
+  const int nw = WC > 0 ? WC : W;
+#pragma unroll
+  for (int i = 0; i < kDedupIPT; ++i) {
+    const int64_t g = wb + i * 32 + lane;
+    const uint32_t b = ball[i];
+    if (g < n) {
+      const uint64_t* row = sorted + g * W;
+      // cell of row g = (flags at rows <= g) - 1
+      const uint32_t cell = c0 + __popc(b & lt) + ((b >> lane) & 1) - 1;
+      if ((b >> lane) & 1) {
+        for (int w = 0; w < nw; ++w) cells[int64_t(cell) * nw + w] = row[w];
+        popc[cell] = R::popc(row, W);
+      }
+      // last row of its run: lcp with the next distinct row (a6 pruning bound)
+      if (g + 1 >= n) {
+        lcp_out[cell] = 0xffff;
+      } else {
+        const uint64_t* nxt = row + W;
+        if (!R::equal(row, nxt, W)) lcp_out[cell] = uint16_t(R::lcp(row, nxt, W));
+      }
+    }
+    c0 += __popc(b);
+  }
+}
+
+}  // namespace
+
+void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, uint32_t* popc,
+                   uint16_t* lcp, uint32_t* n_cells, cudaStream_t s) {
+  constexpr int TILE = kDedupThreads * kDedupIPT;
+  const int64_t tiles = (n + TILE - 1) / TILE;
+  DevBuf<uint64_t> status(size_t(tiles), s);
+  DevBuf<uint32_t> counter(1, s);
+  CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint64_t), s));
+  CG_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(uint32_t), s));
+  const unsigned g = unsigned(tiles);
+  switch (W) {
+    case 1: k_dedupe<1><<<g, kDedupThreads, 0, s>>>(sorted, n, W, cells, popc, lcp, status.p, counter.p, n_cells); break;
+    case 2: k_dedupe<2><<<g, kDedupThreads, 0, s>>>(sorted, n, W, cells, popc, lcp, status.p, counter.p, n_cells); break;
+    case 4: k_dedupe<4><<<g, kDedupThreads, 0, s>>>(sorted, n, W, cells, popc, lcp, status.p, counter.p, n_cells); break;
+    default: k_dedupe<0><<<g, kDedupThreads, 0, s>>>(sorted, n, W, cells, popc, lcp, status.p, counter.p, n_cells); break;
+  }
+  CG_LAUNCH_CHECK();
+}
+
+}  // namespace cgk

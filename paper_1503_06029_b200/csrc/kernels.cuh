@@ -1,0 +1,82 @@
+// kernels.cuh -- host-side launchers of the cell-graph kernels (internal API).
+#pragma once
+
+#include "common.cuh"
+
+namespace cgk {
+
+// ---------------------------------------------------------------- a1 pack
+// uint8[n][ell] (0/1 bytes) -> u64[n][W] MSB-first; *err |= 1 on a byte > 1.
+void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
+                 cudaStream_t s);
+// packed input: copy + check pad bits (err |= 1 if a pad bit is set)
+void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s);
+
+// ---------------------------------------------------------------- radix engine (a2, a4, a7)
+struct SortStats {
+  int passes = 0;
+};
+
+// Stable LSD sort of n keys (K = uint32_t or uint64_t) on bits [0, key_bits),
+// 8-bit digits, constant digits skipped.  Optional u32 payload: vals_in ==
+// nullptr with want_vals means "payload = original index".  Buffers are
+// ping-ponged; on return *keys_out / *vals_out point to the sorted data
+// (one of the given buffers).  Host-synchronising (digit histogram read-back).
+template <class K>
+void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, uint32_t* vals_alt,
+                bool want_vals, int64_t n, int key_bits, K** keys_out, uint32_t** vals_out,
+                cudaStream_t s, SortStats* st);
+
+// Canonical sort of packed rows u64[n][W] (W >= 2): LSD over words W-1..0
+// on (word, u32 index) pairs, then a row gather into `sorted` (u64[n][W]).
+void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
+                         cudaStream_t s, SortStats* st);
+
+// ---------------------------------------------------------------- a3 dedupe + compaction
+// sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],
+// lcp[n_c] (leading equal bits with the next cell; 0xffff for the last),
+// *n_cells (device u32).
+void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, uint32_t* popc,
+                   uint16_t* lcp, uint32_t* n_cells, cudaStream_t s);
+
+// ---------------------------------------------------------------- a4/a5 layers + dictionary
+struct DictView {
+  const uint64_t* keys;       // layer-major cell rows u64[n_c][W]
+  const uint32_t* idx;        // canonical index of each layer-major row
+  const uint32_t* layer_off;  // [ell + 2]
+  const uint32_t* T;          // prefix index entries
+  const uint64_t* tbase;      // [ell + 1] offset of layer p's prefix table in T
+  const uint8_t* tbits;       // [ell + 1] prefix bits b_p (0 = no prefix index)
+  int W;
+  int ell;
+  int64_t n_cells;
+};
+
+// layer_off[p] = first position of popcount p in sorted_popc (p in [0, ell+1]).
+void launch_layer_offsets(const uint32_t* sorted_popc, int64_t nc, int ell, uint32_t* layer_off,
+                          cudaStream_t s);
+// out rows[j] = in rows[idx[j]] (W words per row); lcp_out[j] = lcp_in[idx[j]].
+void launch_gather_rows(const uint64_t* in, const uint32_t* idx, int64_t n, int W, uint64_t* out,
+                        cudaStream_t s);
+void launch_gather_u16(const uint16_t* in, const uint32_t* idx, int64_t n, uint16_t* out,
+                       cudaStream_t s);
+// T entries of every layer (sizes precomputed in tbase/tbits).
+void launch_build_prefix_index(const DictView& d, const uint32_t* sorted_popc, uint32_t* T,
+                               cudaStream_t s);
+
+// ---------------------------------------------------------------- a6/a7 probes + edges
+// For each layer-major cell j (popcount p), each bit k (<= lcp if lcp_prune)
+// with V(k) = 0: look up V | e_k in layer p+1.  Hits are appended with
+// warp-aggregated atomics as u64 (i << 32 | j) into edges[0..cap); *count
+// gets the total (may exceed cap -> rerun with a bigger buffer).
+void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
+                  int lcp_prune, int64_t j_lo, int64_t j_hi, uint64_t* edges, uint64_t cap,
+                  unsigned long long* count, unsigned long long* issued, cudaStream_t s);
+// (i << 32 | j) -> u32 pair (i, j) little-endian.
+void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- cg_query
+void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,
+                  int32_t* nbr_idx, cudaStream_t s);
+
+}  // namespace cgk

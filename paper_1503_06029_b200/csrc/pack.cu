@@ -1,0 +1,121 @@
+// pack.cu -- a1: bit-pack the cell signatures.
+//
+// Input: uint8[n][ell], byte k of row r = x_r(k) in {0,1} ("the i-th bit of
+// v_P is 1 iff P satisfies the inequality c_i"; the paper stores each
+// vector "as a continuous array of bytes").  Output: u64[n][W],
+// W = ceil(ell/64), bit k at word k/64, bit position 63-(k%64) (MSB-first),
+// so unsigned word-by-word comparison is the canonical order (DESIGN G1) and
+// pad bits are zero (G6).  Any byte > 1 raises *err (CG_EINPUT, G5).
+//
+// HBM-streaming kernel: one thread per output word reads the word's <= 64
+// input bytes with 16-byte (ell % 16 == 0), 8-byte (ell % 8 == 0) or 1-byte
+// loads, turns each group of 8 bytes into 8 MSB-first bits with one multiply
+// (x * 0x8040201008040201 >> 56 places byte j at bit 7-j: the 64 partial
+// products land on distinct bit positions, so there are no carries), and
+// writes the word.  Consecutive threads read consecutive 64-byte spans.
+#include "kernels.cuh"
+
+namespace cgk {
+namespace {
+
+__device__ __forceinline__ uint32_t bits8_msb(uint64_t x) {
+  return uint32_t((x * 0x8040201008040201ull) >> 56);
+}
+
+constexpr uint64_t kHi7 = 0xfefefefefefefefeull;
+
+template <int VEC>
+__global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, int64_t n,
+                                              int ell, int W, uint64_t* __restrict__ keys,
+                                              uint32_t* __restrict__ err) {
+  const int64_t total = n * W;
+  uint64_t bad = 0;
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = g / W;
+    const int w = int(g - r * W);
+    const int len = min(64, ell - 64 * w);
+    const uint8_t* src = vecs + r * ell + 64 * w;
+    uint64_t word = 0;
+    if (VEC == 16) {
+      const uint4* p = reinterpret_cast<const uint4*>(src);
+      uint4 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (16 * c < len) v[c] = __ldcs(p + c);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (16 * c < len) {
+          const uint64_t lo = (uint64_t(v[c].y) << 32) | v[c].x;
+          const uint64_t hi = (uint64_t(v[c].w) << 32) | v[c].z;
+          bad |= (lo | hi) & kHi7;
+          word |= uint64_t(bits8_msb(lo)) << (56 - 16 * c);
+          word |= uint64_t(bits8_msb(hi)) << (48 - 16 * c);
+        }
+      }
+    } else if (VEC == 8) {
+      const uint2* p = reinterpret_cast<const uint2*>(src);
+      uint2 v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (8 * c < len) v[c] = __ldcs(p + c);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (8 * c < len) {
+          const uint64_t x = (uint64_t(v[c].y) << 32) | v[c].x;
+          bad |= x & kHi7;
+          word |= uint64_t(bits8_msb(x)) << (56 - 8 * c);
+        }
+      }
+    } else {
+      for (int k = 0; k < len; ++k) {
+        const uint8_t b = src[k];
+        bad |= b & 0xfe;
+        word |= uint64_t(b & 1) << (63 - k);
+      }
+    }
+    keys[g] = word;
+  }
+  if (bad) atomicOr(err, 1u);
+}
+
+__global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W, uint64_t pad,
+                            uint32_t* __restrict__ err) {
+  uint64_t bad = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x)
+    bad |= words[r * W + W - 1] & pad;
+  if (bad) atomicOr(err, 1u);
+}
+
+}  // namespace
+
+void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
+                 cudaStream_t s) {
+  const int W = (ell + 63) / 64;
+  const int64_t total = n * W;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  blocks = std::min<int64_t>(blocks, int64_t(num_sms()) * 8);
+  if (blocks < 1) blocks = 1;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(vecs);
+  if (ell % 16 == 0 && a % 16 == 0) {
+    k_pack<16><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+  } else if (ell % 8 == 0 && a % 8 == 0) {
+    k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+  } else {
+    k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+  }
+  CG_LAUNCH_CHECK();
+}
+
+void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s) {
+  if (ell % 64 == 0) return;
+  const int W = (ell + 63) / 64;
+  const uint64_t pad = ~uint64_t(0) >> (ell % 64);
+  int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8);
+  k_check_pad<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(words, n, W, pad, err);
+  CG_LAUNCH_CHECK();
+}
+
+}  // namespace cgk
