@@ -81,6 +81,9 @@ typedef struct {
   int64_t issued_probes;  /* lookups actually issued (0->1 flips, <= lcp when pruning) */
   int32_t sort_passes;    /* radix passes executed by the cell sort */
   int32_t probe_reruns;   /* probe stage reruns because the edge buffer was too small */
+  int64_t kernel_launches; /* CUDA kernels this library launched for the call */
+  double us_host_alloc;    /* host time spent inside device allocation calls */
+  int64_t n_allocs;        /* device allocations made for the call */
 } cg_stats;
 
 enum {
@@ -93,7 +96,8 @@ typedef struct {
   int32_t dict_kind;    /* CG_DICT_* */
   int32_t lcp_prune;    /* 1: probe bit k only if k <= lcp(V_i, V_{i+1}) (exact, DESIGN a6) */
   int32_t bucket_log2;  /* prefix index: target log2(cells per bucket); -1 = default (2) */
-  int32_t reserved;
+  int32_t sort_kind;    /* 0 = auto (MSD prefix buckets + shared-memory sort for ell <= 128,
+                           full LSD fallback), 1 = full LSD only */
   cg_index** index_out; /* if non-NULL, receives the dictionary (release with cg_index_free) */
   cg_stats* stats;      /* if non-NULL, stage times and counters */
 } cg_opts;

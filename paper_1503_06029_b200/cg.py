@@ -46,13 +46,15 @@ class cg_stats(ctypes.Structure):
                  "us_probe", "us_edges")] + \
                [(k, ctypes.c_int64) for k in
                 ("n_in", "n_cells", "n_edges", "logical_probes", "issued_probes")] + \
-               [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32)]
+               [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32),
+                ("kernel_launches", ctypes.c_int64), ("us_host_alloc", ctypes.c_double),
+                ("n_allocs", ctypes.c_int64)]
 
 
 class cg_opts(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("dict_kind", ctypes.c_int32),
                 ("lcp_prune", ctypes.c_int32), ("bucket_log2", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("index_out", ctypes.c_void_p),
+                ("sort_kind", ctypes.c_int32), ("index_out", ctypes.c_void_p),
                 ("stats", ctypes.POINTER(cg_stats))]
 
 
@@ -209,7 +211,10 @@ class BuildResult:
     index: Index | None = None
 
 
-def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats):
+SORT_KINDS = {"auto": 0, "lsd": 1}
+
+
+def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats, sort_kind="auto"):
     L = lib()
     o = cg_opts()
     L.cg_opts_init(ctypes.byref(o))
@@ -217,6 +222,7 @@ def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats):
     o.dict_kind = DICT_KINDS[dict_kind] if isinstance(dict_kind, str) else int(dict_kind)
     o.lcp_prune = int(bool(lcp_prune))
     o.bucket_log2 = int(bucket_log2)
+    o.sort_kind = SORT_KINDS[sort_kind] if isinstance(sort_kind, str) else int(sort_kind)
     ih = ctypes.c_void_p()
     st = cg_stats()
     if want_index:
@@ -232,7 +238,8 @@ def _stats_dict(st: cg_stats) -> dict:
 
 def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
           dict_kind="sorted", lcp_prune: bool = True, bucket_log2: int = -1,
-          want_index: bool = False, want_stats: bool = False) -> BuildResult:
+          want_index: bool = False, want_stats: bool = False,
+          sort_kind="auto") -> BuildResult:
     """cg_build_ex on a CUDA uint8 tensor [n, ell] of 0/1 bytes."""
     if not isinstance(vecs, torch.Tensor) or vecs.dim() != 2:
         raise CgError(CG_EINVAL, "vecs must be a 2-D tensor [n, ell]")
@@ -243,7 +250,8 @@ def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
     vecs = vecs.contiguous()
     n, ell = vecs.shape
     stream = stream or torch.cuda.current_stream(vecs.device)
-    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats)
+    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats,
+                      sort_kind)
     c, e = cg_cells(), cg_edges()
     with torch.cuda.device(vecs.device):
         _check(lib().cg_build_ex(ctypes.c_void_p(vecs.data_ptr()), n, ell, ctypes.byref(o),

@@ -6,6 +6,7 @@
 // See DESIGN.md for the data layout and the paper passages of each step.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -23,6 +24,7 @@ struct cg_index {
   uint32_t* T = nullptr;
   uint64_t* tbase = nullptr;
   uint8_t* tbits = nullptr;
+  uint32_t* F = nullptr;
   int device = 0;
 };
 
@@ -31,6 +33,8 @@ namespace cgk {
 // ---------------------------------------------------------------- errors
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
+static thread_local int64_t g_launches = 0;
+void note_launch() { ++g_launches; }
 
 // ---------------------------------------------------------------- allocator
 static void* (*g_alloc)(size_t, cg_stream_t, void*) = nullptr;
@@ -48,7 +52,30 @@ static void init_pool() {
   }
 }
 
+static thread_local double g_alloc_us = 0;
+static thread_local int64_t g_nallocs = 0;
+static void reset_counters() {
+  g_launches = 0;
+  g_alloc_us = 0;
+  g_nallocs = 0;
+}
+static void store_counters(cg_stats* st) {
+  if (!st) return;
+  st->kernel_launches = g_launches;
+  st->us_host_alloc = g_alloc_us;
+  st->n_allocs = g_nallocs;
+}
+
+struct AllocTimer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~AllocTimer() {
+    g_alloc_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    ++g_nallocs;
+  }
+};
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
+  AllocTimer at;
   void* p = nullptr;
   if (g_alloc) {
     p = g_alloc(bytes, reinterpret_cast<cg_stream_t>(s), g_alloc_ctx);
@@ -71,6 +98,106 @@ void dev_free(void* p, cudaStream_t s) {
     return;
   }
   cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------- workspace arena
+namespace {
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t top = 0;          // bytes in use at the top of the stack
+  size_t overflow = 0;     // live scratch bytes that did not fit (pool-allocated)
+  size_t peak = 0;         // high-water of top + overflow in this build
+  size_t want = 0;         // capacity to provide at the next build
+  int depth = 0;           // nested WsScope count
+  struct Blk { size_t off, size; bool freed; };
+  std::vector<Blk> stack;
+};
+constexpr int kMaxDev = 16;
+thread_local Arena g_arena[kMaxDev];
+
+Arena& cur_arena() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return g_arena[(dev >= 0 && dev < kMaxDev) ? dev : 0];
+}
+}  // namespace
+
+WsScope::WsScope() {
+  Arena& a = cur_arena();
+  if (a.depth++ > 0) return;
+  if (a.want > a.cap) {
+    if (a.base) {
+      cudaDeviceSynchronize();
+      if (g_dealloc) g_dealloc(a.base, nullptr, g_alloc_ctx);
+      else cudaFree(a.base);
+    }
+    a.base = nullptr;
+    a.cap = 0;
+    void* p = nullptr;
+    if (g_alloc) {
+      p = g_alloc(a.want, nullptr, g_alloc_ctx);
+    } else if (cudaMalloc(&p, a.want) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    if (p) {
+      a.base = static_cast<char*>(p);
+      a.cap = a.want;
+    }
+  }
+  a.top = 0;
+  a.overflow = 0;
+  a.peak = 0;
+  a.stack.clear();
+}
+
+WsScope::~WsScope() {
+  Arena& a = cur_arena();
+  if (--a.depth > 0) return;
+  if (a.peak > a.cap) a.want = a.peak + a.peak / 16;
+  a.stack.clear();
+  a.top = 0;
+}
+
+void* ws_alloc(size_t bytes, cudaStream_t s, bool* from_arena) {
+  Arena& a = cur_arena();
+  const size_t sz = (bytes + 255) & ~size_t(255);
+  if (a.depth > 0 && a.base && a.top + sz <= a.cap) {
+    void* p = a.base + a.top;
+    a.stack.push_back({a.top, sz, false});
+    a.top += sz;
+    a.peak = std::max(a.peak, a.top + a.overflow);
+    *from_arena = true;
+    return p;
+  }
+  *from_arena = false;
+  if (a.depth > 0) {
+    a.overflow += sz;
+    a.peak = std::max(a.peak, a.top + a.overflow);
+  }
+  return dev_alloc(sz, s);
+}
+
+void ws_free(void* p, cudaStream_t s, bool from_arena, size_t bytes) {
+  Arena& a = cur_arena();
+  if (!from_arena) {
+    const size_t sz = (bytes + 255) & ~size_t(255);
+    if (a.depth > 0) a.overflow -= std::min(a.overflow, sz);
+    dev_free(p, s);
+    return;
+  }
+  const size_t off = static_cast<size_t>(static_cast<char*>(p) - a.base);
+  for (size_t i = a.stack.size(); i-- > 0;) {
+    if (a.stack[i].off == off) {
+      a.stack[i].freed = true;
+      break;
+    }
+  }
+  while (!a.stack.empty() && a.stack.back().freed) {
+    a.top = a.stack.back().off;
+    a.stack.pop_back();
+  }
 }
 
 void* host_stage(size_t bytes) {
@@ -201,18 +328,28 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   // ---- a2 sort
   DevBuf<uint64_t> alt(size_t(n) * W, s);
   const uint64_t* sorted = nullptr;
-  if (W == 1) {
+  bool done = false;
+  if (W <= 2 && o.sort_kind != 1) {
+    // MSD fast path; falls back below when a prefix bucket overflows
     uint64_t* ko = nullptr;
-    radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, n, 64, &ko, nullptr, s,
-                         &sst);
+    done = sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst);
     sorted = ko;
-  } else {
-    sort_rows_multiword(keys.p, n, W, alt.p, s, &sst);
-    sorted = alt.p;
+    if (!done && ko != keys.p) std::swap(keys.p, alt.p);  // partially sorted data in keys
+  }
+  if (!done) {
+    if (W == 1) {
+      uint64_t* ko = nullptr;
+      radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, n, 64, &ko, nullptr,
+                           s, &sst);
+      sorted = ko;
+    } else {
+      sort_rows_multiword(keys.p, n, W, alt.p, s, &sst);
+      sorted = alt.p;
+    }
   }
   tm.mark();  // 2: sort
   // ---- a3 dedupe + compaction
-  DevBuf<uint64_t> cellbuf(size_t(n) * W, s);
+  DevBuf<uint64_t> cellbuf(size_t(n) * W, s, Mem::Persist);  // the output cell table
   DevBuf<uint32_t> popc(size_t(n), s);
   DevBuf<uint16_t> lcp(size_t(n), s);
   launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
@@ -225,18 +362,20 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   keys.reset();
   alt.reset();
   // ---- a4 popcount layering: stable sort of (popc, canonical index)
-  DevBuf<uint32_t> popc_alt(size_t(nc), s), lidx(size_t(nc), s), lidx_alt(size_t(nc), s);
+  // buffers that become the cg_index (when requested) outlive the build
+  const Mem ix = o.index_out ? Mem::Persist : Mem::Scratch;
+  DevBuf<uint32_t> popc_alt(size_t(nc), s), lidx(size_t(nc), s, ix), lidx_alt(size_t(nc), s, ix);
   uint32_t* sp = nullptr;
   uint32_t* li = nullptr;
   radix_sort<uint32_t>(popc.p, popc_alt.p, nullptr, lidx.p, lidx_alt.p, true, nc,
                        bits_for(uint32_t(ell)), &sp, &li, s, nullptr);
-  DevBuf<uint32_t> loff(size_t(ell) + 2, s);
+  DevBuf<uint32_t> loff(size_t(ell) + 2, s, ix);
   launch_layer_offsets(sp, nc, ell, loff.p, s);
   uint32_t* hoff = static_cast<uint32_t*>(host_stage((ell + 2) * sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(hoff, loff.p, (ell + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
   std::vector<uint32_t> h_off(hoff, hoff + ell + 2);
-  DevBuf<uint64_t> lkeys(size_t(nc) * W, s);
+  DevBuf<uint64_t> lkeys(size_t(nc) * W, s, ix);
   launch_gather_rows(cellbuf.p, li, nc, W, lkeys.p, s);
   DevBuf<uint16_t> llcp(size_t(nc), s);
   launch_gather_u16(lcp.p, li, nc, llcp.p, s);
@@ -244,8 +383,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   // ---- a5 dictionary: per-layer prefix index sizes
   const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 2;
   std::vector<uint8_t> h_bits(ell + 1);
-  std::vector<uint64_t> h_base(ell + 1);
-  uint64_t tot = 0;
+  std::vector<uint64_t> h_base(2 * (ell + 1));  // [tbase | fbase]
+  uint64_t tot = 0, ftot = 0;
   for (int p = 0; p <= ell; ++p) {
     const uint64_t sz = h_off[p + 1] - h_off[p];
     int b = 0;
@@ -254,14 +393,18 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     h_bits[p] = uint8_t(b);
     h_base[p] = tot;
     tot += (uint64_t(1) << b) + 1;
+    h_base[ell + 1 + p] = ftot;
+    ftot += std::max<uint64_t>(1, (uint64_t(1) << (b + kFilterExtra)) / 32);
   }
-  DevBuf<uint8_t> tbits(size_t(ell) + 1, s);
-  DevBuf<uint64_t> tbase(size_t(ell) + 1, s);
-  DevBuf<uint32_t> T(size_t(tot), s);
+  DevBuf<uint8_t> tbits(size_t(ell) + 1, s, ix);
+  DevBuf<uint64_t> tbase(2 * (size_t(ell) + 1), s, ix);
+  DevBuf<uint32_t> T(size_t(tot), s, ix);
+  DevBuf<uint32_t> F(size_t(ftot), s, ix);
   CG_CUDA(cudaMemcpyAsync(tbits.p, h_bits.data(), h_bits.size(), cudaMemcpyHostToDevice, s));
   CG_CUDA(cudaMemcpyAsync(tbase.p, h_base.data(), h_base.size() * 8, cudaMemcpyHostToDevice, s));
-  DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, W, ell, nc};
-  launch_build_prefix_index(dv, sp, T.p, s);
+  CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * sizeof(uint32_t), s));
+  DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, F.p, tbase.p + ell + 1, W, ell, nc};
+  launch_build_prefix_index(dv, sp, T.p, F.p, s);
   tm.mark();  // 5: dict
   // ---- a6 probes + a7 warp-aggregated append
   DevBuf<unsigned long long> ctr(2, s);
@@ -307,8 +450,10 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     ix->T = T.release();
     ix->tbase = tbase.release();
     ix->tbits = tbits.release();
+    ix->F = F.release();
     cudaGetDevice(&ix->device);
-    ix->view = DictView{ix->keys, ix->idx, ix->layer_off, ix->T, ix->tbase, ix->tbits, W, ell, nc};
+    ix->view = DictView{ix->keys, ix->idx, ix->layer_off, ix->T, ix->tbase, ix->tbits,
+                        ix->F, ix->tbase + ell + 1, W, ell, nc};
     out->index = ix;
   }
   CG_CUDA(cudaStreamSynchronize(s));
@@ -378,8 +523,10 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
       throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
     check_arch();
     check_device_ptr(vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words), "input");
+    reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     const int W = (ell + 63) / 64;
+    WsScope ws;
     StageTimer tm;
     tm.start(o.stats != nullptr, s);  // 0
     DevBuf<uint32_t> flags(4, s);
@@ -394,6 +541,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     tm.mark();  // 1: pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b);
     fill_stats(tm, n, o.stats);
+    store_counters(o.stats);
   } catch (const CgError& e) {
     set_last_error(e.msg);
     if (b.cells) dev_free(b.cells, nullptr);
@@ -457,8 +605,10 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
     cg_edges dummy_e;
     validate_common(n, ell, h_vecs, &dummy_c, &dummy_e);
     check_arch();
+    reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     const int W = (ell + 63) / 64;
+    WsScope ws;
     StageTimer tm;
     tm.start(o.stats != nullptr, s);
     DevBuf<uint32_t> flags(4, s);
@@ -508,6 +658,7 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
     tm.mark();  // 1: H2D + pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b);
     fill_stats(tm, n, o.stats);
+    store_counters(o.stats);
     const size_t cb = size_t(b.n_cells) * W * 8, ebytes = size_t(b.n_edges) * 8;
     hc = static_cast<uint64_t*>(host_pool_alloc(cb));
     he = static_cast<uint32_t*>(host_pool_alloc(ebytes));
@@ -589,6 +740,7 @@ void cg_index_free(cg_index* idx) {
   dev_free(idx->T, nullptr);
   dev_free(idx->tbase, nullptr);
   dev_free(idx->tbits, nullptr);
+  dev_free(idx->F, nullptr);
   delete idx;
 }
 

@@ -31,45 +31,77 @@ void set_last_error(const std::string& s);
     }                                                                              \
   } while (0)
 
-#define CG_LAUNCH_CHECK() CG_CUDA(cudaGetLastError())
+// every kernel launch is followed by CG_LAUNCH_CHECK(), which also counts it
+// (cg_stats.kernel_launches: the bench's gpu_launches evidence)
+void note_launch();
+#define CG_LAUNCH_CHECK()          \
+  do {                             \
+    ::cgk::note_launch();          \
+    CG_CUDA(cudaGetLastError());   \
+  } while (0)
 
 // ---------------------------------------------------------------- allocation
+// Persistent allocations (outputs, index) go to the allocator hook / the
+// device memory pool.  Workspace inside a build comes from a per-thread,
+// per-device stack arena (one cudaMalloc, grown to the previous build's
+// high-water mark), so a build makes no pool calls for its scratch buffers.
 void* dev_alloc(size_t bytes, cudaStream_t s);  // throws CG_ENOMEM
 void dev_free(void* p, cudaStream_t s);
+void* ws_alloc(size_t bytes, cudaStream_t s, bool* from_arena);
+void ws_free(void* p, cudaStream_t s, bool from_arena, size_t bytes);
 
-// RAII device buffer, stream-ordered free.
+// Marks one build: the arena is usable inside the scope; at the end it is
+// sized for the next build.  All DevBufs of the build must die inside it.
+struct WsScope {
+  WsScope();
+  ~WsScope();
+};
+
+enum class Mem { Scratch, Persist };
+
+// RAII device buffer (scratch: arena stack; persist: pool), stream-ordered.
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool arena = false;    // lives in the arena stack
+  bool scratch = false;  // allocated as scratch (arena or overflow)
   DevBuf() = default;
-  DevBuf(size_t count, cudaStream_t st) { alloc(count, st); }
-  void alloc(size_t count, cudaStream_t st) {
+  DevBuf(size_t count, cudaStream_t st, Mem m = Mem::Scratch) { alloc(count, st, m); }
+  void alloc(size_t count, cudaStream_t st, Mem m = Mem::Scratch) {
     reset();
     s = st;
     n = count;
-    p = static_cast<T*>(dev_alloc(count ? count * sizeof(T) : 16, st));
+    const size_t bytes = count ? count * sizeof(T) : 16;
+    if (m == Mem::Persist) {
+      p = static_cast<T*>(dev_alloc(bytes, st));
+      arena = scratch = false;
+    } else {
+      p = static_cast<T*>(ws_alloc(bytes, st, &arena));
+      scratch = true;
+    }
   }
+  // hand a persistent buffer to the caller (never valid for scratch memory)
   T* release() {
+    if (scratch) throw CgError{CG_ECUDA, "internal: release() of a scratch buffer"};
     T* r = p;
     p = nullptr;
     n = 0;
     return r;
   }
   void reset() {
-    if (p) dev_free(p, s);
+    if (p) {
+      if (scratch) ws_free(p, s, arena, n ? n * sizeof(T) : 16);
+      else dev_free(p, s);
+    }
     p = nullptr;
     n = 0;
+    arena = scratch = false;
   }
   ~DevBuf() { reset(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
-  DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { reset(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
-    return *this;
-  }
 };
 
 // pinned host staging for small read-backs (per thread, grows)

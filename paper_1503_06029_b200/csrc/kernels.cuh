@@ -32,6 +32,14 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
                          cudaStream_t s, SortStats* st);
 
+// MSD fast path for W in {1, 2}: LSD passes over the top B bits only (whole
+// keys move), then a shared-memory bitonic sort of each 2^B prefix bucket.
+// keys/alt are ping-ponged; *sorted points at the result.  Returns false if
+// a bucket exceeded the shared-memory capacity: *sorted is then only
+// bucket-ordered and the caller must finish with a full sort.
+bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
+                   cudaStream_t s, SortStats* st);
+
 // ---------------------------------------------------------------- a3 dedupe + compaction
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],
 // lcp[n_c] (leading equal bits with the next cell; 0xffff for the last),
@@ -40,6 +48,10 @@ void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, ui
                    uint16_t* lcp, uint32_t* n_cells, cudaStream_t s);
 
 // ---------------------------------------------------------------- a4/a5 layers + dictionary
+// Prefix filter: per layer p a bitmap over the top (b_p + kFilterExtra) bits
+// of its cells; a probe whose target prefix bit is clear cannot hit.
+constexpr int kFilterExtra = 4;
+
 struct DictView {
   const uint64_t* keys;       // layer-major cell rows u64[n_c][W]
   const uint32_t* idx;        // canonical index of each layer-major row
@@ -47,6 +59,8 @@ struct DictView {
   const uint32_t* T;          // prefix index entries
   const uint64_t* tbase;      // [ell + 1] offset of layer p's prefix table in T
   const uint8_t* tbits;       // [ell + 1] prefix bits b_p (0 = no prefix index)
+  const uint32_t* F;          // prefix filter bitmaps (u32 words)
+  const uint64_t* fbase;      // [ell + 1] offset (in u32 words) of layer p's bitmap in F
   int W;
   int ell;
   int64_t n_cells;
@@ -60,9 +74,10 @@ void launch_gather_rows(const uint64_t* in, const uint32_t* idx, int64_t n, int 
                         cudaStream_t s);
 void launch_gather_u16(const uint16_t* in, const uint32_t* idx, int64_t n, uint16_t* out,
                        cudaStream_t s);
-// T entries of every layer (sizes precomputed in tbase/tbits).
+// T entries and filter bits of every layer (sizes precomputed in
+// tbase/tbits/fbase; F must be zeroed by the caller).
 void launch_build_prefix_index(const DictView& d, const uint32_t* sorted_popc, uint32_t* T,
-                               cudaStream_t s);
+                               uint32_t* F, cudaStream_t s);
 
 // ---------------------------------------------------------------- a6/a7 probes + edges
 // For each layer-major cell j (popcount p), each bit k (<= lcp if lcp_prune)

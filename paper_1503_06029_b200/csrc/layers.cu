@@ -55,14 +55,19 @@ __device__ __forceinline__ int64_t prefix_of(uint64_t w0, int b) {
   return b ? int64_t(w0 >> (64 - b)) : 0;
 }
 
-__global__ void k_prefix_index(DictView d, const uint32_t* __restrict__ sp, uint32_t* __restrict__ T) {
+__global__ void k_prefix_index(DictView d, const uint32_t* __restrict__ sp, uint32_t* __restrict__ T,
+                               uint32_t* __restrict__ F) {
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < d.n_cells;
        j += int64_t(gridDim.x) * blockDim.x) {
     const int p = int(sp[j]);
     const uint32_t o = d.layer_off[p], e = d.layer_off[p + 1];
     const int b = d.tbits[p];
     uint32_t* Tp = T + d.tbase[p];
-    const int64_t x = prefix_of(d.keys[j * d.W], b);
+    const uint64_t w0 = d.keys[j * d.W];
+    // filter bit of the cell's (b + kFilterExtra)-bit prefix
+    const uint64_t y = w0 >> (64 - (b + kFilterExtra));
+    atomicOr(F + d.fbase[p] + (y >> 5), 1u << (y & 31));
+    const int64_t x = prefix_of(w0, b);
     const int64_t xp = (uint32_t(j) == o) ? -1 : prefix_of(d.keys[(j - 1) * d.W], b);
     for (int64_t q = xp + 1; q <= x; ++q) Tp[q] = uint32_t(j);
     if (uint32_t(j) + 1 == e) {
@@ -107,11 +112,11 @@ void launch_gather_u16(const uint16_t* in, const uint32_t* idx, int64_t n, uint1
 }
 
 void launch_build_prefix_index(const DictView& d, const uint32_t* sorted_popc, uint32_t* T,
-                               cudaStream_t s) {
+                               uint32_t* F, cudaStream_t s) {
   k_prefix_index_empty<<<blocks_for(d.ell + 1, 128), 128, 0, s>>>(d, T);
   CG_LAUNCH_CHECK();
   if (d.n_cells > 0) {
-    k_prefix_index<<<blocks_for(d.n_cells, 256), 256, 0, s>>>(d, sorted_popc, T);
+    k_prefix_index<<<blocks_for(d.n_cells, 256), 256, 0, s>>>(d, sorted_popc, T, F);
     CG_LAUNCH_CHECK();
   }
 }

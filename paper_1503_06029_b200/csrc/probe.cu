@@ -11,18 +11,22 @@
 //     all three share bits 0..k-1 (sorted prefix ranges are contiguous),
 //     so only k <= lcp(V_i, V_{i+1}) can hit;
 //   * x' is never materialised ("we do not have to keep the vector x'
-//     explicitly"): a comparison reads word w of x' as
-//     x_w | (w == k/64 ? bit : 0);
-//   * one thread per cell walks its candidate bits; the warp advances in
-//     lock-step rounds so each round's hits are appended with ONE atomicAdd
-//     per warp (ballot + popc ranks).
+//     explicitly"): word w of x' is x_w | (w == k/64 ? bit : 0);
+//   * near / far split on the target layer's prefix width b:
+//       near (k >= b): x' has x's b-bit prefix, so all near probes of a cell
+//         fall in ONE prefix bucket of layer p+1; they are resolved by a
+//         single merge walk over that bucket (x' ascends as k descends);
+//       far (k < b): each x' has its own bucket; a 1-bit-per-(b+4)-bit-prefix
+//         filter rejects most misses with one load before the bucket search;
+//   * one thread per cell; the warp advances in lock-step rounds so each
+//     round's hits are appended with ONE atomicAdd per warp (ballot + popc).
 #include "kernels.cuh"
 
 namespace cgk {
 namespace {
 
 // Lower-bound search of the implicit key t (word accessor tw) in layer q of
-// the dictionary; returns the layer-major row or -1.
+// the dictionary; returns the layer-major row or -1.  (cg_query path.)
 template <class TW>
 __device__ __forceinline__ int64_t dict_find(const DictView& d, int q, uint64_t t0, TW tw) {
   const uint32_t* Tq = d.T + d.tbase[q];
@@ -33,13 +37,11 @@ __device__ __forceinline__ int64_t dict_find(const DictView& d, int q, uint64_t 
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
     const uint64_t* r = d.keys + int64_t(mid) * W;
-    // compare row < t ?
     bool less = false;
-    uint64_t a = r[0];
+    const uint64_t a = r[0];
     if (a != t0) {
       less = a < t0;
     } else {
-      less = false;
       for (int w = 1; w < W; ++w) {
         const uint64_t aw = r[w], bw = tw(w);
         if (aw != bw) {
@@ -59,6 +61,45 @@ __device__ __forceinline__ int64_t dict_find(const DictView& d, int q, uint64_t 
   return lo;
 }
 
+// Cell words: registers for W <= 2, global memory otherwise.
+template <int WC>
+struct CellWords {
+  uint64_t r[WC > 0 ? WC : 1];
+  const uint64_t* g;
+  __device__ __forceinline__ void load(const uint64_t* p) {
+    g = p;
+    if (WC > 0) {
+#pragma unroll
+      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) r[w] = p[w];
+    }
+  }
+  __device__ __forceinline__ uint64_t operator()(int w) const {
+    if (WC > 0) {
+      uint64_t v = r[0];
+#pragma unroll
+      for (int u = 1; u < (WC > 0 ? WC : 1); ++u)
+        if (u == w) v = r[u];
+      return v;
+    }
+    return g[w];
+  }
+};
+
+// row < t, where t = V with bit mask bm set in word fw (rows share nothing
+// assumed); compares word 0 first (nearly always decisive).
+template <int WC>
+__device__ __forceinline__ int cmp_row(const uint64_t* row, const CellWords<WC>& V, int W, int fw,
+                                       uint64_t bm, uint64_t t0) {
+  const uint64_t a0 = row[0];
+  if (a0 != t0) return a0 < t0 ? -1 : 1;
+  const int n = WC > 0 ? WC : W;
+  for (int w = 1; w < n; ++w) {
+    const uint64_t a = row[w], b = V(w) | (w == fw ? bm : 0ull);
+    if (a != b) return a < b ? -1 : 1;
+  }
+  return 0;
+}
+
 template <int WC>
 __global__ void __launch_bounds__(256)
     k_probe(DictView d, const uint16_t* __restrict__ llcp, const uint32_t* __restrict__ sp,
@@ -70,30 +111,29 @@ __global__ void __launch_bounds__(256)
   const int ell = d.ell;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   unsigned long long my_issued = 0;
+
+  // emit one round's hits with a single atomicAdd per warp
+  auto emit = [&](bool hit, uint64_t e) {
+    const uint32_t hb = __ballot_sync(kFull, hit);
+    if (hb) {
+      const int leader = __ffs(hb) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(hb));
+      base = __shfl_sync(kFull, base, leader);
+      if (hit) {
+        const unsigned long long pos = base + __popc(hb & lt);
+        if (pos < cap) edges[pos] = e;
+      }
+    }
+  };
+
   for (int64_t jb = j_lo + int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); jb < j_hi;
        jb += stride) {
     const int64_t j = jb + lane;
     const bool valid = j < j_hi;
-    // ---- per-cell candidate iterator over zero bits k <= kmax
-    const uint64_t* V = d.keys + (valid ? j : 0) * W;
-    uint64_t vreg[WC > 0 ? WC : 1];
-    if (WC > 0) {
-#pragma unroll
-      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) vreg[w] = valid ? V[w] : 0;
-    }
-    auto vword = [&](int w) -> uint64_t {
-      if (WC > 0) {
-        uint64_t r = vreg[0];
-#pragma unroll
-        for (int u = 1; u < (WC > 0 ? WC : 1); ++u)
-          if (u == w) r = vreg[u];
-        return r;
-      }
-      return V[w];
-    };
-    int kmax = -1;
-    int q = 0;
-    uint64_t ci = 0;
+    CellWords<WC> V;
+    V.load(d.keys + (valid ? j : 0) * W);
+    int kmax = -1, q = 0;
     if (valid) {
       const int p = int(sp[j]);
       q = p + 1;
@@ -105,53 +145,133 @@ __global__ void __launch_bounds__(256)
           kmax = ell - 1;
         }
       }
-      ci = uint64_t(d.idx[j]) << 32;
     }
-    const int wmax = kmax >= 0 ? (kmax >> 6) : -1;
-    const uint64_t hm = kmax >= 0 ? (~0ull << (63 - (kmax & 63))) : 0ull;
-    int cw = 0;
-    uint64_t z = 0;
-    if (kmax >= 0) z = ~vword(0) & (wmax == 0 ? hm : ~0ull);
-    auto advance = [&]() -> bool {
-      while (z == 0 && cw < wmax) {
-        ++cw;
-        z = ~vword(cw) & (cw == wmax ? hm : ~0ull);
+    const uint64_t ci = valid ? (uint64_t(d.idx[valid ? j : 0]) << 32) : 0;
+    int b = 0;
+    const uint32_t* Tq = d.T;
+    const uint32_t* Fq = d.F;
+    uint32_t qend = 0;
+    if (kmax >= 0) {
+      b = d.tbits[q];
+      Tq = d.T + d.tbase[q];
+      Fq = d.F + d.fbase[q];
+      qend = d.layer_off[q + 1];
+    }
+    const uint64_t v0 = V(0);
+    // ---------------- near candidates: zero bits k in [b, kmax], taken in
+    // descending k (ascending target) against the one bucket of V's prefix
+    int nw_hi = -1, nw = -1;  // current word and last word (descending)
+    uint64_t nz = 0;          // remaining near candidate bits of word nw
+    uint32_t r = 0, rhi = 0;  // merge cursor in the bucket
+    if (kmax >= b) {
+      const int64_t x = b ? int64_t(v0 >> (64 - b)) : 0;
+      r = Tq[x];
+      rhi = Tq[x + 1];
+      if (r < rhi) {
+        nw_hi = kmax >> 6;
+        nw = nw_hi;
       }
-      return z != 0;
+    }
+    const int nw_lo = b >> 6;  // b <= 28: always word 0
+    auto near_mask = [&](int w) -> uint64_t {
+      uint64_t m = ~V(w);
+      if (w == nw_hi) m &= ~0ull << (63 - (kmax & 63));  // k <= kmax
+      if (w == nw_lo && b > 0) m &= ~0ull >> b;          // k >= b (b < 64)
+      return m;
     };
-    bool has = (kmax >= 0) && advance();
+    if (nw >= 0) nz = near_mask(nw);
+    auto near_next = [&]() -> bool {
+      while (nz == 0 && nw > nw_lo) {
+        --nw;
+        nz = near_mask(nw);
+      }
+      return nz != 0;
+    };
+    bool has = (nw >= 0) && near_next();
+    my_issued += 0;
     while (__any_sync(kFull, has)) {
       bool hit = false;
       uint64_t e = 0;
       if (has) {
-        const int c = __clzll(z);
-        const uint64_t bm = 1ull << (63 - c);
-        z ^= bm;
-        const int fw = cw;
-        const uint64_t t0 = vword(0) | (fw == 0 ? bm : 0ull);
-        auto tw = [&](int w) -> uint64_t { return vword(w) | (w == fw ? bm : 0ull); };
-        const int64_t r = dict_find(d, q, t0, tw);
-        if (r >= 0) {
+        const uint64_t bm = nz & (~nz + 1);  // lowest set bit = largest k
+        nz ^= bm;
+        const uint64_t t0 = v0 | (nw == 0 ? bm : 0ull);
+        ++my_issued;
+        if (rhi - r > 32) {
+          // big bucket (skewed data): binary search instead of a long walk
+          uint32_t lo = r, len = rhi - r;
+          while (len > 0) {
+            const uint32_t half = len >> 1;
+            if (cmp_row<WC>(d.keys + int64_t(lo + half) * W, V, W, nw, bm, t0) < 0) {
+              lo += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          r = lo;
+        } else {
+          while (r < rhi && cmp_row<WC>(d.keys + int64_t(r) * W, V, W, nw, bm, t0) < 0) ++r;
+        }
+        if (r < rhi && cmp_row<WC>(d.keys + int64_t(r) * W, V, W, nw, bm, t0) == 0) {
           hit = true;
           e = ci | d.idx[r];
+          ++r;
         }
+        if (r >= rhi) nz = 0, nw = nw_lo;  // bucket exhausted: no more near hits
+        has = near_next();
       }
-      const uint32_t hb = __ballot_sync(kFull, hit);
-      const uint32_t hv = __ballot_sync(kFull, has);
-      if (lane == 0) my_issued += __popc(hv);
-      if (hb) {
-        const int leader = __ffs(hb) - 1;
-        unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(hb));
-        base = __shfl_sync(kFull, base, leader);
-        if (hit) {
-          const unsigned long long pos = base + __popc(hb & lt);
-          if (pos < cap) edges[pos] = e;
+      emit(hit, e);
+    }
+    // ---------------- far candidates: zero bits k < min(b, kmax + 1), all in
+    // word 0 (b <= 28); filter first, then search the surviving ones
+    uint32_t surv = 0;  // bit k set = candidate k passed the filter
+    const int kfar = min(b - 1, kmax);
+    if (kfar >= 0) {
+      const int fbits = b + kFilterExtra;
+      const uint64_t y0 = v0 >> (64 - fbits);
+      uint64_t z = ~v0 & (~0ull << (63 - kfar));  // zero bits with k <= kfar
+      while (z) {
+        const int c = __clzll(z);  // k
+        z &= ~(1ull << (63 - c));
+        const uint64_t y = y0 | (1ull << (fbits - 1 - c));
+        ++my_issued;
+        if ((Fq[y >> 5] >> (y & 31)) & 1u) surv |= 1u << c;
+      }
+    }
+    has = surv != 0;
+    while (__any_sync(kFull, has)) {
+      bool hit = false;
+      uint64_t e = 0;
+      if (has) {
+        const int k = __ffs(surv) - 1;
+        surv &= surv - 1;
+        const uint64_t bm = 1ull << (63 - k);
+        const uint64_t t0 = v0 | bm;
+        const int64_t x = int64_t(t0 >> (64 - b));
+        uint32_t lo = Tq[x];
+        uint32_t len = Tq[x + 1] - lo;
+        while (len > 0) {
+          const uint32_t half = len >> 1;
+          if (cmp_row<WC>(d.keys + int64_t(lo + half) * W, V, W, 0, bm, t0) < 0) {
+            lo += half + 1;
+            len -= half + 1;
+          } else {
+            len = half;
+          }
         }
+        if (lo < qend && cmp_row<WC>(d.keys + int64_t(lo) * W, V, W, 0, bm, t0) == 0) {
+          hit = true;
+          e = ci | d.idx[lo];
+        }
+        has = surv != 0;
       }
-      if (has) has = advance();
+      emit(hit, e);
     }
   }
+  // warp-reduce the issued-probe counter
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_issued += __shfl_xor_sync(kFull, my_issued, o);
   if (lane == 0 && my_issued) atomicAdd(issued, my_issued);
 }
 

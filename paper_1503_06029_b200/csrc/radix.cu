@@ -1,18 +1,32 @@
-// radix.cu -- stable LSD radix sort engine (8-bit digits, one-sweep passes
-// with decoupled look-back) used by the cell sort (a2), the popcount layering
-// (a4) and the canonical edge sort (a7).
+// radix.cu -- the radix sort engine (a2 cell sort, a4 popcount layering, a7
+// canonical edge sort).
 //
 // "As these vectors are binary, the sorting can clearly be done in O(n*ell)
 // time, using the radix sort algorithm".  The paper does not say
-// which radix sort; this is a one-sweep LSD design for sm_100a:
-//   * one histogram kernel reads the keys once and counts every digit
-//     (run-length accumulated in registers so constant digits do not
-//     serialise shared-memory atomics); digits whose histogram is a single
-//     bucket are skipped (pad bits, small edge indices, narrow popcounts);
+// which radix sort.  This file implements, for sm_100a:
+//
+// (1) a stable one-sweep LSD pass engine over 8-bit digits:
+//   * one histogram kernel reads the keys once and counts the digits of all
+//     requested passes (run-length accumulated in registers so constant
+//     digits do not serialise shared-memory atomics); passes whose histogram
+//     is a single bucket are skipped (pad bits, small indices, narrow
+//     popcounts);
 //   * each pass: a CTA takes a tile by atomic ticket, loads it warp-striped
 //     (coalesced), ranks digits per warp with __match_any_sync, publishes
 //     per-digit tile counts through a decoupled look-back, reorders the tile
 //     in shared memory by digit and writes each digit run contiguously.
+//   Keys are u32, u64 or 128-bit rows (ulonglong2: .x = word 0, the most
+//   significant); digits are taken from the most significant word.
+//
+// (2) the cell sort for W <= 2 words (MSD fast path): LSD passes over only
+//   the top B bits move the whole keys into 2^B prefix buckets; a boundary
+//   kernel finds the bucket ranges; each bucket (~2^10 keys for uniform keys)
+//   is then fully sorted in shared memory by a bitonic network on the whole
+//   key.  A bucket larger than the shared-memory capacity makes the caller
+//   fall back to the full LSD sort (skewed data), which is always correct.
+//
+// (3) the multi-word LSD (W > 2): per word (least significant first) a
+//   stable sort of (word, u32 row index) pairs, then a row gather.
 #include <algorithm>
 #include <vector>
 
@@ -25,17 +39,40 @@ constexpr int kRadix = 256;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 
+template <class K>
+struct KT;
+template <>
+struct KT<uint32_t> {
+  __device__ __forceinline__ static uint64_t top(const uint32_t& k) { return k; }
+  __device__ __forceinline__ static uint32_t zero_val() { return 0; }
+};
+template <>
+struct KT<uint64_t> {
+  __device__ __forceinline__ static uint64_t top(const uint64_t& k) { return k; }
+};
+template <>
+struct KT<ulonglong2> {
+  __device__ __forceinline__ static uint64_t top(const ulonglong2& k) { return k.x; }
+};
+
+template <class K>
+__device__ __forceinline__ uint32_t digit_of(const K& k, int shift) {
+  return uint32_t(KT<K>::top(k) >> shift) & 255u;
+}
+
 template <class K, bool V>
 struct TileCfg {
-  static constexpr int IPT = V ? 12 : 16;
+  static constexpr int IPT = sizeof(K) == 16 ? 8 : (V ? 12 : 16);
   static constexpr int TILE = kSortThreads * IPT;
   static constexpr size_t SMEM = size_t(TILE) * (sizeof(K) + (V ? 4 : 0));
 };
 
+// hist[(d - dlo) * 256 + bin] for digits d in [dlo, dhi) of the top word
 template <class K>
 __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
-                                                    int ndig, uint32_t* __restrict__ hist) {
+                                                    int dlo, int dhi, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[8][kRadix];
+  const int nd = dhi - dlo;
   for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
   uint32_t last[8], cnt[8];
@@ -46,11 +83,11 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = uint64_t(keys[i]);
+    const uint64_t k = KT<K>::top(keys[i]);
 #pragma unroll
     for (int d = 0; d < 8; ++d) {
-      if (d < ndig) {
-        const uint32_t b = uint32_t(k >> (8 * d)) & 255u;
+      if (d < nd) {
+        const uint32_t b = uint32_t(k >> (8 * (d + dlo))) & 255u;
         if (b != last[d]) {
           if (cnt[d]) atomicAdd(&h[d][last[d]], cnt[d]);
           last[d] = b;
@@ -62,9 +99,9 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
 #pragma unroll
   for (int d = 0; d < 8; ++d)
-    if (d < ndig && cnt[d]) atomicAdd(&h[d][last[d]], cnt[d]);
+    if (d < nd && cnt[d]) atomicAdd(&h[d][last[d]], cnt[d]);
   __syncthreads();
-  for (int i = threadIdx.x; i < ndig * kRadix; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nd * kRadix; i += blockDim.x) {
     const uint32_t v = (&h[0][0])[i];
     if (v) atomicAdd(&hist[i], v);
   }
@@ -105,7 +142,7 @@ __global__ void __launch_bounds__(kSortThreads)
       key[i] = kin[g];
       if (V) val[i] = vin ? vin[g] : uint32_t(g);
     } else {
-      key[i] = 0;
+      key[i] = K{};
       val[i] = 0;
     }
   }
@@ -115,7 +152,7 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const bool valid = wbase + i * 32 + lane < n;
-    const uint32_t d = valid ? (uint32_t(uint64_t(key[i]) >> shift) & 255u) : 256u;
+    const uint32_t d = valid ? digit_of(key[i], shift) : 256u;
     const uint32_t peers = __match_any_sync(kFull, d);
     uint32_t prev = 0;
     if (valid) prev = wcnt[w][d];
@@ -143,7 +180,7 @@ __global__ void __launch_bounds__(kSortThreads)
   for (int i = 0; i < IPT; ++i) {
     const bool valid = wbase + i * 32 + lane < n;
     if (valid) {
-      const uint32_t d = uint32_t(uint64_t(key[i]) >> shift) & 255u;
+      const uint32_t d = digit_of(key[i], shift);
       const uint32_t pos = s_dexcl[d] + wcnt[w][d] + rank[i];
       skeys[pos] = key[i];
       if (V) svals[pos] = val[i];
@@ -153,7 +190,7 @@ __global__ void __launch_bounds__(kSortThreads)
   const int tile_n = int(tile_n_u);
   for (int j = tid; j < tile_n; j += kSortThreads) {
     const K k = skeys[j];
-    const uint32_t d = uint32_t(uint64_t(k) >> shift) & 255u;
+    const uint32_t d = digit_of(k, shift);
     const uint32_t gp = s_gbase[d] + uint32_t(j);
     kout[gp] = k;
     if (V) vout[gp] = svals[j];
@@ -176,19 +213,87 @@ __global__ void k_gather_word(const uint64_t* __restrict__ keys, int W, int w,
   }
 }
 
+// ---------------------------------------------------------------- MSD fast path
+// off[b] = first row whose top-B prefix is >= b, b in [0, 2^B]
+template <class K>
+__global__ void k_bucket_bounds(const K* __restrict__ keys, int64_t n, int B,
+                                uint32_t* __restrict__ off) {
+  const int sh = 64 - B;
+  const int64_t nb = int64_t(1) << B;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = int64_t(KT<K>::top(keys[i]) >> sh);
+    const int64_t pp = i == 0 ? -1 : int64_t(KT<K>::top(keys[i - 1]) >> sh);
+    for (int64_t q = pp + 1; q <= p; ++q) off[q] = uint32_t(i);
+    if (i == n - 1)
+      for (int64_t q = p + 1; q <= nb; ++q) off[q] = uint32_t(n);
+  }
+}
+
+__device__ __forceinline__ bool key_less(const uint64_t& a, const uint64_t& b) { return a < b; }
+__device__ __forceinline__ bool key_less(const ulonglong2& a, const ulonglong2& b) {
+  return a.x < b.x || (a.x == b.x && a.y < b.y);
+}
+template <class K>
+__device__ __forceinline__ K key_max();
+template <>
+__device__ __forceinline__ uint64_t key_max<uint64_t>() { return ~0ull; }
+template <>
+__device__ __forceinline__ ulonglong2 key_max<ulonglong2>() { return make_ulonglong2(~0ull, ~0ull); }
+
+// One CTA sorts one prefix bucket at a time (persistent loop) in shared
+// memory with a bitonic network over the whole key; buckets larger than CAP
+// raise *overflow (the caller then runs the full LSD sort instead).
+template <class K, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    k_bucket_sort(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets,
+                  int CAP, uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* s = reinterpret_cast<K*>(smem_raw);
+  const int tid = threadIdx.x;
+  for (int64_t b = blockIdx.x; b < nbuckets; b += gridDim.x) {
+    const uint32_t lo = off[b], hi = off[b + 1];
+    const int size = int(hi - lo);
+    if (size <= 1) continue;
+    if (size > CAP) {
+      if (tid == 0) atomicOr(overflow, 1u);
+      continue;
+    }
+    int P = 2;
+    while (P < size) P <<= 1;
+    for (int i = tid; i < P; i += THREADS) s[i] = i < size ? keys[lo + i] : key_max<K>();
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int p = tid; p < (P >> 1); p += THREADS) {
+          const int i = 2 * j * (p / j) + (p % j);
+          const int ixj = i + j;
+          const bool up = (i & k) == 0;
+          const K a = s[i], c = s[ixj];
+          if (key_less(c, a) == up) {
+            s[i] = c;
+            s[ixj] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = tid; i < size; i += THREADS) keys[lo + i] = s[i];
+    __syncthreads();
+  }
+}
+
 int grid_for(int64_t n, int threads, int per_sm = 8) {
   int64_t b = (n + threads - 1) / threads;
   int64_t cap = int64_t(num_sms()) * per_sm;
   return int(std::max<int64_t>(1, std::min(b, cap)));
 }
 
-}  // namespace
-
+// Generic pass driver over digits [dlo, dhi) of the top word.
 template <class K>
-void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, uint32_t* vals_alt,
-                bool want_vals, int64_t n, int key_bits, K** keys_out, uint32_t** vals_out,
-                cudaStream_t s, SortStats* st) {
-  const int ndig = std::max(1, (key_bits + 7) / 8);
+void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
+                  uint32_t* vals_alt, bool want_vals, int64_t n, int dlo, int dhi, K** keys_out,
+                  uint32_t** vals_out, cudaStream_t s, SortStats* st) {
   *keys_out = keys;
   if (vals_out) *vals_out = nullptr;
   auto identity_or_input = [&]() {
@@ -201,26 +306,27 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
       *vals_out = vals;
     }
   };
-  if (n <= 1) {
+  if (n <= 1 || dhi <= dlo) {
     identity_or_input();
     return;
   }
-  DevBuf<uint32_t> hist(size_t(ndig) * kRadix, s);
+  const int nd = dhi - dlo;
+  DevBuf<uint32_t> hist(size_t(nd) * kRadix, s);
   CG_CUDA(cudaMemsetAsync(hist.p, 0, hist.n * sizeof(uint32_t), s));
-  k_digit_hist<K><<<grid_for(n, 256, 4), 256, 0, s>>>(keys, n, ndig, hist.p);
+  k_digit_hist<K><<<grid_for(n, 256, 4), 256, 0, s>>>(keys, n, dlo, dhi, hist.p);
   CG_LAUNCH_CHECK();
   uint32_t* hh = static_cast<uint32_t*>(host_stage(hist.n * sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(hh, hist.p, hist.n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
   std::vector<int> digits;
   std::vector<uint32_t> bases;
-  for (int d = 0; d < ndig; ++d) {
+  for (int d = 0; d < nd; ++d) {
     const uint32_t* h = hh + d * kRadix;
     bool trivial = false;
     for (int b = 0; b < kRadix; ++b)
       if (int64_t(h[b]) == n) trivial = true;
     if (trivial) continue;
-    digits.push_back(d);
+    digits.push_back(d + dlo);
     uint32_t run = 0;
     for (int b = 0; b < kRadix; ++b) {
       bases.push_back(run);
@@ -243,8 +349,6 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
   DevBuf<uint32_t> counters(size_t(P), s);
   CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint64_t), s));
   CG_CUDA(cudaMemsetAsync(counters.p, 0, counters.n * sizeof(uint32_t), s));
-  // The host staging buffer is reused by later read-backs; bases were copied
-  // from a std::vector, and the copy is ordered before those on the stream.
   K* ck = keys;
   K* ak = keys_alt;
   const uint32_t* cv = vals_in;
@@ -264,16 +368,25 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
     CG_LAUNCH_CHECK();
     std::swap(ck, ak);
     if (V) {
-      // next pass reads av; writes into the other buffer (never into vals_in)
+      // next pass reads what was just written; never writes into vals_in
       uint32_t* written = av;
       av = (cv == vals_in) ? spare_v : const_cast<uint32_t*>(cv);
       cv = written;
     }
   }
-  // The pass kernels must finish before the temporaries (status, bases) are
-  // released: stream-ordered frees take care of that.
   *keys_out = ck;
   if (vals_out && V) *vals_out = const_cast<uint32_t*>(cv);
+}
+
+}  // namespace
+
+template <class K>
+void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, uint32_t* vals_alt,
+                bool want_vals, int64_t n, int key_bits, K** keys_out, uint32_t** vals_out,
+                cudaStream_t s, SortStats* st) {
+  const int ndig = std::max(1, (key_bits + 7) / 8);
+  radix_passes<K>(keys, keys_alt, vals_in, vals, vals_alt, want_vals, n, 0, ndig, keys_out,
+                  vals_out, s, st);
 }
 
 template void radix_sort<uint32_t>(uint32_t*, uint32_t*, const uint32_t*, uint32_t*, uint32_t*,
@@ -299,6 +412,59 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     idx = vo;
   }
   launch_gather_rows(keys, idx, n, W, sorted, s);
+}
+
+namespace {
+template <class K>
+bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStats* st) {
+  // B top bits (a multiple of 8) so buckets hold ~2^10 keys on average
+  int B = 8;
+  while (B < 24 && (n >> B) > 1024) B += 8;
+  K* ko = nullptr;
+  radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
+                  s, st);
+  const int64_t nb = int64_t(1) << B;
+  DevBuf<uint32_t> off(size_t(nb) + 1, s);
+  DevBuf<uint32_t> flag(1, s);
+  CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
+  k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, off.p);
+  CG_LAUNCH_CHECK();
+  // shared-memory capacity: 2x the mean bucket (>= 2048 keys), at most 128 KB
+  const int64_t avg = (n + nb - 1) / nb;
+  const int maxcap = int((128 << 10) / sizeof(K));
+  int cap = 2048;
+  while (cap < maxcap && cap < 2 * avg) cap <<= 1;
+  const size_t smem = size_t(cap) * sizeof(K);
+  CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               128 << 10));
+  const int per_sm = std::max(1, int((200 << 10) / smem));
+  const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
+  k_bucket_sort<K, 512><<<grid, 512, smem, s>>>(ko, off.p, nb, cap, flag.p);
+  CG_LAUNCH_CHECK();
+  uint32_t* hf = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(hf, flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  *out = ko;
+  return hf[0] == 0;
+}
+}  // namespace
+
+bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
+                   cudaStream_t s, SortStats* st) {
+  if (W == 1) {
+    uint64_t* o = nullptr;
+    const bool ok = msd_sort_impl<uint64_t>(keys, alt, n, &o, s, st);
+    *sorted = o;
+    return ok;
+  }
+  if (W == 2) {
+    ulonglong2* o = nullptr;
+    const bool ok = msd_sort_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
+                                              reinterpret_cast<ulonglong2*>(alt), n, &o, s, st);
+    *sorted = reinterpret_cast<uint64_t*>(o);
+    return ok;
+  }
+  return false;
 }
 
 }  // namespace cgk

@@ -198,6 +198,28 @@ def test_options_agree(cg):
     assert r0.stats["issued_probes"] <= rn.stats["issued_probes"]
 
 
+@pytest.mark.parametrize("case", ["C3", "C5small", "W1uniform", "W2dups"])
+def test_sort_paths_agree(cg, case):
+    """MSD fast path (prefix buckets + shared-memory bitonic sort, with the
+    overflow fallback) and the full LSD path give identical bytes."""
+    if case == "C3":  # heavy duplicates: buckets overflow -> fallback path
+        x = synth.config("C3")["bytes"]
+    elif case == "C5small":
+        d = synth.config("C5", scale_log2=18)
+        x = synth.unpack_words_np(d["words"], 128)
+    elif case == "W1uniform":
+        x = synth.random_bytes(4, 300000, 64)
+    else:
+        x = synth.random_bytes(6, 200000, 100, dup_frac=0.5)
+    c0, e0, _ = gpu_build(cg, x, sort_kind="auto")
+    c1, e1, _ = gpu_build(cg, x, sort_kind="lsd")
+    np.testing.assert_array_equal(c0, c1)
+    np.testing.assert_array_equal(e0, e1)
+    rc, oc, oe = oracle.build(x)
+    np.testing.assert_array_equal(c0, oc)
+    np.testing.assert_array_equal(e0, oe)
+
+
 def test_determinism(cg):
     d = synth.config("C3")
     c0, e0, _ = gpu_build(cg, d["bytes"])
