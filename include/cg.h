@@ -84,6 +84,8 @@ typedef struct {
   int64_t kernel_launches; /* CUDA kernels this library launched for the call */
   double us_host_alloc;    /* host time spent inside device allocation calls */
   int64_t n_allocs;        /* device allocations made for the call */
+  double us_host_total;    /* host wall time of the whole call */
+  double us_host_setup;    /* host wall time before the first stage event */
 } cg_stats;
 
 enum {

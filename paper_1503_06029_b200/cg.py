@@ -48,7 +48,8 @@ class cg_stats(ctypes.Structure):
                 ("n_in", "n_cells", "n_edges", "logical_probes", "issued_probes")] + \
                [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int64), ("us_host_alloc", ctypes.c_double),
-                ("n_allocs", ctypes.c_int64)]
+                ("n_allocs", ctypes.c_int64), ("us_host_total", ctypes.c_double),
+                ("us_host_setup", ctypes.c_double)]
 
 
 class cg_opts(ctypes.Structure):

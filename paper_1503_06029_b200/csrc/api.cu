@@ -516,6 +516,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
   if (o_in) o = *o_in;
   if (o.index_out) *o.index_out = nullptr;
   Built b;
+  const auto h0 = std::chrono::steady_clock::now();
+  double setup_us = 0;
   try {
     validate_common(n, ell, vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words),
                     cells, edges);
@@ -529,6 +531,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     WsScope ws;
     StageTimer tm;
     tm.start(o.stats != nullptr, s);  // 0
+    setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
     DevBuf<uint64_t> keys(size_t(n) * W, s);
@@ -553,6 +556,11 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
   } catch (const std::exception& e) {
     set_last_error(e.what());
     return CG_ECUDA;
+  }
+  if (o.stats) {
+    o.stats->us_host_setup = setup_us;
+    o.stats->us_host_total =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
   }
   return finish(CG_OK, b, cells, edges, o, ell);
 }

@@ -187,8 +187,32 @@ __global__ void __launch_bounds__(256)
       }
       return nz != 0;
     };
-    bool has = (nw >= 0) && near_next();
-    my_issued += 0;
+    // Small bucket (the common case): scan its rows instead of iterating the
+    // candidates.  A row R of layer p+1 with V's b-bit prefix equals V | e_k
+    // for some k >= b iff R contains every bit of V (popc(R) = popc(V) + 1),
+    // and any such k is <= lcp (the LCP argument above), so the subset test
+    // finds exactly the near edges.
+    const bool scan = (nw >= 0) && (rhi - r <= 16);
+    bool has = scan ? true : ((nw >= 0) && near_next());
+    while (__any_sync(kFull, scan && has)) {
+      bool hit = false;
+      uint64_t e = 0;
+      if (scan && has) {
+        const uint64_t* R = d.keys + int64_t(r) * W;
+        bool sub = (v0 & ~R[0]) == 0;
+        const int n = WC > 0 ? WC : W;
+        for (int w = 1; w < n && sub; ++w) sub = (V(w) & ~R[w]) == 0;
+        ++my_issued;
+        if (sub) {
+          hit = true;
+          e = ci | d.idx[r];
+        }
+        ++r;
+        has = r < rhi;
+      }
+      emit(hit, e);
+    }
+    if (scan) has = false;
     while (__any_sync(kFull, has)) {
       bool hit = false;
       uint64_t e = 0;

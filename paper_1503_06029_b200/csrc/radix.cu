@@ -241,44 +241,180 @@ __device__ __forceinline__ uint64_t key_max<uint64_t>() { return ~0ull; }
 template <>
 __device__ __forceinline__ ulonglong2 key_max<ulonglong2>() { return make_ulonglong2(~0ull, ~0ull); }
 
-// One CTA sorts one prefix bucket at a time (persistent loop) in shared
-// memory with a bitonic network over the whole key; buckets larger than CAP
-// raise *overflow (the caller then runs the full LSD sort instead).
-template <class K, int THREADS>
-__global__ void __launch_bounds__(THREADS)
+// byte P of the key, P = 0 the most significant byte of word 0
+__device__ __forceinline__ uint32_t key_byte(const uint64_t& k, int P) {
+  return uint32_t(k >> (56 - 8 * P)) & 255u;
+}
+__device__ __forceinline__ uint32_t key_byte(const ulonglong2& k, int P) {
+  return P < 8 ? uint32_t(k.x >> (56 - 8 * P)) & 255u : uint32_t(k.y >> (56 - 8 * (P - 8))) & 255u;
+}
+__device__ __forceinline__ void key_andor(const uint64_t& k, uint64_t* a, uint64_t* o) {
+  a[0] &= k;
+  o[0] |= k;
+}
+__device__ __forceinline__ void key_andor(const ulonglong2& k, uint64_t* a, uint64_t* o) {
+  a[0] &= k.x;
+  o[0] |= k.x;
+  a[1] &= k.y;
+  o[1] |= k.y;
+}
+
+constexpr int kBktThreads = 256;
+constexpr int kBktWarps = kBktThreads / 32;
+constexpr int kBktMaxRounds = 64;
+
+// One CTA sorts one prefix bucket at a time (persistent loop), entirely in
+// shared memory.  The keys stay in place; u16 row indices move:
+//   1. block AND/OR reduction finds the bytes that vary inside the bucket;
+//   2. stable LSD passes over the two most significant varying bytes
+//      (warp ranking with __match_any_sync, as in the global passes);
+//   3. odd-even transposition rounds on the whole key finish the order
+//      (ties of the two bytes are short runs: planted pairs, duplicates);
+//      a bucket that does not settle within kBktMaxRounds, or is larger than
+//      CAP, raises *overflow and the caller runs the full LSD sort instead.
+template <class K>
+__global__ void __launch_bounds__(kBktThreads)
     k_bucket_sort(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets,
-                  int CAP, uint32_t* __restrict__ overflow) {
+                  int CAP, int B, uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
-  const int tid = threadIdx.x;
-  for (int64_t b = blockIdx.x; b < nbuckets; b += gridDim.x) {
-    const uint32_t lo = off[b], hi = off[b + 1];
-    const int size = int(hi - lo);
-    if (size <= 1) continue;
-    if (size > CAP) {
+  uint16_t* ia = reinterpret_cast<uint16_t*>(smem_raw + size_t(CAP) * sizeof(K));
+  uint16_t* ib = ia + CAP;
+  __shared__ uint32_t cnt[kBktWarps][kRadix];
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint64_t s_red[2][kBktWarps][2];
+  constexpr int NW = sizeof(K) / 8;
+  constexpr int NBYTES = sizeof(K);
+  constexpr int MAXC = 16;  // chunks of 32 per warp: CAP <= 8 warps * 16 * 32 = 4096
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+  for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x) {
+    const uint32_t lo = off[bk], hi = off[bk + 1];
+    const int S = int(hi - lo);
+    if (S <= 1) continue;
+    if (S > CAP) {
       if (tid == 0) atomicOr(overflow, 1u);
       continue;
     }
-    int P = 2;
-    while (P < size) P <<= 1;
-    for (int i = tid; i < P; i += THREADS) s[i] = i < size ? keys[lo + i] : key_max<K>();
+    // ---- load + AND/OR of the key words
+    uint64_t av[2] = {~0ull, ~0ull}, ov[2] = {0ull, 0ull};
+    for (int i = tid; i < S; i += kBktThreads) {
+      const K k = keys[lo + i];
+      s[i] = k;
+      ia[i] = uint16_t(i);
+      key_andor(k, av, ov);
+    }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        av[w] &= __shfl_xor_sync(kFull, av[w], o);
+        ov[w] |= __shfl_xor_sync(kFull, ov[w], o);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        s_red[0][wid][w] = av[w];
+        s_red[1][wid][w] = ov[w];
+      }
+    }
     __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int p = tid; p < (P >> 1); p += THREADS) {
-          const int i = 2 * j * (p / j) + (p % j);
-          const int ixj = i + j;
-          const bool up = (i & k) == 0;
-          const K a = s[i], c = s[ixj];
-          if (key_less(c, a) == up) {
-            s[i] = c;
-            s[ixj] = a;
+    uint64_t dif[2] = {0ull, 0ull};
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      uint64_t a = ~0ull, o = 0ull;
+      for (int ww = 0; ww < kBktWarps; ++ww) {
+        a &= s_red[0][ww][w];
+        o |= s_red[1][ww][w];
+      }
+      dif[w] = a ^ o;  // bits that vary inside the bucket
+    }
+    int P1 = -1, P2 = -1;  // two most significant varying bytes
+    for (int P = B / 8; P < NBYTES; ++P) {
+      const uint64_t wv = dif[P >> 3];
+      if ((wv >> (56 - 8 * (P & 7))) & 255u) {
+        if (P1 < 0) P1 = P;
+        else if (P2 < 0) P2 = P;
+      }
+    }
+    uint16_t* cur = ia;
+    uint16_t* nxt = ib;
+    // ---- stable LSD passes: P2 then P1
+    const int seg = ((S + kBktWarps * 32 - 1) / (kBktWarps * 32)) * 32;  // rows per warp
+    for (int pass = 0; pass < 2; ++pass) {
+      const int P = pass == 0 ? P2 : P1;
+      if (P < 0) continue;
+      for (int i = tid; i < kBktWarps * kRadix; i += kBktThreads) (&cnt[0][0])[i] = 0;
+      __syncthreads();
+      uint32_t rk[MAXC], dg[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = wid * seg + c * 32 + lane;
+        const bool in_seg = c * 32 < seg;
+        const bool valid = in_seg && i < S;
+        const uint32_t d = valid ? key_byte(s[cur[i]], P) : 256u;
+        dg[c] = d;
+        rk[c] = 0;
+        if (in_seg) {  // warp-uniform
+          const uint32_t peers = __match_any_sync(kFull, d);
+          uint32_t prev = 0;
+          if (valid) prev = cnt[wid][d];
+          __syncwarp();
+          if (valid && lane == __ffs(peers) - 1) cnt[wid][d] = prev + __popc(peers);
+          __syncwarp();
+          rk[c] = prev + __popc(peers & lt);
+        }
+      }
+      __syncthreads();
+      uint32_t tot = 0;
+#pragma unroll
+      for (int ww = 0; ww < kBktWarps; ++ww) {
+        const uint32_t c = cnt[ww][tid];
+        cnt[ww][tid] = tot;
+        tot += c;
+      }
+      uint32_t all;
+      const uint32_t dbase = block_excl_scan(tot, s_scan, &all);
+#pragma unroll
+      for (int ww = 0; ww < kBktWarps; ++ww) cnt[ww][tid] += dbase;
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = wid * seg + c * 32 + lane;
+        if (c * 32 < seg && i < S) nxt[cnt[wid][dg[c]] + rk[c]] = cur[i];
+      }
+      __syncthreads();
+      uint16_t* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    // ---- odd-even transposition on whole keys until settled
+    bool settled = false;
+    for (int round = 0; round < kBktMaxRounds; ++round) {
+      int changed = 0;
+      for (int ph = 0; ph < 2; ++ph) {
+        for (int i = 2 * tid + ph; i + 1 < S; i += 2 * kBktThreads) {
+          const uint16_t a = cur[i], c = cur[i + 1];
+          if (key_less(s[c], s[a])) {
+            cur[i] = c;
+            cur[i + 1] = a;
+            changed = 1;
           }
         }
         __syncthreads();
       }
+      if (!__syncthreads_or(changed)) {
+        settled = true;
+        break;
+      }
     }
-    for (int i = tid; i < size; i += THREADS) keys[lo + i] = s[i];
+    if (!settled) {
+      if (tid == 0) atomicOr(overflow, 1u);
+      __syncthreads();
+      continue;
+    }
+    for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[cur[i]];
     __syncthreads();
   }
 }
@@ -429,17 +565,15 @@ bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStat
   CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
   k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, off.p);
   CG_LAUNCH_CHECK();
-  // shared-memory capacity: 2x the mean bucket (>= 2048 keys), at most 128 KB
+  // shared-memory capacity: 2x the mean bucket, 2048..4096 rows
   const int64_t avg = (n + nb - 1) / nb;
-  const int maxcap = int((128 << 10) / sizeof(K));
-  int cap = 2048;
-  while (cap < maxcap && cap < 2 * avg) cap <<= 1;
-  const size_t smem = size_t(cap) * sizeof(K);
-  CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               128 << 10));
-  const int per_sm = std::max(1, int((200 << 10) / smem));
+  const int cap = avg <= 1024 ? 2048 : 4096;
+  const size_t smem = size_t(cap) * (sizeof(K) + 4);
+  CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  const int per_sm = std::max(1, int((200 << 10) / (smem + 12 * 1024)));
   const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
-  k_bucket_sort<K, 512><<<grid, 512, smem, s>>>(ko, off.p, nb, cap, flag.p);
+  k_bucket_sort<K><<<grid, kBktThreads, smem, s>>>(ko, off.p, nb, cap, B, flag.p);
   CG_LAUNCH_CHECK();
   uint32_t* hf = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(hf, flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

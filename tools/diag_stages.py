@@ -25,3 +25,14 @@ for i in range(reps):
     st = {k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.stats.items()}
     print(json.dumps({"rep": i, "wall_ms": round(wall, 2), **st}))
     del r
+
+# python-side overhead breakdown of one call
+import cProfile, pstats  # noqa: E402
+torch.cuda.synchronize()
+pr = cProfile.Profile()
+pr.enable()
+r = cg.build(x, want_stats=True)
+torch.cuda.synchronize()
+pr.disable()
+print(json.dumps({k: round(v, 1) for k, v in r.stats.items() if k.startswith("us_host")}))
+pstats.Stats(pr).sort_stats("cumulative").print_stats(12)
