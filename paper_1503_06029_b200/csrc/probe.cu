@@ -112,18 +112,32 @@ __global__ void __launch_bounds__(256)
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   unsigned long long my_issued = 0;
 
-  // emit one round's hits with a single atomicAdd per warp
+  // Per-warp staging buffer in shared memory: each round's hits are ranked
+  // with a ballot and appended locally; when the buffer fills up (and at the
+  // end) the warp reserves space with ONE atomicAdd and copies the staged
+  // edges out coalesced.  (One global counter hit by every round made the
+  // atomic's return latency the kernel's top stall.)
+  constexpr int kStage = 256;
+  __shared__ uint64_t stage[256 / 32][kStage];
+  uint64_t* my_stage = stage[threadIdx.x >> 5];
+  int fill = 0;  // warp-uniform
+  auto flush = [&]() {
+    if (fill == 0) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)fill);
+    base = __shfl_sync(kFull, base, 0);
+    __syncwarp();
+    for (int i = lane; i < fill; i += 32)
+      if (base + i < cap) edges[base + i] = my_stage[i];
+    __syncwarp();
+    fill = 0;
+  };
   auto emit = [&](bool hit, uint64_t e) {
     const uint32_t hb = __ballot_sync(kFull, hit);
     if (hb) {
-      const int leader = __ffs(hb) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(hb));
-      base = __shfl_sync(kFull, base, leader);
-      if (hit) {
-        const unsigned long long pos = base + __popc(hb & lt);
-        if (pos < cap) edges[pos] = e;
-      }
+      if (hit) my_stage[fill + __popc(hb & lt)] = e;
+      fill += __popc(hb);
+      if (fill > kStage - 32) flush();
     }
   };
 
@@ -194,23 +208,31 @@ __global__ void __launch_bounds__(256)
     // finds exactly the near edges.
     const bool scan = (nw >= 0) && (rhi - r <= 16);
     bool has = scan ? true : ((nw >= 0) && near_next());
-    while (__any_sync(kFull, scan && has)) {
-      bool hit = false;
-      uint64_t e = 0;
-      if (scan && has) {
-        const uint64_t* R = d.keys + int64_t(r) * W;
-        bool sub = (v0 & ~R[0]) == 0;
-        const int n = WC > 0 ? WC : W;
-        for (int w = 1; w < n && sub; ++w) sub = (V(w) & ~R[w]) == 0;
-        ++my_issued;
-        if (sub) {
-          hit = true;
-          e = ci | d.idx[r];
+    while (__any_sync(kFull, scan && r < rhi)) {
+      // four rows per round, loaded independently (16-byte loads for W = 2)
+      bool sub[4] = {false, false, false, false};
+      if (scan && r < rhi) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t rr = r + u;
+          if (rr < rhi) {
+            const uint64_t* R = d.keys + int64_t(rr) * W;
+            if (WC == 2) {
+              const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(R);
+              sub[u] = ((v0 & ~v.x) | (V(1) & ~v.y)) == 0;
+            } else {
+              bool sb = (v0 & ~R[0]) == 0;
+              const int n = WC > 0 ? WC : W;
+              for (int w = 1; w < n && sb; ++w) sb = (V(w) & ~R[w]) == 0;
+              sub[u] = sb;
+            }
+            ++my_issued;
+          }
         }
-        ++r;
-        has = r < rhi;
       }
-      emit(hit, e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) emit(sub[u], sub[u] ? (ci | d.idx[r + u]) : 0ull);
+      if (scan) r += 4;  // non-scan lanes keep their merge cursor
     }
     if (scan) has = false;
     while (__any_sync(kFull, has)) {
@@ -256,11 +278,28 @@ __global__ void __launch_bounds__(256)
       const uint64_t y0 = v0 >> (64 - fbits);
       uint64_t z = ~v0 & (~0ull << (63 - kfar));  // zero bits with k <= kfar
       while (z) {
-        const int c = __clzll(z);  // k
-        z &= ~(1ull << (63 - c));
-        const uint64_t y = y0 | (1ull << (fbits - 1 - c));
-        ++my_issued;
-        if ((Fq[y >> 5] >> (y & 31)) & 1u) surv |= 1u << c;
+        // four independent filter loads in flight per thread
+        int ks[4];
+        uint32_t fw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ks[u] = -1;
+          fw[u] = 0;
+          if (z) {
+            const int c = __clzll(z);  // k
+            z &= ~(1ull << (63 - c));
+            ks[u] = c;
+            fw[u] = __ldg(Fq + ((y0 | (1ull << (fbits - 1 - c))) >> 5));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (ks[u] >= 0) {
+            const uint64_t y = y0 | (1ull << (fbits - 1 - ks[u]));
+            ++my_issued;
+            if ((fw[u] >> (y & 31)) & 1u) surv |= 1u << ks[u];
+          }
+        }
       }
     }
     has = surv != 0;
@@ -274,25 +313,52 @@ __global__ void __launch_bounds__(256)
         const uint64_t t0 = v0 | bm;
         const int64_t x = int64_t(t0 >> (64 - b));
         uint32_t lo = Tq[x];
-        uint32_t len = Tq[x + 1] - lo;
-        while (len > 0) {
-          const uint32_t half = len >> 1;
-          if (cmp_row<WC>(d.keys + int64_t(lo + half) * W, V, W, 0, bm, t0) < 0) {
-            lo += half + 1;
-            len -= half + 1;
-          } else {
-            len = half;
+        const uint32_t hi = Tq[x + 1];
+        int64_t found = -1;
+        if (hi - lo <= 12) {
+          // small bucket: compare up to four rows per step, loads independent
+          for (uint32_t rr = lo; rr < hi && found < 0; rr += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t ru = rr + u;
+              if (ru < hi) {
+                const uint64_t* R = d.keys + int64_t(ru) * W;
+                bool eq;
+                if (WC == 2) {
+                  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(R);
+                  eq = v.x == t0 && v.y == V(1);
+                } else {
+                  eq = R[0] == t0;
+                  const int n = WC > 0 ? WC : W;
+                  for (int w = 1; w < n && eq; ++w) eq = R[w] == V(w);
+                }
+                if (eq) found = ru;
+              }
+            }
           }
+        } else {
+          uint32_t len = hi - lo;
+          while (len > 0) {
+            const uint32_t half = len >> 1;
+            if (cmp_row<WC>(d.keys + int64_t(lo + half) * W, V, W, 0, bm, t0) < 0) {
+              lo += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          if (lo < qend && cmp_row<WC>(d.keys + int64_t(lo) * W, V, W, 0, bm, t0) == 0) found = lo;
         }
-        if (lo < qend && cmp_row<WC>(d.keys + int64_t(lo) * W, V, W, 0, bm, t0) == 0) {
+        if (found >= 0) {
           hit = true;
-          e = ci | d.idx[lo];
+          e = ci | d.idx[found];
         }
         has = surv != 0;
       }
       emit(hit, e);
     }
   }
+  flush();
   // warp-reduce the issued-probe counter
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) my_issued += __shfl_xor_sync(kFull, my_issued, o);
