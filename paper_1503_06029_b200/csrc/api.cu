@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -385,6 +386,9 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   std::vector<uint8_t> h_bits(ell + 1);
   std::vector<uint64_t> h_base(2 * (ell + 1));  // [tbase | fbase]
   uint64_t tot = 0, ftot = 0;
+  // filter resolution (tuning knob, ncu-driven): b_p + fextra prefix bits
+  int fextra = kFilterExtra;
+  if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
   for (int p = 0; p <= ell; ++p) {
     const uint64_t sz = h_off[p + 1] - h_off[p];
     int b = 0;
@@ -394,7 +398,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     h_base[p] = tot;
     tot += (uint64_t(1) << b) + 1;
     h_base[ell + 1 + p] = ftot;
-    ftot += std::max<uint64_t>(1, (uint64_t(1) << (b + kFilterExtra)) / 32);
+    ftot += std::max<uint64_t>(1, (uint64_t(1) << (b + fextra)) / 32);
   }
   DevBuf<uint8_t> tbits(size_t(ell) + 1, s, ix);
   DevBuf<uint64_t> tbase(2 * (size_t(ell) + 1), s, ix);
@@ -403,7 +407,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   CG_CUDA(cudaMemcpyAsync(tbits.p, h_bits.data(), h_bits.size(), cudaMemcpyHostToDevice, s));
   CG_CUDA(cudaMemcpyAsync(tbase.p, h_base.data(), h_base.size() * 8, cudaMemcpyHostToDevice, s));
   CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * sizeof(uint32_t), s));
-  DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, F.p, tbase.p + ell + 1, W, ell, nc};
+  DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, F.p, tbase.p + ell + 1, W, ell, nc, fextra};
   launch_build_prefix_index(dv, sp, T.p, F.p, s);
   tm.mark();  // 5: dict
   // ---- a6 probes + a7 warp-aggregated append
@@ -453,7 +457,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     ix->F = F.release();
     cudaGetDevice(&ix->device);
     ix->view = DictView{ix->keys, ix->idx, ix->layer_off, ix->T, ix->tbase, ix->tbits,
-                        ix->F, ix->tbase + ell + 1, W, ell, nc};
+                        ix->F, ix->tbase + ell + 1, W, ell, nc, fextra};
     out->index = ix;
   }
   CG_CUDA(cudaStreamSynchronize(s));

@@ -146,14 +146,29 @@ __device__ __forceinline__ uint32_t lookback(uint64_t* status, int64_t tile, int
   uint32_t excl = 0;
   int64_t j = tile - 1;
   const uint32_t ep = epoch & 0x3fffffffu;
+  // Walk back in windows of 8 predecessors whose statuses are loaded
+  // independently (8 loads in flight), accumulating aggregates until an
+  // inclusive prefix is found; an unpublished entry restarts the window there.
+  constexpr int kWin = 8;
   while (true) {
-    uint64_t s = ld_relaxed_u64(status + j * nslots + slot);
-    uint32_t flag = uint32_t(s >> 62);
-    uint32_t sep = uint32_t(s >> 32) & 0x3fffffffu;
-    if (flag == 0 || sep != ep) continue;  // not yet published in this epoch
-    excl += uint32_t(s);
-    if (flag == 2) break;
-    --j;
+    uint64_t s[kWin];
+#pragma unroll
+    for (int u = 0; u < kWin; ++u)
+      s[u] = (j - u >= 0) ? ld_relaxed_u64(status + (j - u) * nslots + slot) : 0;
+    bool done = false;
+    int consumed = 0;
+#pragma unroll
+    for (int u = 0; u < kWin; ++u) {
+      if (done || consumed < u) continue;  // stop at the first unusable entry
+      const uint32_t flag = uint32_t(s[u] >> 62);
+      const uint32_t sep = uint32_t(s[u] >> 32) & 0x3fffffffu;
+      if (flag == 0 || sep != ep) continue;  // not yet published: reload from here
+      excl += uint32_t(s[u]);
+      consumed = u + 1;
+      if (flag == 2) done = true;
+    }
+    if (done) break;
+    j -= consumed;
   }
   st_relaxed_u64(me, lb_pack(2, epoch, excl + agg));
   return excl;

@@ -50,7 +50,10 @@ void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, ui
 // ---------------------------------------------------------------- a4/a5 layers + dictionary
 // Prefix filter: per layer p a bitmap over the top (b_p + kFilterExtra) bits
 // of its cells; a probe whose target prefix bit is clear cannot hit.
-constexpr int kFilterExtra = 4;
+// default 7 (C5 probe: E=4 12.6 ms, 5 10.5, 6 8.9, 7 8.1, 8 7.9 ms on B200;
+// the bitmap costs 2^(b+E) bits per layer, ~16-32 bits per cell at E=7);
+// DictView.fextra holds the value in use (env CG_FILTER_EXTRA overrides).
+constexpr int kFilterExtra = 7;
 
 struct DictView {
   const uint64_t* keys;       // layer-major cell rows u64[n_c][W]
@@ -64,6 +67,7 @@ struct DictView {
   int W;
   int ell;
   int64_t n_cells;
+  int fextra;                 // filter prefix = b_p + fextra bits
 };
 
 // layer_off[p] = first position of popcount p in sorted_popc (p in [0, ell+1]).

@@ -64,8 +64,8 @@ __global__ void k_prefix_index(DictView d, const uint32_t* __restrict__ sp, uint
     const int b = d.tbits[p];
     uint32_t* Tp = T + d.tbase[p];
     const uint64_t w0 = d.keys[j * d.W];
-    // filter bit of the cell's (b + kFilterExtra)-bit prefix
-    const uint64_t y = w0 >> (64 - (b + kFilterExtra));
+    // filter bit of the cell's (b + fextra)-bit prefix
+    const uint64_t y = w0 >> (64 - (b + d.fextra));
     atomicOr(F + d.fbase[p] + (y >> 5), 1u << (y & 31));
     const int64_t x = prefix_of(w0, b);
     const int64_t xp = (uint32_t(j) == o) ? -1 : prefix_of(d.keys[(j - 1) * d.W], b);

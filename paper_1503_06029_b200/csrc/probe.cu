@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256)
     uint32_t surv = 0;  // bit k set = candidate k passed the filter
     const int kfar = min(b - 1, kmax);
     if (kfar >= 0) {
-      const int fbits = b + kFilterExtra;
+      const int fbits = b + d.fextra;
       const uint64_t y0 = v0 >> (64 - fbits);
       uint64_t z = ~v0 & (~0ull << (63 - kfar));  // zero bits with k <= kfar
       while (z) {
@@ -302,19 +302,70 @@ __global__ void __launch_bounds__(256)
         }
       }
     }
-    has = surv != 0;
-    while (__any_sync(kFull, has)) {
+    // Flatten the warp's surviving far probes (a few per cell, unevenly
+    // spread) so every lane works in every round: survivor g of the warp is
+    // the m-th set bit of the mask of lane `owner`, whose cell data arrive by
+    // shuffles.
+    const uint32_t nsv = __popc(surv);
+    uint32_t incl = nsv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total_sv = __shfl_sync(kFull, incl, 31);
+    const uint32_t tq_off = uint32_t(Tq - d.T);
+    const uint64_t my_v1 = (WC == 2) ? V(1) : 0ull;
+    for (uint32_t gb = 0; gb < total_sv; gb += 32) {
+      const uint32_t g = gb + lane;
+      int owner = 0;
+#pragma unroll
+      for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+        const uint32_t ic = __shfl_sync(kFull, incl, owner + s2 - 1);
+        if (ic <= g) owner += s2;
+      }
+      owner = min(owner, 31);
+      const uint32_t o_incl = __shfl_sync(kFull, incl, owner);
+      const uint32_t o_cnt = __shfl_sync(kFull, nsv, owner);
+      const uint32_t o_surv = __shfl_sync(kFull, surv, owner);
+      const uint64_t o_v0 = __shfl_sync(kFull, v0, owner);
+      const uint64_t o_v1 = __shfl_sync(kFull, my_v1, owner);
+      const int o_b = __shfl_sync(kFull, b, owner);
+      const uint32_t o_tq = __shfl_sync(kFull, tq_off, owner);
+      const uint32_t o_qend = __shfl_sync(kFull, qend, owner);
+      const uint64_t o_ci = __shfl_sync(kFull, ci, owner);
+      const int64_t o_j = __shfl_sync(kFull, j, owner);
       bool hit = false;
       uint64_t e = 0;
-      if (has) {
-        const int k = __ffs(surv) - 1;
-        surv &= surv - 1;
+      if (g < total_sv) {
+        // m-th set bit (from the least significant end) of the owner's mask
+        int m = int(g - (o_incl - o_cnt));
+        int k = 0;
+#pragma unroll
+        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+          const int c = __popc((o_surv >> k) & ((1u << s2) - 1u));
+          if (m >= c) {
+            m -= c;
+            k += s2;
+          }
+        }
+        CellWords<WC> OV;
+        if (WC == 2) {
+          OV.r[0] = o_v0;
+          OV.r[WC > 1 ? 1 : 0] = o_v1;
+        } else {
+          OV.load(d.keys + o_j * W);
+        }
         const uint64_t bm = 1ull << (63 - k);
-        const uint64_t t0 = v0 | bm;
-        const int64_t x = int64_t(t0 >> (64 - b));
-        uint32_t lo = Tq[x];
-        const uint32_t hi = Tq[x + 1];
+        const uint64_t t0 = o_v0 | bm;
+        const uint32_t* To = d.T + o_tq;
+        const int64_t x = int64_t(t0 >> (64 - o_b));
+        uint32_t lo = To[x];
+        const uint32_t hi = To[x + 1];
+        const uint32_t qend_ = o_qend;
         int64_t found = -1;
+        auto V = OV;  // the owner's cell from here on
+        const uint32_t qend = qend_;
         if (hi - lo <= 12) {
           // small bucket: compare up to four rows per step, loads independent
           for (uint32_t rr = lo; rr < hi && found < 0; rr += 4) {
@@ -351,9 +402,8 @@ __global__ void __launch_bounds__(256)
         }
         if (found >= 0) {
           hit = true;
-          e = ci | d.idx[found];
+          e = o_ci | d.idx[found];
         }
-        has = surv != 0;
       }
       emit(hit, e);
     }

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
 }
 
 template <class K, bool V>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 4)
     k_onesweep(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                uint32_t* __restrict__ vout, int64_t n, int shift,
                const uint32_t* __restrict__ bucket_base, uint64_t* status,
@@ -479,6 +479,9 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
   CG_CUDA(cudaMemcpyAsync(dbases.p, bases.data(), bases.size() * sizeof(uint32_t),
                           cudaMemcpyHostToDevice, s));
   const bool V = want_vals;
+  // as many resident tiles per SM as registers allow: prefer shared memory
+  if (V) CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  else CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const int TILE = V ? TileCfg<K, true>::TILE : TileCfg<K, false>::TILE;
   const int64_t tiles = (n + TILE - 1) / TILE;
   DevBuf<uint64_t> status(size_t(tiles) * kRadix, s);
