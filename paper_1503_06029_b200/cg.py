@@ -347,3 +347,60 @@ def release_host(*ptrs):
 
 def version() -> int:
     return lib().cg_version()
+
+
+# ---------------------------------------------------------------- distributed phases
+def dist_local(vecs: torch.Tensor, *, stream=None) -> torch.Tensor:
+    """cg_dist_local: pack + sort + dedupe this rank's rows -> sorted unique
+    run, int64 [c, W] (device)."""
+    if vecs.dtype != torch.uint8 or vecs.dim() != 2 or not vecs.is_cuda:
+        raise CgError(CG_EINVAL, "vecs must be a CUDA uint8 tensor [n, ell]")
+    vecs = vecs.contiguous()
+    n, ell = vecs.shape
+    stream = stream or torch.cuda.current_stream(vecs.device)
+    o, _, _ = _opts(stream, "sorted", True, -1, False, False)
+    c = cg_cells()
+    with torch.cuda.device(vecs.device):
+        _check(lib().cg_dist_local(ctypes.c_void_p(vecs.data_ptr()), n, ell, ctypes.byref(o),
+                                   ctypes.byref(c)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    return _wrap_cells(c, vecs.device)
+
+
+def dist_merge_probe(runs: torch.Tensor, counts, rank: int, ell: int, *, stream=None,
+                     want_stats=False):
+    """cg_dist_merge_probe: runs = int64 [G, stride, W] gathered sorted runs
+    (counts[g] valid rows each).  Returns (table int64 [n_c, W], this rank's
+    edges int32 [m_r, 2], stats)."""
+    if runs.dtype != torch.int64 or runs.dim() != 3 or not runs.is_cuda:
+        raise CgError(CG_EINVAL, "runs must be a CUDA int64 tensor [G, stride, W]")
+    runs = runs.contiguous()
+    G, stride, W = runs.shape
+    cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
+    stream = stream or torch.cuda.current_stream(runs.device)
+    o, _, st = _opts(stream, "sorted", True, -1, False, want_stats)
+    c, e = cg_cells(), cg_edges()
+    with torch.cuda.device(runs.device):
+        _check(lib().cg_dist_merge_probe(ctypes.c_void_p(runs.data_ptr()), cnt, G, stride, ell,
+                                         rank, ctypes.byref(o), ctypes.byref(c),
+                                         ctypes.byref(e)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    return (_wrap_cells(c, runs.device), _wrap_edges(e, runs.device),
+            _stats_dict(st) if want_stats else {})
+
+
+def dist_finalize(gathered: torch.Tensor, counts, *, stream=None) -> torch.Tensor:
+    """cg_dist_finalize: gathered = int32 [G, stride, 2] per-rank edge lists
+    (counts[g] valid pairs each) -> canonical edge list int32 [m, 2]."""
+    if gathered.dtype != torch.int32 or gathered.dim() != 3 or not gathered.is_cuda:
+        raise CgError(CG_EINVAL, "gathered must be a CUDA int32 tensor [G, stride, 2]")
+    gathered = gathered.contiguous()
+    G, stride, _ = gathered.shape
+    cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
+    stream = stream or torch.cuda.current_stream(gathered.device)
+    o, _, _ = _opts(stream, "sorted", True, -1, False, False)
+    e = cg_edges()
+    with torch.cuda.device(gathered.device):
+        _check(lib().cg_dist_finalize(ctypes.c_void_p(gathered.data_ptr()), cnt, G, stride,
+                                      ctypes.byref(o), ctypes.byref(e)))
+    return _wrap_edges(e, gathered.device)

@@ -320,9 +320,18 @@ struct Built {
   cg_index* index = nullptr;
 };
 
+// Distributed role of a build: cells only (phase 1), or probe only the
+// rank's share of the (popcount, canonical index) order (phase 2).
+struct Shard {
+  bool cells_only = false;
+  int rank = 0;
+  int world = 1;
+};
+
 // Runs a2..a7 given packed keys (u64[n][W], consumed as scratch).
 static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
-                            uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out) {
+                            uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out,
+                            const Shard& sh = Shard()) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
@@ -362,6 +371,23 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   tm.mark();  // 3: dedupe
   keys.reset();
   alt.reset();
+  if (sh.cells_only) {  // distributed phase 1: the sorted unique run
+    uint64_t* cout = nullptr;
+    if (nc * 2 < n) {
+      cout = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
+      CG_CUDA(cudaMemcpyAsync(cout, cellbuf.p, size_t(nc) * W * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      cout = cellbuf.release();
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+    out->cells = cout;
+    out->n_cells = nc;
+    if (st) {
+      st->n_cells = nc;
+      st->sort_passes = sst.passes;
+    }
+    return;
+  }
   // ---- a4 popcount layering: stable sort of (popc, canonical index)
   // buffers that become the cg_index (when requested) outlive the build
   const Mem ix = o.index_out ? Mem::Persist : Mem::Scratch;
@@ -410,16 +436,39 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, F.p, tbase.p + ell + 1, W, ell, nc, fextra};
   launch_build_prefix_index(dv, sp, T.p, F.p, s);
   tm.mark();  // 5: dict
+  // ---- which cells this build probes: all, or (distributed) the rank's
+  // share of the layer-major order cut at equal probe weight (candidate bits)
+  int64_t j_lo = 0, j_hi = nc;
+  if (sh.world > 1) {
+    const int64_t tiles = (nc + kWeightTile - 1) / kWeightTile;
+    DevBuf<uint32_t> tw(size_t(std::max<int64_t>(tiles, 1)), s);
+    launch_probe_weights(dv, llcp.p, sp, o.lcp_prune, tw.p, s);
+    uint32_t* htw = static_cast<uint32_t*>(host_stage(size_t(std::max<int64_t>(tiles, 1)) * 4));
+    CG_CUDA(cudaMemcpyAsync(htw, tw.p, size_t(tiles) * 4, cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint64_t> pre(tiles + 1, 0);
+    for (int64_t t = 0; t < tiles; ++t) pre[t + 1] = pre[t] + htw[t];
+    auto cut = [&](int r) -> int64_t {  // first tile whose prefix reaches r/G of the weight
+      if (r <= 0) return 0;
+      if (r >= sh.world) return tiles;
+      const uint64_t target = (pre[tiles] * uint64_t(r)) / uint64_t(sh.world);
+      return int64_t(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+    };
+    j_lo = std::min<int64_t>(nc, cut(sh.rank) * kWeightTile);
+    j_hi = std::min<int64_t>(nc, cut(sh.rank + 1) * kWeightTile);
+    if (sh.rank + 1 >= sh.world) j_hi = nc;
+    if (j_hi < j_lo) j_hi = j_lo;
+  }
   // ---- a6 probes + a7 warp-aggregated append
   DevBuf<unsigned long long> ctr(2, s);
-  uint64_t cap = std::max<uint64_t>(4 * uint64_t(nc), 1 << 16);
+  uint64_t cap = std::max<uint64_t>(4 * uint64_t(j_hi - j_lo), 1 << 16);
   DevBuf<uint64_t> eb(cap, s);
   unsigned long long* hc = static_cast<unsigned long long*>(host_stage(2 * sizeof(unsigned long long)));
   int reruns = 0;
   uint64_t m = 0, issued = 0;
   while (true) {
     CG_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * sizeof(unsigned long long), s));
-    launch_probe(dv, llcp.p, sp, o.lcp_prune, 0, nc, eb.p, cap, ctr.p, ctr.p + 1, s);
+    launch_probe(dv, llcp.p, sp, o.lcp_prune, j_lo, j_hi, eb.p, cap, ctr.p, ctr.p + 1, s);
     CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CG_CUDA(cudaStreamSynchronize(s));
     m = hc[0];
@@ -774,25 +823,157 @@ const char* cg_last_error(void) { return g_last_error.c_str(); }
 
 int cg_version(void) { return (0 << 16) | 1; }
 
-int cg_dist_local(const uint8_t*, int64_t, int32_t, const cg_opts*, cg_cells* run) {
+int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_opts* o_in,
+                  cg_cells* run) {
   if (run) std::memset(run, 0, sizeof(*run));
-  set_last_error("cg_dist_local: not implemented yet");
-  return CG_ENOTIMPL;
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  Built b;
+  try {
+    cg_edges dummy;
+    validate_common(n_local, ell, vecs, run, &dummy);
+    check_arch();
+    check_device_ptr(vecs, "vecs");
+    reset_counters();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    WsScope ws;
+    StageTimer tm;
+    tm.start(o.stats != nullptr, s);
+    DevBuf<uint32_t> flags(4, s);
+    CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
+    DevBuf<uint64_t> keys(size_t(n_local) * W, s);
+    launch_pack(vecs, n_local, ell, keys.p, flags.p, s);
+    tm.mark();
+    Shard sh;
+    sh.cells_only = true;
+    build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh);
+    store_counters(o.stats);
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (b.cells) dev_free(b.cells, nullptr);
+    return e.code;
+  }
+  run->words = b.cells;
+  run->n_cells = b.n_cells;
+  run->ell = ell;
+  run->words_per_cell = (ell + 63) / 64;
+  return CG_OK;
 }
 
-int cg_dist_merge_probe(const uint64_t*, const int64_t*, int32_t, int64_t, int32_t, int32_t,
-                        const cg_opts*, cg_cells* table, cg_edges* local_edges) {
+int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, int64_t stride,
+                        int32_t ell, int32_t rank, const cg_opts* o_in, cg_cells* table,
+                        cg_edges* local_edges) {
   if (table) std::memset(table, 0, sizeof(*table));
   if (local_edges) std::memset(local_edges, 0, sizeof(*local_edges));
-  set_last_error("cg_dist_merge_probe: not implemented yet");
-  return CG_ENOTIMPL;
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  o.index_out = nullptr;
+  Built b;
+  try {
+    if (!runs || !counts || !table || !local_edges) throw CgError{CG_EINVAL, "NULL argument"};
+    if (G < 1 || rank < 0 || rank >= G || stride < 0) throw CgError{CG_EINVAL, "bad G/rank/stride"};
+    if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    int64_t total = 0;
+    for (int g = 0; g < G; ++g) {
+      if (counts[g] < 0 || counts[g] > stride) throw CgError{CG_EINVAL, "counts[g] out of range"};
+      total += counts[g];
+    }
+    if (total < 1) throw CgError{CG_EINVAL, "no rows in the gathered runs"};
+    if (total > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "too many rows"};
+    check_arch();
+    check_device_ptr(runs, "runs");
+    reset_counters();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    WsScope ws;
+    StageTimer tm;
+    tm.start(o.stats != nullptr, s);
+    DevBuf<uint32_t> flags(4, s);
+    CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
+    // concatenate the runs (each sorted and unique; duplicates across runs
+    // are removed by the global sort + dedupe below)
+    DevBuf<uint64_t> keys(size_t(total) * W, s);
+    int64_t at = 0;
+    for (int g = 0; g < G; ++g) {
+      if (counts[g])
+        CG_CUDA(cudaMemcpyAsync(keys.p + at * W, runs + int64_t(g) * stride * W,
+                                size_t(counts[g]) * W * 8, cudaMemcpyDeviceToDevice, s));
+      at += counts[g];
+    }
+    tm.mark();
+    Shard sh;
+    sh.rank = rank;
+    sh.world = G;
+    build_from_keys(keys, total, ell, o, flags.p, tm, o.stats, &b, sh);
+    fill_stats(tm, total, o.stats);
+    store_counters(o.stats);
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (b.cells) dev_free(b.cells, nullptr);
+    if (b.edges) dev_free(b.edges, nullptr);
+    return e.code;
+  }
+  table->words = b.cells;
+  table->n_cells = b.n_cells;
+  table->ell = ell;
+  table->words_per_cell = (ell + 63) / 64;
+  local_edges->ij = b.edges;
+  local_edges->n_edges = b.n_edges;
+  return CG_OK;
 }
 
-int cg_dist_finalize(const uint32_t*, const int64_t*, int32_t, int64_t, const cg_opts*,
-                     cg_edges* edges) {
+int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G, int64_t stride,
+                     const cg_opts* o_in, cg_edges* edges) {
   if (edges) std::memset(edges, 0, sizeof(*edges));
-  set_last_error("cg_dist_finalize: not implemented yet");
-  return CG_ENOTIMPL;
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  uint64_t* eout = nullptr;
+  int64_t m = 0;
+  try {
+    if (!gathered || !counts || !edges) throw CgError{CG_EINVAL, "NULL argument"};
+    if (G < 1 || stride < 0) throw CgError{CG_EINVAL, "bad G/stride"};
+    for (int g = 0; g < G; ++g) {
+      if (counts[g] < 0 || counts[g] > stride) throw CgError{CG_EINVAL, "counts[g] out of range"};
+      m += counts[g];
+    }
+    check_arch();
+    if (m > 0) check_device_ptr(gathered, "gathered");
+    reset_counters();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    WsScope ws;
+    // (i, j) u32 pairs -> (i << 32 | j) keys, canonical sort, back to pairs.
+    // The per-rank lists are disjoint (each edge is emitted by the rank that
+    // owns its smaller endpoint), so no dedupe is needed.
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(gathered);
+    DevBuf<uint64_t> cat(size_t(std::max<int64_t>(m, 1)), s), k1(size_t(std::max<int64_t>(m, 1)), s),
+        k2(size_t(std::max<int64_t>(m, 1)), s);
+    int64_t at = 0;
+    for (int g = 0; g < G; ++g) {
+      if (counts[g])
+        CG_CUDA(cudaMemcpyAsync(cat.p + at, src + int64_t(g) * stride, size_t(counts[g]) * 8,
+                                cudaMemcpyDeviceToDevice, s));
+      at += counts[g];
+    }
+    eout = static_cast<uint64_t*>(dev_alloc(size_t(std::max<int64_t>(m, 1)) * 8, s));
+    if (m > 0) {
+      launch_rotate_edges(cat.p, m, k1.p, s);
+      uint64_t* ko = k1.p;
+      if (m > 1) radix_sort<uint64_t>(k1.p, k2.p, nullptr, nullptr, nullptr, false, m, 64, &ko, nullptr, s, nullptr);
+      launch_rotate_edges(ko, m, eout, s);
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (eout) dev_free(eout, nullptr);
+    return e.code;
+  }
+  edges->ij = reinterpret_cast<uint32_t*>(eout);
+  edges->n_edges = m;
+  return CG_OK;
 }
 
 }  // extern "C"

@@ -91,6 +91,11 @@ void launch_build_prefix_index(const DictView& d, const uint32_t* sorted_popc, u
 void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
                   int lcp_prune, int64_t j_lo, int64_t j_hi, uint64_t* edges, uint64_t cap,
                   unsigned long long* count, unsigned long long* issued, cudaStream_t s);
+// Probe weight (candidate bits + 1) summed per tile of kWeightTile
+// layer-major cells: the distributed query split cuts at equal weight.
+constexpr int kWeightTile = 4096;
+void launch_probe_weights(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
+                          int lcp_prune, uint32_t* tile_w, cudaStream_t s);
 // (i << 32 | j) -> u32 pair (i, j) little-endian.
 void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStream_t s);
 
