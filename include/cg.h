@@ -89,8 +89,11 @@ typedef struct {
 } cg_stats;
 
 enum {
-  CG_DICT_SORTED = 0, /* per-layer sorted array + 2^b prefix index, then binary search (default) */
-  CG_DICT_BSEARCH = 1 /* per-layer sorted array, plain binary search (no prefix index) */
+  CG_DICT_SORTED = 0,  /* popcount layers: per-layer sorted array + 2^b prefix index + filter */
+  CG_DICT_BSEARCH = 1, /* popcount layers, plain per-layer binary search (no prefix index) */
+  CG_DICT_GLOBAL = 2   /* one prefix index + filter over the canonical table; the probe
+                          writes the edge list in canonical order (no edge sort).  Default
+                          of cg_opts_init; an index_out request uses CG_DICT_SORTED. */
 };
 
 typedef struct {

@@ -21,8 +21,8 @@ LIB_PATH = os.path.join(HERE, "lib", "libcg.so")
 
 CG_OK, CG_EINVAL, CG_EINPUT, CG_ENOMEM, CG_ECUDA, CG_ETOOBIG, CG_EARCH, CG_ENOTIMPL = (
     0, -1, -2, -3, -4, -5, -6, -7)
-CG_DICT_SORTED, CG_DICT_BSEARCH = 0, 1
-DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH}
+CG_DICT_SORTED, CG_DICT_BSEARCH, CG_DICT_GLOBAL = 0, 1, 2
+DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH, "global": CG_DICT_GLOBAL}
 
 
 class CgError(RuntimeError):
@@ -238,7 +238,7 @@ def _stats_dict(st: cg_stats) -> dict:
 
 
 def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
-          dict_kind="sorted", lcp_prune: bool = True, bucket_log2: int = -1,
+          dict_kind="global", lcp_prune: bool = True, bucket_log2: int = -1,
           want_index: bool = False, want_stats: bool = False,
           sort_kind="auto") -> BuildResult:
     """cg_build_ex on a CUDA uint8 tensor [n, ell] of 0/1 bytes."""
@@ -266,7 +266,7 @@ def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
     return res
 
 
-def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="sorted",
+def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="global",
                  lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False):
     """cg_build_packed_ex on CUDA int64 [n, ceil(ell/64)] MSB-first words."""
     if words.dim() != 2 or words.dtype != torch.int64 or not words.is_cuda:
@@ -288,7 +288,7 @@ def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="sorte
     return res
 
 
-def build_host(vecs_host: torch.Tensor, *, device=None, stream=None, dict_kind="sorted",
+def build_host(vecs_host: torch.Tensor, *, device=None, stream=None, dict_kind="global",
                lcp_prune=True, bucket_log2=-1, want_stats=False):
     """cg_build_host: uint8 [n, ell] HOST tensor (pinned for full speed) in,
     numpy-compatible host results out: (cells int64 [nc, W], edges int32 [m, 2],
@@ -329,7 +329,7 @@ def build_host_raw(vecs_host: torch.Tensor, *, stream=None, want_stats=False):
     n, ell = vecs_host.shape
     device = torch.device("cuda")
     stream = stream or torch.cuda.current_stream(device)
-    o, ih, st = _opts(stream, "sorted", True, -1, False, want_stats)
+    o, ih, st = _opts(stream, "global", True, -1, False, want_stats)
     hc, he = ctypes.c_void_p(), ctypes.c_void_p()
     nc, ne = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().cg_build_host(ctypes.c_void_p(vecs_host.data_ptr()), n, ell, ctypes.byref(o),
@@ -368,17 +368,19 @@ def dist_local(vecs: torch.Tensor, *, stream=None) -> torch.Tensor:
 
 
 def dist_merge_probe(runs: torch.Tensor, counts, rank: int, ell: int, *, stream=None,
-                     want_stats=False):
+                     want_stats=False, dict_kind="global"):
     """cg_dist_merge_probe: runs = int64 [G, stride, W] gathered sorted runs
     (counts[g] valid rows each).  Returns (table int64 [n_c, W], this rank's
-    edges int32 [m_r, 2], stats)."""
+    edges int32 [m_r, 2], stats).  dict_kind "global": the rank probes a
+    contiguous canonical range; "sorted": its share of the (popcount layer,
+    index) order cut at equal probe weight."""
     if runs.dtype != torch.int64 or runs.dim() != 3 or not runs.is_cuda:
         raise CgError(CG_EINVAL, "runs must be a CUDA int64 tensor [G, stride, W]")
     runs = runs.contiguous()
     G, stride, W = runs.shape
     cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
     stream = stream or torch.cuda.current_stream(runs.device)
-    o, _, st = _opts(stream, "sorted", True, -1, False, want_stats)
+    o, _, st = _opts(stream, dict_kind, True, -1, False, want_stats)
     c, e = cg_cells(), cg_edges()
     with torch.cuda.device(runs.device):
         _check(lib().cg_dist_merge_probe(ctypes.c_void_p(runs.data_ptr()), cnt, G, stride, ell,

@@ -388,6 +388,107 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
     return;
   }
+  if (o.dict_kind == CG_DICT_GLOBAL && !o.index_out) {
+    tm.mark();  // 4: layers (implicit in the global dictionary)
+    // ---- a5 one prefix index + filter over the canonical table
+    const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 2;
+    int b = 0;
+    while (b < 28 && (uint64_t(nc) >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
+    int fextra = kFilterExtra;
+    if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
+    DevBuf<uint32_t> T((size_t(1) << b) + 1, s);
+    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s);
+    CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
+    build_global_index(cellbuf.p, nc, W, b, fextra, T.p, F.p, s);
+    tm.mark();  // 5: dict
+    GlobalDict g{cellbuf.p, lcp.p, T.p, F.p, b, fextra, W, ell, nc};
+    // ---- a6 + a7: probes write the canonical edge list directly
+    int64_t i_lo = 0, i_hi = nc;
+    if (sh.world > 1) {  // distributed: contiguous canonical ranges
+      i_lo = nc * sh.rank / sh.world;
+      i_hi = nc * (sh.rank + 1) / sh.world;
+    }
+    const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
+    DevBuf<uint64_t> status(size_t(ntiles), s);
+    DevBuf<uint32_t> ticket(2, s);
+    DevBuf<unsigned long long> ctr(4, s);
+    DevBuf<uint4> ovf(size_t(ntiles), s);
+    uint64_t cap = std::max<uint64_t>(2 * uint64_t(i_hi - i_lo), 1 << 16);
+    DevBuf<uint64_t> eo(cap, s, Mem::Persist);
+    unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
+    int reruns = 0;
+    uint64_t m = 0, issued = 0, novf = 0;
+    while (true) {
+      CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * 8, s));
+      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
+      CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, eo.p, cap, status.p, ticket.p, ctr.p,
+                          ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
+      CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      m = hc[0];
+      issued = hc[1];
+      novf = uint32_t(hc[2] & 0xffffffffu);
+      if (m <= cap) break;
+      cap = m;
+      eo.alloc(cap, s, Mem::Persist);
+      ++reruns;
+    }
+    if (novf) {
+      // tiles whose hits overflowed the shared buffer: re-run each in spill
+      // mode, sort its hits and drop them into its slot range
+      std::vector<uint4> hv(novf);
+      CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      const int tc = probe_global_tile_cells();
+      for (const uint4& t : hv) {
+        const uint32_t cnt = t.z;
+        DevBuf<uint64_t> sp1(cnt, s), sp2(cnt, s), rot(cnt, s);
+        DevBuf<uint64_t> st1(1, s);
+        CG_CUDA(cudaMemsetAsync(st1.p, 0, 8, s));
+        CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
+        CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
+        const int64_t lo = i_lo + int64_t(t.x) * tc, hi = std::min<int64_t>(i_hi, lo + tc);
+        launch_probe_global(g, o.lcp_prune, lo, hi, nullptr, 0, st1.p, ticket.p, ctr.p + 3,
+                            ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, cnt, ctr.p + 2, s);
+        uint64_t* so = sp1.p;
+        if (cnt > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, cnt, 64, &so, nullptr, s, nullptr);
+        launch_rotate_edges(so, cnt, eo.p + t.y, s);
+      }
+      CG_CUDA(cudaStreamSynchronize(s));
+    }
+    tm.mark();  // 6: probe
+    tm.mark();  // 7: edges (already canonical)
+    uint64_t* eout = nullptr;
+    if (m * 2 < cap) {
+      eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
+      if (m) CG_CUDA(cudaMemcpyAsync(eout, eo.p, m * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      eout = eo.release();
+    }
+    uint64_t* cout = nullptr;
+    if (nc * 2 < n) {
+      cout = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
+      CG_CUDA(cudaMemcpyAsync(cout, cellbuf.p, size_t(nc) * W * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      cout = cellbuf.release();
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+    out->cells = cout;
+    out->n_cells = nc;
+    out->edges = reinterpret_cast<uint32_t*>(eout);
+    out->n_edges = int64_t(m);
+    if (st) {
+      st->n_cells = nc;
+      st->n_edges = int64_t(m);
+      st->logical_probes = nc * int64_t(ell);
+      st->issued_probes = int64_t(issued);
+      st->sort_passes = sst.passes;
+      st->probe_reruns = reruns + int(novf);
+    }
+    return;
+  }
   // ---- a4 popcount layering: stable sort of (popc, canonical index)
   // buffers that become the cg_index (when requested) outlive the build
   const Mem ix = o.index_out ? Mem::Persist : Mem::Scratch;
@@ -479,12 +580,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     ++reruns;
   }
   tm.mark();  // 6: probe
-  // ---- a7 canonical sort of (i << 32 | j), then (i, j) pairs
-  uint64_t* eo = eb.p;
-  DevBuf<uint64_t> eb_alt(std::max<uint64_t>(m, 1), s);
-  if (m > 1) radix_sort<uint64_t>(eb.p, eb_alt.p, nullptr, nullptr, nullptr, false, int64_t(m), 64, &eo, nullptr, s, nullptr);
+  // ---- a7 canonical order: radix sort of (i << 32 | j); CG_EDGE_PLACE=1
+  // selects placement by source cell (count, scan, place, fix), which
+  // measured slower at C5 (3.6 vs 3.0 ms: scattered counter atomics)
   uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
-  launch_rotate_edges(eo, int64_t(m), eout, s);
+  static const bool edge_place = std::getenv("CG_EDGE_PLACE") && std::atoi(std::getenv("CG_EDGE_PLACE")) == 1;
+  if (edge_place) {
+    place_edges(eb.p, int64_t(m), nc, eout, s);
+  } else {
+    uint64_t* eo = eb.p;
+    DevBuf<uint64_t> eb_alt(std::max<uint64_t>(m, 1), s);
+    if (m > 1) radix_sort<uint64_t>(eb.p, eb_alt.p, nullptr, nullptr, nullptr, false, int64_t(m), 64, &eo, nullptr, s, nullptr);
+    launch_rotate_edges(eo, int64_t(m), eout, s);
+  }
   tm.mark();  // 7: edges
   // ---- outputs
   uint64_t* cout = nullptr;
@@ -574,7 +682,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
   try {
     validate_common(n, ell, vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words),
                     cells, edges);
-    if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH)
+    if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
+        o.dict_kind != CG_DICT_GLOBAL)
       throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
     check_arch();
     check_device_ptr(vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words), "input");
@@ -627,7 +736,7 @@ extern "C" {
 void cg_opts_init(cg_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
-  o->dict_kind = CG_DICT_SORTED;
+  o->dict_kind = CG_DICT_GLOBAL;
   o->lcp_prune = 1;
   o->bucket_log2 = -1;
 }

@@ -96,8 +96,39 @@ void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* 
 constexpr int kWeightTile = 4096;
 void launch_probe_weights(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
                           int lcp_prune, uint32_t* tile_w, cudaStream_t s);
+// Canonical (i, j) u32 pairs from unordered (i << 32 | j) hits without a
+// full sort (count per source, scan, place, per-cell fix-up); edges.cu.
+void place_edges(const uint64_t* hits, int64_t m, int64_t nc, uint64_t* out, cudaStream_t s);
 // (i << 32 | j) -> u32 pair (i, j) little-endian.
 void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- global dictionary
+// (probe_global.cu): one prefix index + filter over the canonical table; the
+// probe writes the canonical edge list directly (tile order + look-back).
+struct GlobalDict {
+  const uint64_t* keys;  // canonical cells u64[n_c][W]
+  const uint16_t* lcp;   // [n_c] lcp with the next cell (0xffff: last)
+  const uint32_t* T;     // [2^b + 1]
+  const uint32_t* F;     // 2^(b + fextra) bits
+  int b;
+  int fextra;
+  int W;
+  int ell;
+  int64_t n_cells;
+};
+void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
+                        uint32_t* F, cudaStream_t s);
+// status/ticket: look-back state for ceil((i_hi - i_lo) / 256) tiles (zeroed);
+// *total = number of edges; tiles whose hits overflow the shared buffer are
+// listed in ovf (tile, base, count) and must be re-run in spill mode
+// (spill != nullptr: unordered append to spill[0..spill_cap), *spill_n).
+void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
+                         uint64_t* out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                         unsigned long long* total, unsigned long long* issued, uint4* ovf,
+                         uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
+                         unsigned long long* spill_n, cudaStream_t s);
+int64_t probe_global_tiles(int64_t n);
+int probe_global_tile_cells();
 
 // ---------------------------------------------------------------- cg_query
 void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,

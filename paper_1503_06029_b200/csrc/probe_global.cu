@@ -1,0 +1,442 @@
+// probe_global.cu -- a5/a6/a7 over ONE prefix-indexed dictionary on the
+// canonical cell table, with the edge list produced in canonical order by
+// the probe itself (no edge sort).
+//
+// Dictionary (a5): the canonical table V (sorted, unique) with a 2^b prefix
+// index T (T[x] = first cell whose top b bits are >= x; ~4-8 cells per
+// bucket) and a prefix filter F of 2^(b+E) bits.  The popcount layering of
+// the north star is implicit: a hit R of cell V must satisfy R ⊇ V and
+// popc(R) = popc(V) + 1 (the adjacent layer), which the subset/equality tests
+// enforce; the layered dictionary remains available (CG_DICT_SORTED).
+//
+// Probes (a6), one thread per canonical cell V_i, candidate bits = zero bits
+// k <= lcp(V_i, V_{i+1}) (exact LCP pruning, see probe.cu):
+//   near (k >= b): every target shares V_i's b-prefix and is > V_i, so it is
+//     one of the cells right after i in the same bucket -- the next rows of
+//     the table, already in L1 for the warp.  Row R is a hit iff R ⊇ V_i and
+//     popc(R ^ V_i) = 1.
+//   far (k < b): filter bit of the target's (b+E)-prefix, then the bucket
+//     T[x]..T[x+1] of the survivors is compared (warp-flattened rounds).
+// Output (a7): a CTA owns a contiguous tile of cells; its hits are collected
+// in shared memory, sorted there by (i, j), and written at the tile's global
+// offset found by decoupled look-back in tile order -- so the concatenation
+// over tiles IS the canonical edge list.  A tile with more hits than the
+// shared buffer spills them (unordered) and records its slot range; the host
+// fixes those ranges after the kernel (sort of the spilled hits).
+#include "kernels.cuh"
+
+namespace cgk {
+namespace {
+
+constexpr int kTileCells = 256;     // cells per tile = threads per CTA
+constexpr int kTileEdgeCap = 4096;  // shared-memory edge buffer per tile
+
+template <int WC>
+struct GRow {
+  uint64_t w[WC > 0 ? WC : 1];
+};
+
+__global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, int W, int b,
+                               int fb, uint32_t* __restrict__ T, uint32_t* __restrict__ F) {
+  const int64_t top = int64_t(1) << b;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nc;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t w0 = cells[i * W];
+    const int64_t x = b ? int64_t(w0 >> (64 - b)) : 0;
+    const int64_t xp = i == 0 ? -1 : (b ? int64_t(cells[(i - 1) * W] >> (64 - b)) : 0);
+    for (int64_t q = xp + 1; q <= x; ++q) T[q] = uint32_t(i);
+    if (i == nc - 1)
+      for (int64_t q = x + 1; q <= top; ++q) T[q] = uint32_t(nc);
+    const uint64_t y = w0 >> (64 - fb);
+    atomicOr(F + (y >> 5), 1u << (y & 31));
+  }
+}
+
+template <int WC>
+__global__ void __launch_bounds__(kTileCells)
+    k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
+                   uint64_t* __restrict__ out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                   unsigned long long* total, unsigned long long* issued,
+                   uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
+                   uint4* __restrict__ ovf, uint32_t* ovf_n) {
+  __shared__ uint64_t ebuf[kTileEdgeCap];
+  __shared__ uint32_t s_cnt;
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t lt = lanemask_lt();
+  const int W = WC > 0 ? WC : g.W;
+  const int b = g.b;
+  const int fb = g.b + g.fextra;
+  unsigned long long my_issued = 0;
+
+  while (true) {
+    if (tid == 0) {
+      s_tile = atomicAdd(ticket, 1u);
+      s_cnt = 0;
+    }
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int64_t i = i_lo + tile * kTileCells + tid;
+    const bool valid = i < i_hi;
+    // ---- the cell
+    const uint64_t* Vp = g.keys + (valid ? i : 0) * W;
+    uint64_t v[WC > 0 ? WC : 1];
+    if (WC > 0) {
+#pragma unroll
+      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) v[w] = valid ? Vp[w] : 0ull;
+    }
+    auto V = [&](int w) -> uint64_t {
+      if (WC > 0) {
+        uint64_t r = v[0];
+#pragma unroll
+        for (int u = 1; u < (WC > 0 ? WC : 1); ++u)
+          if (u == w) r = v[u];
+        return r;
+      }
+      return Vp[w];
+    };
+    int kmax = -1;
+    if (valid) {
+      if (lcp_prune) {
+        const int l = g.lcp[i];
+        kmax = (l == 0xffff) ? -1 : min(l, g.ell - 1);
+      } else {
+        kmax = g.ell - 1;
+      }
+    }
+    const uint64_t v0 = V(0);
+    const uint64_t ci = uint64_t(i) << 32;
+
+    // append a round's hits to the tile buffer (one shared atomic per warp);
+    // spill mode (overflow re-run): append unordered to the global spill list
+    auto emit = [&](bool hit, uint64_t e) {
+      const uint32_t hb = __ballot_sync(kFull, hit);
+      if (hb) {
+        const int leader = __ffs(hb) - 1;
+        if (spill) {
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(spill_n, (unsigned long long)__popc(hb));
+          base = __shfl_sync(kFull, base, leader);
+          if (hit) {
+            const unsigned long long pos = base + __popc(hb & lt);
+            if (pos < spill_cap) spill[pos] = e;
+          }
+          return;
+        }
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&s_cnt, uint32_t(__popc(hb)));
+        base = __shfl_sync(kFull, base, leader);
+        if (hit) {
+          const uint32_t pos = base + __popc(hb & lt);
+          if (pos < kTileEdgeCap) ebuf[pos] = e;
+        }
+      }
+    };
+
+    // ---- near: rows i+1.. in V's own b-prefix bucket
+    const bool near_on = kmax >= b;
+    const uint64_t pv = b ? (v0 >> (64 - b)) : 0ull;
+    int64_t bucket_end = i + 1;
+    if (near_on) bucket_end = g.T[pv + 1];
+    const bool near_scan = near_on && (bucket_end - (i + 1) <= 16);
+    int64_t r = i + 1;
+    while (__any_sync(kFull, near_scan && r < bucket_end)) {
+      bool hit[4] = {false, false, false, false};
+      if (near_scan && r < bucket_end) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t rr = r + u;
+          if (rr < bucket_end) {
+            const uint64_t* R = g.keys + rr * W;
+            uint64_t miss = 0;
+            int diff = 0;
+            if (WC == 2) {
+              const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(R);
+              miss = (v0 & ~x.x) | (V(1) & ~x.y);
+              diff = __popcll(x.x ^ v0) + __popcll(x.y ^ V(1));
+            } else {
+              const int n = WC > 0 ? WC : W;
+              for (int w = 0; w < n; ++w) {
+                const uint64_t x = R[w];
+                miss |= V(w) & ~x;
+                diff += __popcll(x ^ V(w));
+              }
+            }
+            hit[u] = (miss == 0) && (diff == 1);
+            ++my_issued;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) emit(hit[u], ci | uint64_t(r + u));
+      if (near_scan) r += 4;
+    }
+    // big bucket (skewed data): per candidate binary search in (i, bucket_end)
+    {
+      bool has = near_on && !near_scan;
+      int cw = has ? (kmax >> 6) : 0;
+      const int cw_lo = b >> 6;
+      auto nmask = [&](int w) -> uint64_t {
+        uint64_t m = ~V(w);
+        if (w == (kmax >> 6)) m &= ~0ull << (63 - (kmax & 63));
+        if (w == cw_lo && b > 0) m &= ~0ull >> b;
+        return m;
+      };
+      uint64_t z = has ? nmask(cw) : 0ull;
+      auto next = [&]() -> bool {
+        while (z == 0 && cw > cw_lo) {
+          --cw;
+          z = nmask(cw);
+        }
+        return z != 0;
+      };
+      has = has && next();
+      while (__any_sync(kFull, has)) {
+        bool hit = false;
+        uint64_t e = 0;
+        if (has) {
+          const uint64_t bm = z & (~z + 1);
+          z ^= bm;
+          const int fw = cw;
+          ++my_issued;
+          int64_t lo = i + 1, len = bucket_end - (i + 1);
+          while (len > 0) {
+            const int64_t half = len >> 1;
+            const uint64_t* R = g.keys + (lo + half) * W;
+            int c = 0;
+            const int n = WC > 0 ? WC : W;
+            for (int w = 0; w < n && c == 0; ++w) {
+              const uint64_t a = R[w], tv = V(w) | (w == fw ? bm : 0ull);
+              c = a < tv ? -1 : (a > tv ? 1 : 0);
+            }
+            if (c < 0) {
+              lo += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          if (lo < bucket_end) {
+            const uint64_t* R = g.keys + lo * W;
+            bool eq = true;
+            const int n = WC > 0 ? WC : W;
+            for (int w = 0; w < n && eq; ++w) eq = R[w] == (V(w) | (w == fw ? bm : 0ull));
+            if (eq) {
+              hit = true;
+              e = ci | uint64_t(lo);
+            }
+          }
+          has = next();
+        }
+        emit(hit, e);
+      }
+    }
+    // ---- far: zero bits k < min(b, kmax + 1) (word 0, b <= 28): filter
+    uint32_t surv = 0;
+    const int kfar = min(b - 1, kmax);
+    if (kfar >= 0) {
+      const uint64_t y0 = v0 >> (64 - fb);
+      uint64_t z = ~v0 & (~0ull << (63 - kfar));
+      while (z) {
+        int ks[4];
+        uint32_t fw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ks[u] = -1;
+          fw[u] = 0;
+          if (z) {
+            const int c = __clzll(z);
+            z &= ~(1ull << (63 - c));
+            ks[u] = c;
+            fw[u] = __ldg(g.F + ((y0 | (1ull << (fb - 1 - c))) >> 5));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (ks[u] >= 0) {
+            const uint64_t y = y0 | (1ull << (fb - 1 - ks[u]));
+            ++my_issued;
+            if ((fw[u] >> (y & 31)) & 1u) surv |= 1u << ks[u];
+          }
+        }
+      }
+    }
+    // ---- far survivors, flattened over the warp
+    const uint32_t nsv = __popc(surv);
+    uint32_t incl = nsv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total_sv = __shfl_sync(kFull, incl, 31);
+    const uint64_t my_v1 = (WC == 2) ? V(1) : 0ull;
+    for (uint32_t gb = 0; gb < total_sv; gb += 32) {
+      const uint32_t gg = gb + lane;
+      int owner = 0;
+#pragma unroll
+      for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+        const uint32_t ic = __shfl_sync(kFull, incl, owner + s2 - 1);
+        if (ic <= gg) owner += s2;
+      }
+      owner = min(owner, 31);
+      const uint32_t o_incl = __shfl_sync(kFull, incl, owner);
+      const uint32_t o_cnt = __shfl_sync(kFull, nsv, owner);
+      const uint32_t o_surv = __shfl_sync(kFull, surv, owner);
+      const uint64_t o_v0 = __shfl_sync(kFull, v0, owner);
+      const uint64_t o_v1 = __shfl_sync(kFull, my_v1, owner);
+      const int64_t o_i = __shfl_sync(kFull, i, owner);
+      bool hit = false;
+      uint64_t e = 0;
+      if (gg < total_sv) {
+        int m = int(gg - (o_incl - o_cnt));
+        int k = 0;
+#pragma unroll
+        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+          const int c = __popc((o_surv >> k) & ((1u << s2) - 1u));
+          if (m >= c) {
+            m -= c;
+            k += s2;
+          }
+        }
+        const uint64_t bm = 1ull << (63 - k);
+        const uint64_t t0 = o_v0 | bm;
+        const int64_t x = int64_t(t0 >> (64 - b));
+        const uint32_t lo = g.T[x], hi = g.T[x + 1];
+        const uint64_t* OV = g.keys + o_i * W;  // owner's row (W > 2 path)
+        int64_t found = -1;
+        if (hi - lo <= 12) {
+          for (uint32_t rr = lo; rr < hi && found < 0; rr += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t ru = rr + u;
+              if (ru < hi) {
+                const uint64_t* R = g.keys + int64_t(ru) * W;
+                bool eq;
+                if (WC == 2) {
+                  const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(R);
+                  eq = xv.x == t0 && xv.y == o_v1;
+                } else {
+                  eq = R[0] == t0;
+                  const int n = WC > 0 ? WC : W;
+                  for (int w = 1; w < n && eq; ++w) eq = R[w] == OV[w];
+                }
+                if (eq) found = ru;
+              }
+            }
+          }
+        } else {
+          int64_t lo2 = lo, len = int64_t(hi) - lo;
+          while (len > 0) {
+            const int64_t half = len >> 1;
+            const uint64_t* R = g.keys + (lo2 + half) * W;
+            int c = R[0] < t0 ? -1 : (R[0] > t0 ? 1 : 0);
+            const int n = WC > 0 ? WC : W;
+            for (int w = 1; w < n && c == 0; ++w) {
+              const uint64_t ow = (WC == 2) ? o_v1 : OV[w];
+              c = R[w] < ow ? -1 : (R[w] > ow ? 1 : 0);
+            }
+            if (c < 0) {
+              lo2 += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          if (lo2 < int64_t(hi)) {
+            const uint64_t* R = g.keys + lo2 * W;
+            bool eq = R[0] == t0;
+            const int n = WC > 0 ? WC : W;
+            for (int w = 1; w < n && eq; ++w) eq = R[w] == ((WC == 2) ? o_v1 : OV[w]);
+            if (eq) found = lo2;
+          }
+        }
+        if (found >= 0) {
+          hit = true;
+          e = (uint64_t(o_i) << 32) | uint64_t(found);
+        }
+      }
+      emit(hit, e);
+    }
+    __syncthreads();
+    if (spill) continue;  // spill mode: no ordered output
+    // ---- tile output: global offset by look-back, local sort, write
+    const uint32_t cnt = s_cnt;
+    if (tid == 0) {
+      s_base = lookback(status, tile, 1, 0, cnt, 1);
+      if (tile == ntiles - 1) *total = (unsigned long long)s_base + cnt;
+    }
+    __syncthreads();
+    const uint32_t base = s_base;
+    if (cnt > kTileEdgeCap) {
+      // rare: re-emit is impossible here, so the tile's hits beyond the
+      // buffer were dropped -> record the slot range; the host re-runs the
+      // tile's cells in spill mode (see run_probe_global)
+      if (tid == 0) {
+        const uint32_t k = atomicAdd(ovf_n, 1u);
+        ovf[k] = make_uint4(uint32_t(tile), base, cnt, 0u);
+      }
+    } else {
+      int P = 1;
+      while (P < int(cnt)) P <<= 1;
+      for (int q = cnt + tid; q < P; q += kTileCells) ebuf[q] = ~0ull;
+      __syncthreads();
+      for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int p = tid; p < (P >> 1); p += kTileCells) {
+            const int a = 2 * j * (p / j) + (p % j);
+            const int c = a + j;
+            const bool up = (a & kk) == 0;
+            const uint64_t x = ebuf[a], y = ebuf[c];
+            if ((y < x) == up) {
+              ebuf[a] = y;
+              ebuf[c] = x;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (uint32_t q = tid; q < cnt; q += kTileCells) {
+        const uint64_t pos = uint64_t(base) + q;
+        const uint64_t k = ebuf[q];
+        if (pos < cap) out[pos] = (k >> 32) | (k << 32);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_issued += __shfl_xor_sync(kFull, my_issued, o);
+  if (lane == 0 && my_issued) atomicAdd(issued, my_issued);
+}
+
+}  // namespace
+
+void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
+                        uint32_t* F, cudaStream_t s) {
+  int64_t blocks = std::min<int64_t>((nc + 255) / 256, int64_t(num_sms()) * 16);
+  k_global_index<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(cells, nc, W, b, b + fextra, T, F);
+  CG_LAUNCH_CHECK();
+}
+
+void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
+                         uint64_t* out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                         unsigned long long* total, unsigned long long* issued, uint4* ovf,
+                         uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
+                         unsigned long long* spill_n, cudaStream_t s) {
+  const int64_t ntiles = (i_hi - i_lo + kTileCells - 1) / kTileCells;
+  if (ntiles <= 0) return;
+  const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms()) * 8));
+  switch (g.W) {
+    case 1: k_probe_global<1><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
+    case 2: k_probe_global<2><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
+    default: k_probe_global<0><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
+  }
+  CG_LAUNCH_CHECK();
+}
+
+int64_t probe_global_tiles(int64_t n) { return (n + kTileCells - 1) / kTileCells; }
+int probe_global_tile_cells() { return kTileCells; }
+
+}  // namespace cgk

@@ -34,7 +34,7 @@ def _pad_stack(ts, dtype, tail):
     return out
 
 
-def logical_ranks(cg, x: np.ndarray, G: int):
+def logical_ranks(cg, x: np.ndarray, G: int, dict_kind="global"):
     n, ell = x.shape
     W = (ell + 63) // 64
     xt = torch.from_numpy(x).cuda()
@@ -43,7 +43,7 @@ def logical_ranks(cg, x: np.ndarray, G: int):
     stacked = _pad_stack(runs, torch.int64, (W,))
     tables, edges = [], []
     for r in range(G):
-        t, e, _ = cg.dist_merge_probe(stacked, counts, r, ell)
+        t, e, _ = cg.dist_merge_probe(stacked, counts, r, ell, dict_kind=dict_kind)
         tables.append(t)
         edges.append(e)
     for t in tables[1:]:
@@ -55,14 +55,15 @@ def logical_ranks(cg, x: np.ndarray, G: int):
             ecounts)
 
 
+@pytest.mark.parametrize("dict_kind", ["global", "sorted"])
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
-def test_logical_ranks_match_single_build(cg, G):
+def test_logical_ranks_match_single_build(cg, G, dict_kind):
     x = synth.clustered_bytes(G, 60000, 100, n_centers=6, max_flips=3)
     x = np.concatenate([x, x[:9999]])
     res = cg.build(torch.from_numpy(x).cuda())
     want_c = res.cells.cpu().numpy().view(np.uint64)
     want_e = res.edges.cpu().numpy().view(np.uint32)
-    c, e, ecounts = logical_ranks(cg, x, G)
+    c, e, ecounts = logical_ranks(cg, x, G, dict_kind)
     np.testing.assert_array_equal(c, want_c)
     np.testing.assert_array_equal(e, want_e)
     if G > 1:

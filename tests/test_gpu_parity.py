@@ -169,6 +169,26 @@ def test_hypercube_closed_form(cg):
         np.testing.assert_array_equal(e, want)  # m = ell * 2^(ell-1), every degree = ell
 
 
+@pytest.mark.parametrize("dict_kind", ["global", "sorted"])
+def test_dense_ball_tile_overflow(cg, dict_kind):
+    """All vectors of weight <= 2 (ell = 100): weight-1 cells have 99
+    out-edges each, so a 256-cell tile of the canonical-order probe overflows
+    its shared edge buffer and takes the spill path."""
+    ell = 100
+    rows = [np.zeros(ell, np.uint8)]
+    for a in range(ell):
+        r = np.zeros(ell, np.uint8)
+        r[a] = 1
+        rows.append(r)
+        for b2 in range(a + 1, ell):
+            r2 = r.copy()
+            r2[b2] = 1
+            rows.append(r2)
+    x = np.stack(rows)[np.random.default_rng(0).permutation(len(rows))]
+    c, e, res = assert_parity(cg, x, dict_kind=dict_kind, want_stats=True)
+    assert e.shape[0] == ell + ell * (ell - 1)
+
+
 def test_all_identical_and_single(cg):
     c, e, _ = assert_parity(cg, np.ones((1000, 70), np.uint8))
     assert c.shape[0] == 1 and e.shape[0] == 0
@@ -189,7 +209,8 @@ def test_multiset_x3_and_permutation(cg):
 def test_options_agree(cg):
     x = synth.clustered_bytes(8, 30000, 150, n_centers=8, max_flips=3)
     c0, e0, r0 = gpu_build(cg, x, want_stats=True)
-    for kw in (dict(lcp_prune=False), dict(dict_kind="bsearch"), dict(bucket_log2=0),
+    for kw in (dict(lcp_prune=False), dict(dict_kind="bsearch"), dict(dict_kind="sorted"),
+               dict(dict_kind="sorted", lcp_prune=False), dict(bucket_log2=0),
                dict(bucket_log2=6)):
         c1, e1, r1 = gpu_build(cg, x, want_stats=True, **kw)
         np.testing.assert_array_equal(c0, c1)
