@@ -409,20 +409,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       i_hi = nc * (sh.rank + 1) / sh.world;
     }
     const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
-    DevBuf<uint64_t> status(size_t(ntiles), s);
+    DevBuf<uint32_t> tinfo(2 * size_t(ntiles), s);  // [count | block position]
     DevBuf<uint32_t> ticket(2, s);
     DevBuf<unsigned long long> ctr(4, s);
     DevBuf<uint4> ovf(size_t(ntiles), s);
     uint64_t cap = std::max<uint64_t>(2 * uint64_t(i_hi - i_lo), 1 << 16);
-    DevBuf<uint64_t> eo(cap, s, Mem::Persist);
+    DevBuf<uint64_t> hits(cap, s);  // tile blocks of sorted (i << 32 | j)
     unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
     int reruns = 0;
     uint64_t m = 0, issued = 0, novf = 0;
     while (true) {
-      CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * 8, s));
       CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
       CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
-      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, eo.p, cap, status.p, ticket.p, ctr.p,
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tinfo.p, ticket.p, ctr.p,
                           ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
       CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -432,21 +431,37 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       novf = uint32_t(hc[2] & 0xffffffffu);
       if (m <= cap) break;
       cap = m;
-      eo.alloc(cap, s, Mem::Persist);
+      hits.alloc(cap, s);
       ++reruns;
     }
+    tm.mark();  // 6: probe
+    // ---- canonical placement of the tile blocks: offsets = exclusive scan
+    // of the tile counts (overflow tiles included), then one copy
+    DevBuf<uint32_t> toff(size_t(ntiles), s);
+    CG_CUDA(cudaMemcpyAsync(toff.p, tinfo.p, size_t(ntiles) * 4, cudaMemcpyDeviceToDevice, s));
+    launch_scan_u32(toff.p, ntiles, s);
+    uint64_t mt = m;  // total including overflow tiles
     if (novf) {
-      // tiles whose hits overflowed the shared buffer: re-run each in spill
-      // mode, sort its hits and drop them into its slot range
       std::vector<uint4> hv(novf);
       CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      for (const uint4& t : hv) mt += t.z;
+    }
+    uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(mt, 1) * 8, s));
+    launch_tile_copy(hits.p, toff.p, tinfo.p + ntiles, tinfo.p, ntiles, eout, s);
+    if (novf) {
+      // tiles whose hits overflowed the shared buffer: re-run each in spill
+      // mode, sort its hits and write them at the tile's offset
+      std::vector<uint4> hv(novf);
+      CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
+      std::vector<uint32_t> hoff(ntiles);
+      CG_CUDA(cudaMemcpyAsync(hoff.data(), toff.p, size_t(ntiles) * 4, cudaMemcpyDeviceToHost, s));
       CG_CUDA(cudaStreamSynchronize(s));
       const int tc = probe_global_tile_cells();
       for (const uint4& t : hv) {
         const uint32_t cnt = t.z;
-        DevBuf<uint64_t> sp1(cnt, s), sp2(cnt, s), rot(cnt, s);
-        DevBuf<uint64_t> st1(1, s);
-        CG_CUDA(cudaMemsetAsync(st1.p, 0, 8, s));
+        DevBuf<uint64_t> sp1(cnt, s), sp2(cnt, s);
+        DevBuf<uint32_t> st1(2, s);
         CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
         CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
         const int64_t lo = i_lo + int64_t(t.x) * tc, hi = std::min<int64_t>(i_hi, lo + tc);
@@ -454,19 +469,11 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
                             ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, cnt, ctr.p + 2, s);
         uint64_t* so = sp1.p;
         if (cnt > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, cnt, 64, &so, nullptr, s, nullptr);
-        launch_rotate_edges(so, cnt, eo.p + t.y, s);
+        launch_rotate_edges(so, cnt, eout + hoff[t.x], s);
       }
-      CG_CUDA(cudaStreamSynchronize(s));
     }
-    tm.mark();  // 6: probe
-    tm.mark();  // 7: edges (already canonical)
-    uint64_t* eout = nullptr;
-    if (m * 2 < cap) {
-      eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
-      if (m) CG_CUDA(cudaMemcpyAsync(eout, eo.p, m * 8, cudaMemcpyDeviceToDevice, s));
-    } else {
-      eout = eo.release();
-    }
+    m = mt;
+    tm.mark();  // 7: edges (placement of the already sorted tile blocks)
     uint64_t* cout = nullptr;
     if (nc * 2 < n) {
       cout = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));

@@ -96,6 +96,18 @@ int blocks_for(int64_t n, int threads, int per_sm) {
 
 }  // namespace
 
+void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  constexpr int TILE = kScanThreads * kScanIPT;
+  const int64_t tiles = (n + TILE - 1) / TILE;
+  DevBuf<uint64_t> status(size_t(tiles), s);
+  DevBuf<uint32_t> ticket(1, s);
+  CG_CUDA(cudaMemsetAsync(status.p, 0, size_t(tiles) * 8, s));
+  CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
+  k_scan_u32<<<unsigned(tiles), kScanThreads, 0, s>>>(v, n, status.p, ticket.p);
+  CG_LAUNCH_CHECK();
+}
+
 void place_edges(const uint64_t* hits, int64_t m, int64_t nc, uint64_t* out, cudaStream_t s) {
   if (m <= 0) return;
   DevBuf<uint32_t> deg(size_t(nc), s), cur(size_t(nc), s);

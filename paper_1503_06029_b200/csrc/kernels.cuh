@@ -118,17 +118,25 @@ struct GlobalDict {
 };
 void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
                         uint32_t* F, cudaStream_t s);
-// status/ticket: look-back state for ceil((i_hi - i_lo) / 256) tiles (zeroed);
-// *total = number of edges; tiles whose hits overflow the shared buffer are
-// listed in ovf (tile, base, count) and must be re-run in spill mode
-// (spill != nullptr: unordered append to spill[0..spill_cap), *spill_n).
+// Each tile of 256 cells writes its sorted hits (i << 32 | j) as one block of
+// out[0..cap) (reserved by atomicAdd on *total) and records status[t] =
+// count, status[ntiles + t] = block position (status: u32[2 * ntiles]).
+// Tiles whose hits overflow the shared buffer are listed in ovf (tile, -,
+// count) and must be re-run in spill mode (spill != nullptr: unordered
+// append to spill[0..spill_cap), *spill_n).
 void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
-                         uint64_t* out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                         uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                          unsigned long long* total, unsigned long long* issued, uint4* ovf,
                          uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
                          unsigned long long* spill_n, cudaStream_t s);
+// place every tile block at its canonical offset off[t] as (i, j) pairs
+void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
+                      const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s);
 int64_t probe_global_tiles(int64_t n);
 int probe_global_tile_cells();
+int probe_global_tile_edge_cap();
+// exclusive prefix sum of u32 in place (total < 2^32); edges.cu
+void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- cg_query
 void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,

@@ -55,7 +55,7 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 template <int WC>
 __global__ void __launch_bounds__(kTileCells)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
-                   uint64_t* __restrict__ out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                   uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                    unsigned long long* total, unsigned long long* issued,
                    uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
                    uint4* __restrict__ ovf, uint32_t* ovf_n) {
@@ -362,23 +362,28 @@ __global__ void __launch_bounds__(kTileCells)
     }
     __syncthreads();
     if (spill) continue;  // spill mode: no ordered output
-    // ---- tile output: global offset by look-back, local sort, write
+    // ---- tile output: the tile's hits, sorted, go to a block of the
+    // scratch list reserved with one atomicAdd; tile_cnt/tile_pos let a
+    // scan + copy place every block at its canonical offset afterwards
+    // (a look-back here would make each tile wait for its predecessor's
+    // probes to finish).
     const uint32_t cnt = s_cnt;
     if (tid == 0) {
-      s_base = lookback(status, tile, 1, 0, cnt, 1);
-      if (tile == ntiles - 1) *total = (unsigned long long)s_base + cnt;
+      status[tile] = cnt;  // tile_cnt
+      if (cnt > kTileEdgeCap) {
+        // rare: hits beyond the shared buffer were dropped; the host re-runs
+        // this tile in spill mode and writes its range directly
+        const uint32_t k = atomicAdd(ovf_n, 1u);
+        ovf[k] = make_uint4(uint32_t(tile), 0u, cnt, 0u);
+        s_base = 0;
+      } else {
+        s_base = uint32_t(atomicAdd(total, (unsigned long long)cnt));
+      }
+      status[ntiles + tile] = s_base;  // tile_pos in the scratch list
     }
     __syncthreads();
     const uint32_t base = s_base;
-    if (cnt > kTileEdgeCap) {
-      // rare: re-emit is impossible here, so the tile's hits beyond the
-      // buffer were dropped -> record the slot range; the host re-runs the
-      // tile's cells in spill mode (see run_probe_global)
-      if (tid == 0) {
-        const uint32_t k = atomicAdd(ovf_n, 1u);
-        ovf[k] = make_uint4(uint32_t(tile), base, cnt, 0u);
-      }
-    } else {
+    if (cnt <= kTileEdgeCap) {
       int P = 1;
       while (P < int(cnt)) P <<= 1;
       for (int q = cnt + tid; q < P; q += kTileCells) ebuf[q] = ~0ull;
@@ -400,8 +405,7 @@ __global__ void __launch_bounds__(kTileCells)
       }
       for (uint32_t q = tid; q < cnt; q += kTileCells) {
         const uint64_t pos = uint64_t(base) + q;
-        const uint64_t k = ebuf[q];
-        if (pos < cap) out[pos] = (k >> 32) | (k << 32);
+        if (pos < cap) out[pos] = ebuf[q];  // sorted (i << 32 | j) keys
       }
     }
     __syncthreads();
@@ -421,7 +425,7 @@ void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fex
 }
 
 void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
-                         uint64_t* out, uint64_t cap, uint64_t* status, uint32_t* ticket,
+                         uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                          unsigned long long* total, unsigned long long* issued, uint4* ovf,
                          uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
                          unsigned long long* spill_n, cudaStream_t s) {
@@ -436,7 +440,35 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
   CG_LAUNCH_CHECK();
 }
 
+// one warp per tile: its sorted block of (i << 32 | j) keys from the scratch
+// list to the tile's canonical offset, as (i, j) u32 pairs
+__global__ void k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t* __restrict__ off,
+                            const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cntv,
+                            int64_t ntiles, uint64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
+    const uint32_t c = cntv[t];
+    if (c > kTileEdgeCap) continue;  // overflow tile: written by the spill path
+    const uint64_t* src = scratch + pos[t];
+    uint64_t* dst = out + off[t];
+    for (uint32_t q = lane; q < c; q += 32) {
+      const uint64_t k = src[q];
+      dst[q] = (k >> 32) | (k << 32);
+    }
+  }
+}
+
+void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
+                      const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  const int64_t blocks = std::min<int64_t>((ntiles * 32 + 255) / 256, int64_t(num_sms()) * 16);
+  k_tile_copy<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(scratch, off, pos, cnt, ntiles, out);
+  CG_LAUNCH_CHECK();
+}
+
 int64_t probe_global_tiles(int64_t n) { return (n + kTileCells - 1) / kTileCells; }
+int probe_global_tile_edge_cap() { return kTileEdgeCap; }
 int probe_global_tile_cells() { return kTileCells; }
 
 }  // namespace cgk
