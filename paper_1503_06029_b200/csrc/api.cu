@@ -156,7 +156,7 @@ WsScope::WsScope() {
 WsScope::~WsScope() {
   Arena& a = cur_arena();
   if (--a.depth > 0) return;
-  if (a.peak > a.cap) a.want = a.peak + a.peak / 16;
+  if (a.peak > a.cap) a.want = a.peak + a.peak / 4;  // grow once, with headroom
   a.stack.clear();
   a.top = 0;
 }
@@ -331,7 +331,7 @@ struct Shard {
 // Runs a2..a7 given packed keys (u64[n][W], consumed as scratch).
 static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
                             uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out,
-                            const Shard& sh = Shard()) {
+                            const Shard& sh = Shard(), const uint32_t* top_hist = nullptr) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
@@ -342,7 +342,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   if (W <= 2 && o.sort_kind != 1) {
     // MSD fast path; falls back below when a prefix bucket overflows
     uint64_t* ko = nullptr;
-    done = sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst);
+    done = sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     sorted = ko;
     if (!done && ko != keys.p) std::swap(keys.p, alt.p);  // partially sorted data in keys
   }
@@ -692,26 +692,42 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
         o.dict_kind != CG_DICT_GLOBAL)
       throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
+    static const bool trace = std::getenv("CG_TRACE") != nullptr;
+    auto lap = [&](const char* what) {
+      if (trace)
+        std::fprintf(stderr, "[cg] %-12s %9.1f us\n", what,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
+    };
     check_arch();
+    lap("arch");
     check_device_ptr(vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words), "input");
+    lap("ptr");
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     const int W = (ell + 63) / 64;
     WsScope ws;
+    lap("arena");
     StageTimer tm;
     tm.start(o.stats != nullptr, s);  // 0
+    lap("events");
     setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
     DevBuf<uint64_t> keys(size_t(n) * W, s);
+    // the MSD sort's top-digit histogram, counted by the pack kernel
+    const bool msd = W <= 2 && o.sort_kind != 1;
+    const int dlo = (64 - msd_prefix_bits(n)) / 8;
+    DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
     if (vecs) {
-      launch_pack(vecs, n, ell, keys.p, flags.p, s);
+      if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
+      launch_pack(vecs, n, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo);
     } else {
       CG_CUDA(cudaMemcpyAsync(keys.p, words, size_t(n) * W * 8, cudaMemcpyDeviceToDevice, s));
       launch_check_pad(keys.p, n, ell, flags.p, s);
     }
     tm.mark();  // 1: pack
-    build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b);
+    build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(),
+                    (vecs && msd) ? top_hist.p : nullptr);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
   } catch (const CgError& e) {

@@ -174,6 +174,42 @@ __device__ __forceinline__ uint32_t lookback(uint64_t* status, int64_t tile, int
   return excl;
 }
 
+// Single-slot look-back run by ONE FULL WARP: each step loads the statuses of
+// the 32 nearest unexamined predecessors at once (lane l -> tile j - l), so an
+// inclusive prefix 32 tiles back costs one round trip instead of 32.
+// Returns the exclusive prefix in every lane.
+__device__ __forceinline__ uint32_t lookback_warp(uint64_t* status, int64_t tile, uint32_t agg,
+                                                  uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_u64(status, lb_pack(2, epoch, agg));
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, lb_pack(1, epoch, agg));
+  const uint32_t ep = epoch & 0x3fffffffu;
+  uint32_t excl = 0;
+  int64_t j = tile - 1;
+  while (true) {
+    const int64_t jj = j - lane;
+    uint64_t s = jj >= 0 ? ld_relaxed_u64(status + jj) : lb_pack(2, epoch, 0);
+    const uint32_t flag = uint32_t(s >> 62);
+    const bool ready = flag != 0 && ((uint32_t(s >> 32) & 0x3fffffffu) == ep);
+    const uint32_t notready = __ballot_sync(kFull, !ready);
+    const uint32_t incl = __ballot_sync(kFull, ready && flag == 2);
+    const int first_inc = incl ? __ffs(incl) - 1 : 32;
+    const int first_nr = notready ? __ffs(notready) - 1 : 32;
+    const int take = first_nr < first_inc ? first_nr : (first_inc < 32 ? first_inc + 1 : 32);
+    uint32_t v = lane < take ? uint32_t(s) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    excl += v;
+    if (first_inc < 32 && first_inc < first_nr) break;
+    j -= take;  // take == first_nr (spin there) or 32 (all aggregates)
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, lb_pack(2, epoch, excl + agg));
+  return excl;
+}
+
 // Block-wide exclusive scan of one u32 per thread (blockDim.x multiple of 32,
 // <= 1024).  `tmp` needs 33 words of shared memory.  Returns the total in *total.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {

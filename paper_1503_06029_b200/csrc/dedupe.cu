@@ -72,16 +72,21 @@ __global__ void __launch_bounds__(kDedupThreads)
   }
   if (lane == 0) s_warp[wid] = wcount;
   __syncthreads();
-  if (tid == 0) {
+  if (wid == 0) {
     uint32_t run = 0;
+    uint32_t mine = 0;
     for (int w = 0; w < NWARP; ++w) {
       const uint32_t c = s_warp[w];
-      s_warp[w] = run;
+      if (lane == w) mine = run;
       run += c;
     }
-    const uint32_t base = lookback(status, tile, 1, 0, run, 1);
-    s_base = base;
-    if (tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
+    __syncwarp();
+    if (lane < NWARP) s_warp[lane] = mine;
+    const uint32_t base = lookback_warp(status, tile, run, 1);
+    if (lane == 0) {
+      s_base = base;
+      if (tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
+    }
   }
   __syncthreads();
   uint32_t c0 = s_base + s_warp[wid];  // first cell index of this warp's flags

@@ -46,7 +46,10 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   uint32_t total;
   const uint32_t excl = block_excl_scan(sum, s_scan, &total);
-  if (threadIdx.x == 0) s_base = lookback(status, tile, 1, 0, total, 1);
+  if (threadIdx.x < 32) {
+    const uint32_t b = lookback_warp(status, tile, total, 1);
+    if (threadIdx.x == 0) s_base = b;
+  }
   __syncthreads();
   uint32_t run = s_base + excl;
 #pragma unroll

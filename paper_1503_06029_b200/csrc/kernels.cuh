@@ -7,8 +7,10 @@ namespace cgk {
 
 // ---------------------------------------------------------------- a1 pack
 // uint8[n][ell] (0/1 bytes) -> u64[n][W] MSB-first; *err |= 1 on a byte > 1.
+// hist (optional, zeroed, u32[(8 - dlo) * 256]): counts of the 8-bit digits
+// dlo..7 of word 0, for the MSD sort (dlo in 5..7).
 void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
-                 cudaStream_t s);
+                 cudaStream_t s, uint32_t* hist = nullptr, int dlo = 8);
 // packed input: copy + check pad bits (err |= 1 if a pad bit is set)
 void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s);
 
@@ -38,7 +40,9 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
 // a bucket exceeded the shared-memory capacity: *sorted is then only
 // bucket-ordered and the caller must finish with a full sort.
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
-                   cudaStream_t s, SortStats* st);
+                   cudaStream_t s, SortStats* st, const uint32_t* top_hist = nullptr);
+// prefix bits B (8, 16 or 24) the MSD path uses for n keys; digit dlo = (64-B)/8
+int msd_prefix_bits(int64_t n);
 
 // ---------------------------------------------------------------- a3 dedupe + compaction
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],

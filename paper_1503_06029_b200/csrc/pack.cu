@@ -24,10 +24,22 @@ __device__ __forceinline__ uint32_t bits8_msb(uint64_t x) {
 
 constexpr uint64_t kHi7 = 0xfefefefefefefefeull;
 
+// Optionally (hist != nullptr) also counts the 8-bit digits dlo..7 of word 0
+// (the top bits the MSD sort partitions on), run-length accumulated per
+// thread so constant digits do not serialise shared-memory atomics; this
+// saves the sort's separate histogram read of the keys.
 template <int VEC>
 __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, int64_t n,
                                               int ell, int W, uint64_t* __restrict__ keys,
-                                              uint32_t* __restrict__ err) {
+                                              uint32_t* __restrict__ err,
+                                              uint32_t* __restrict__ hist, int dlo) {
+  __shared__ uint32_t sh[3][256];
+  const int nd = hist ? 8 - dlo : 0;
+  if (hist) {
+    for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+  }
+  uint32_t last[3] = {0, 0, 0}, cnt[3] = {0, 0, 0};
   const int64_t total = n * W;
   uint64_t bad = 0;
   for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
@@ -75,8 +87,32 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
       }
     }
     keys[g] = word;
+    if (nd && w == 0) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        if (d < nd) {
+          const uint32_t bin = uint32_t(word >> (8 * (dlo + d))) & 255u;
+          if (bin != last[d]) {
+            if (cnt[d]) atomicAdd(&sh[d][last[d]], cnt[d]);
+            last[d] = bin;
+            cnt[d] = 0;
+          }
+          ++cnt[d];
+        }
+      }
+    }
   }
   if (bad) atomicOr(err, 1u);
+  if (hist) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d < nd && cnt[d]) atomicAdd(&sh[d][last[d]], cnt[d]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nd * 256; i += blockDim.x) {
+      const uint32_t v = (&sh[0][0])[i];
+      if (v) atomicAdd(&hist[i], v);
+    }
+  }
 }
 
 __global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W, uint64_t pad,
@@ -91,20 +127,21 @@ __global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W
 }  // namespace
 
 void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
-                 cudaStream_t s) {
+                 cudaStream_t s, uint32_t* hist, int dlo) {
   const int W = (ell + 63) / 64;
   const int64_t total = n * W;
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, int64_t(num_sms()) * 8);
   if (blocks < 1) blocks = 1;
+  if (hist && (dlo < 5 || dlo > 7)) hist = nullptr;  // at most 3 top digits
   const uintptr_t a = reinterpret_cast<uintptr_t>(vecs);
   if (ell % 16 == 0 && a % 16 == 0) {
-    k_pack<16><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+    k_pack<16><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
   } else if (ell % 8 == 0 && a % 8 == 0) {
-    k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+    k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
   } else {
-    k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err);
+    k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
   }
   CG_LAUNCH_CHECK();
 }

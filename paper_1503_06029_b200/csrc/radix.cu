@@ -429,7 +429,8 @@ int grid_for(int64_t n, int threads, int per_sm = 8) {
 template <class K>
 void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
                   uint32_t* vals_alt, bool want_vals, int64_t n, int dlo, int dhi, K** keys_out,
-                  uint32_t** vals_out, cudaStream_t s, SortStats* st) {
+                  uint32_t** vals_out, cudaStream_t s, SortStats* st,
+                  const uint32_t* dev_hist = nullptr) {
   *keys_out = keys;
   if (vals_out) *vals_out = nullptr;
   auto identity_or_input = [&]() {
@@ -448,11 +449,15 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
   }
   const int nd = dhi - dlo;
   DevBuf<uint32_t> hist(size_t(nd) * kRadix, s);
-  CG_CUDA(cudaMemsetAsync(hist.p, 0, hist.n * sizeof(uint32_t), s));
-  k_digit_hist<K><<<grid_for(n, 256, 4), 256, 0, s>>>(keys, n, dlo, dhi, hist.p);
-  CG_LAUNCH_CHECK();
+  const uint32_t* hsrc = dev_hist;
+  if (!hsrc) {  // (the pack kernel may have counted these digits already)
+    CG_CUDA(cudaMemsetAsync(hist.p, 0, hist.n * sizeof(uint32_t), s));
+    k_digit_hist<K><<<grid_for(n, 256, 4), 256, 0, s>>>(keys, n, dlo, dhi, hist.p);
+    CG_LAUNCH_CHECK();
+    hsrc = hist.p;
+  }
   uint32_t* hh = static_cast<uint32_t*>(host_stage(hist.n * sizeof(uint32_t)));
-  CG_CUDA(cudaMemcpyAsync(hh, hist.p, hist.n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(hh, hsrc, hist.n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
   std::vector<int> digits;
   std::vector<uint32_t> bases;
@@ -553,15 +558,21 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
   launch_gather_rows(keys, idx, n, W, sorted, s);
 }
 
-namespace {
-template <class K>
-bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStats* st) {
+int msd_prefix_bits(int64_t n) {
   // B top bits (a multiple of 8) so buckets hold ~2^10 keys on average
   int B = 8;
   while (B < 24 && (n >> B) > 1024) B += 8;
+  return B;
+}
+
+namespace {
+template <class K>
+bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStats* st,
+                   const uint32_t* top_hist) {
+  const int B = msd_prefix_bits(n);
   K* ko = nullptr;
   radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
-                  s, st);
+                  s, st, top_hist);
   const int64_t nb = int64_t(1) << B;
   DevBuf<uint32_t> off(size_t(nb) + 1, s);
   DevBuf<uint32_t> flag(1, s);
@@ -587,17 +598,18 @@ bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStat
 }  // namespace
 
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
-                   cudaStream_t s, SortStats* st) {
+                   cudaStream_t s, SortStats* st, const uint32_t* top_hist) {
   if (W == 1) {
     uint64_t* o = nullptr;
-    const bool ok = msd_sort_impl<uint64_t>(keys, alt, n, &o, s, st);
+    const bool ok = msd_sort_impl<uint64_t>(keys, alt, n, &o, s, st, top_hist);
     *sorted = o;
     return ok;
   }
   if (W == 2) {
     ulonglong2* o = nullptr;
     const bool ok = msd_sort_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
-                                              reinterpret_cast<ulonglong2*>(alt), n, &o, s, st);
+                                              reinterpret_cast<ulonglong2*>(alt), n, &o, s, st,
+                                              top_hist);
     *sorted = reinterpret_cast<uint64_t*>(o);
     return ok;
   }
