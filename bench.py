@@ -114,7 +114,9 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
     W = (ell + 63) // 64
     K = 8 * W
     nc, m, issued = st["n_cells"], st["n_edges"], st["issued_probes"]
-    sort_key_bytes = 128 if W == 1 else 192 + 32 + K  # per key (8 passes x 2 x 12 B + gather)
+    # MSD path (W <= 2): 2 top-digit passes + the bucket pass, each 2K per key;
+    # multi-word LSD (W > 2): per word 8 passes x 2 x 12 B + gathers
+    sort_key_bytes = 6 * K if W <= 2 else W * (192 + 16) + 2 * K
     return {
         "pack": n * (ell + K),
         "sort": n * sort_key_bytes,
@@ -124,6 +126,36 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
         "probe": nc * (K + 10) + issued * 32 + m * 8,
         "edges": m * 8 * 2 * 8 + m * 16,
     }
+
+
+STAGE_KERNEL = {"pack": "k_pack", "sort": "k_bucket_sort", "dedupe": "k_dedupe",
+                "dict": "k_global_index", "probe": "k_probe_global", "edges": "k_tile_copy",
+                "layers": "k_gather_rows"}
+
+
+def _ncu_traffic(stage: str):
+    """DRAM bytes (read + write) per launch of the stage's main kernel from the
+    committed ncu --set full summary (profiles/*_kernels.json), or None."""
+    import glob
+
+    name = STAGE_KERNEL.get(stage)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
+    if not name or not files:
+        return None, None
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    with open(files[-1]) as f:
+        ks = json.load(f)
+    for k in ks:
+        if name in k["kernel"]:
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v = k["metrics"].get(m)
+                if v is None:
+                    return None, None
+                num, u = v.split()[0], v.split()[1] if len(v.split()) > 1 else "byte"
+                tot += float(num) * unit.get(u, 1)
+            return int(tot), os.path.basename(files[-1])
+    return None, None
 
 
 def run_ours(args):
@@ -176,10 +208,12 @@ def run_ours(args):
     peak, peak_src = _peaks()
     dom = max(stage_us, key=lambda k: stage_us[k])
     achieved = ab[dom] / (stage_us[dom] * 1e-6) / 1e9
-    roof = {"bound": "hbm", "kernel_stage": dom, "achieved": round(achieved, 1),
-            "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "alg_bytes_per_launch": int(ab[dom])}
+    traffic, tsrc = _ncu_traffic(dom)
+    roof = {"bound": "hbm", "kernel_stage": dom, "kernel": STAGE_KERNEL.get(dom),
+            "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": tsrc, "alg_bytes_per_launch": int(ab[dom]),
+            "alg_bytes_def": "SURVEY 8.d.3 per-unit figures (DESIGN.md section 6)"}
     total_alg = sum(ab.values())
     whole = total_alg / (ms * 1e-3) / 1e9
     # ---- e2e through the host-buffer C-ABI entry
