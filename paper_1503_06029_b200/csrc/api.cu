@@ -335,16 +335,34 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
-  // ---- a2 sort
-  DevBuf<uint64_t> alt(size_t(n) * W, s);
+  // ---- a2 sort (+ a3 dedupe fused into the MSD bucket pass)
+  const bool msd = W <= 2 && o.sort_kind != 1;
+  // on the MSD path the result stays in keys or alt, which becomes the
+  // output cell table: both are persistent allocations there
+  DevBuf<uint64_t> alt(size_t(n) * W, s, (msd && !keys.scratch) ? Mem::Persist : Mem::Scratch);
+  DevBuf<uint64_t> cellbuf;  // the output cell table
+  DevBuf<uint32_t> popc(size_t(n), s);
+  DevBuf<uint16_t> lcp(size_t(n), s);
   const uint64_t* sorted = nullptr;
   bool done = false;
-  if (W <= 2 && o.sort_kind != 1) {
-    // MSD fast path; falls back below when a prefix bucket overflows
+  int64_t nc = -1;
+  if (msd) {
     uint64_t* ko = nullptr;
-    done = sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
+    int64_t ncu = 0;
+    const bool fused = !keys.scratch && !alt.scratch;
+    done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist)
+                 : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     sorted = ko;
-    if (!done && ko != keys.p) std::swap(keys.p, alt.p);  // partially sorted data in keys
+    if (done && fused) {
+      nc = ncu;
+      if (ko == keys.p) cellbuf.adopt(keys.release(), size_t(n) * W, s);
+      else cellbuf.adopt(alt.release(), size_t(n) * W, s);
+    }
+    if (!done && ko != keys.p) {  // partially sorted data belongs in keys
+      std::swap(keys.p, alt.p);
+      std::swap(keys.arena, alt.arena);
+      std::swap(keys.scratch, alt.scratch);
+    }
   }
   if (!done) {
     if (W == 1) {
@@ -358,16 +376,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
   }
   tm.mark();  // 2: sort
-  // ---- a3 dedupe + compaction
-  DevBuf<uint64_t> cellbuf(size_t(n) * W, s, Mem::Persist);  // the output cell table
-  DevBuf<uint32_t> popc(size_t(n), s);
-  DevBuf<uint16_t> lcp(size_t(n), s);
-  launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+  if (nc < 0) {
+    // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
+    cellbuf.alloc(size_t(n) * W, s, Mem::Persist);
+    launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+  } else {
+    // cells came out of the fused MSD pass: per-cell popcount and LCP
+    launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
+  }
   uint32_t* hf = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(hf, d_flags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
   if (hf[0]) throw CgError{CG_EINPUT, "input byte not in {0,1} (or pad bit set in packed input)"};
-  const int64_t nc = hf[1];
+  if (nc < 0) nc = hf[1];
   tm.mark();  // 3: dedupe
   keys.reset();
   alt.reset();
@@ -713,9 +734,10 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-    DevBuf<uint64_t> keys(size_t(n) * W, s);
-    // the MSD sort's top-digit histogram, counted by the pack kernel
+    // the MSD sort's top-digit histogram, counted by the pack kernel; on the
+    // MSD path the key buffer becomes the output cell table (persistent)
     const bool msd = W <= 2 && o.sort_kind != 1;
+    DevBuf<uint64_t> keys(size_t(n) * W, s, msd ? Mem::Persist : Mem::Scratch);
     const int dlo = (64 - msd_prefix_bits(n)) / 8;
     DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
     if (vecs) {
@@ -806,7 +828,8 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
     tm.start(o.stats != nullptr, s);
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-    DevBuf<uint64_t> keys(size_t(n) * W, s);
+    DevBuf<uint64_t> keys(size_t(n) * W, s,
+                          (W <= 2 && o.sort_kind != 1) ? Mem::Persist : Mem::Scratch);
     // H2D in row chunks, each packed as soon as it lands (copy/compute overlap
     // through two staging buffers and a copy stream).
     const int64_t row_bytes = ell;

@@ -82,6 +82,14 @@ struct DevBuf {
       scratch = true;
     }
   }
+  // take ownership of a persistent buffer released by another DevBuf
+  void adopt(T* ptr, size_t count, cudaStream_t st) {
+    reset();
+    p = ptr;
+    n = count;
+    s = st;
+    arena = scratch = false;
+  }
   // hand a persistent buffer to the caller (never valid for scratch memory)
   T* release() {
     if (scratch) throw CgError{CG_ECUDA, "internal: release() of a scratch buffer"};

@@ -116,7 +116,32 @@ __global__ void __launch_bounds__(kDedupThreads)
   }
 }
 
+template <int WC>
+__global__ void k_cell_meta(const uint64_t* __restrict__ cells, int64_t nc, int W,
+                            uint32_t* __restrict__ popc, uint16_t* __restrict__ lcp) {
+  using R = Row<WC>;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nc;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t* row = cells + i * W;
+    if (popc) popc[i] = R::popc(row, W);
+    lcp[i] = (i + 1 < nc) ? uint16_t(R::lcp(row, row + W, W)) : uint16_t(0xffff);
+  }
+}
+
 }  // namespace
+
+void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
+                      cudaStream_t s) {
+  if (nc <= 0) return;
+  const int64_t blocks = std::min<int64_t>((nc + 255) / 256, int64_t(num_sms()) * 16);
+  const unsigned g = unsigned(std::max<int64_t>(1, blocks));
+  switch (W) {
+    case 1: k_cell_meta<1><<<g, 256, 0, s>>>(cells, nc, W, popc, lcp); break;
+    case 2: k_cell_meta<2><<<g, 256, 0, s>>>(cells, nc, W, popc, lcp); break;
+    default: k_cell_meta<0><<<g, 256, 0, s>>>(cells, nc, W, popc, lcp); break;
+  }
+  CG_LAUNCH_CHECK();
+}
 
 void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, uint32_t* popc,
                    uint16_t* lcp, uint32_t* n_cells, cudaStream_t s) {

@@ -43,6 +43,15 @@ bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** s
                    cudaStream_t s, SortStats* st, const uint32_t* top_hist = nullptr);
 // prefix bits B (8, 16 or 24) the MSD path uses for n keys; digit dlo = (64-B)/8
 int msd_prefix_bits(int64_t n);
+// MSD sort with dedupe fused into the bucket pass: the sorted unique cells
+// end up in keys or alt (*cells), *nc of them.  false = a bucket overflowed
+// (keys/alt then hold the same SET of keys, bucket-ordered; run the full
+// sort + dedupe instead).
+bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
+                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist);
+// popcount (optional) and lcp with the next cell, for a canonical table
+void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
+                      cudaStream_t s);
 
 // ---------------------------------------------------------------- a3 dedupe + compaction
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],

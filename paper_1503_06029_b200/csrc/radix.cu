@@ -272,10 +272,10 @@ constexpr int kBktMaxRounds = 64;
 //      (ties of the two bytes are short runs: planted pairs, duplicates);
 //      a bucket that does not settle within kBktMaxRounds, or is larger than
 //      CAP, raises *overflow and the caller runs the full LSD sort instead.
-template <class K>
+template <class K, int MAXC>  // MAXC chunks of 32 rows per warp: CAP <= 8 * 32 * MAXC
 __global__ void __launch_bounds__(kBktThreads)
     k_bucket_sort(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets,
-                  int CAP, int B, uint32_t* __restrict__ overflow) {
+                  int CAP, int B, uint32_t* __restrict__ overflow, uint32_t* __restrict__ ucnt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
   uint16_t* ia = reinterpret_cast<uint16_t*>(smem_raw + size_t(CAP) * sizeof(K));
@@ -285,13 +285,15 @@ __global__ void __launch_bounds__(kBktThreads)
   __shared__ uint64_t s_red[2][kBktWarps][2];
   constexpr int NW = sizeof(K) / 8;
   constexpr int NBYTES = sizeof(K);
-  constexpr int MAXC = 16;  // chunks of 32 per warp: CAP <= 8 warps * 16 * 32 = 4096
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t lt = lanemask_lt();
   for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x) {
     const uint32_t lo = off[bk], hi = off[bk + 1];
     const int S = int(hi - lo);
-    if (S <= 1) continue;
+    if (S <= 1) {
+      if (ucnt && tid == 0) ucnt[bk] = uint32_t(S);
+      continue;
+    }
     if (S > CAP) {
       if (tid == 0) atomicOr(overflow, 1u);
       continue;
@@ -389,9 +391,41 @@ __global__ void __launch_bounds__(kBktThreads)
       cur = nxt;
       nxt = t;
     }
-    // ---- odd-even transposition on whole keys until settled
-    bool settled = false;
-    for (int round = 0; round < kBktMaxRounds; ++round) {
+    // ---- finish the order.  Keys are now sorted by (byte P1, byte P2), and
+    // every byte before P2 other than P1 is constant, so keys that tie on
+    // (P1, P2) form contiguous runs that only need sorting internally: the
+    // thread at the head of each run insertion-sorts it on the whole key.
+    // Runs longer than 32 (skewed data) fall back to odd-even rounds.
+    int long_run = 0;
+    if (P2 >= 0) {
+      auto tb = [&](int i) -> uint32_t {
+        const K k = s[cur[i]];
+        return (key_byte(k, P1) << 8) | key_byte(k, P2);
+      };
+      for (int i = tid; i + 1 < S; i += kBktThreads) {
+        const uint32_t bi = tb(i);
+        if (bi != tb(i + 1) || (i > 0 && tb(i - 1) == bi)) continue;  // not a run head
+        int j = i + 2;
+        while (j < S && j - i <= 32 && tb(j) == bi) ++j;
+        if (j - i > 32) {
+          long_run = 1;
+          continue;
+        }
+        for (int a = i + 1; a < j; ++a) {
+          const uint16_t v = cur[a];
+          const K kv = s[v];
+          int q = a;
+          while (q > i && key_less(kv, s[cur[q - 1]])) {
+            cur[q] = cur[q - 1];
+            --q;
+          }
+          cur[q] = v;
+        }
+      }
+    }
+    const bool need_rounds = __syncthreads_or(long_run) != 0;
+    bool settled = !need_rounds;
+    for (int round = 0; need_rounds && round < kBktMaxRounds; ++round) {
       int changed = 0;
       for (int ph = 0; ph < 2; ++ph) {
         for (int i = 2 * tid + ph; i + 1 < S; i += 2 * kBktThreads) {
@@ -414,7 +448,30 @@ __global__ void __launch_bounds__(kBktThreads)
       __syncthreads();
       continue;
     }
-    for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[cur[i]];
+    if (!ucnt) {
+      for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[cur[i]];
+    } else {
+      // a3 fused: keep the first of each run of equal keys, written
+      // compacted at the front of the bucket's range; ucnt[b] = unique count.
+      // (Keys of different buckets differ in their prefix, so the first key
+      // of a bucket is always new.)
+      const int nchunk = (S + kBktThreads - 1) / kBktThreads;
+      uint32_t run = 0;
+      for (int c = 0; c < nchunk; ++c) {
+        const int i = c * kBktThreads + tid;
+        bool f = false;
+        K k{};
+        if (i < S) {
+          k = s[cur[i]];
+          f = (i == 0) || key_less(s[cur[i - 1]], k);
+        }
+        uint32_t tot;
+        const uint32_t r = block_excl_scan(f ? 1u : 0u, s_scan, &tot);
+        if (f) keys[lo + run + r] = k;
+        run += tot;
+      }
+      if (tid == 0) ucnt[bk] = run;
+    }
     __syncthreads();
   }
 }
@@ -423,6 +480,25 @@ int grid_for(int64_t n, int threads, int per_sm = 8) {
   int64_t b = (n + threads - 1) / threads;
   int64_t cap = int64_t(num_sms()) * per_sm;
   return int(std::max<int64_t>(1, std::min(b, cap)));
+}
+
+// shared-memory capacity 2x the mean bucket (2048 or 4096 rows)
+template <class K>
+void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
+                        uint32_t* ucnt, cudaStream_t s) {
+  const int64_t avg = (n + nb - 1) / nb;
+  const int cap = avg <= 1024 ? 2048 : 4096;
+  const size_t smem = size_t(cap) * (sizeof(K) + 4);
+  const int per_sm = std::max(1, int((200 << 10) / (smem + 12 * 1024)));
+  const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
+  if (cap == 2048) {
+    CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_bucket_sort<K, 8><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt);
+  } else {
+    CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_bucket_sort<K, 16><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt);
+  }
+  CG_LAUNCH_CHECK();
 }
 
 // Generic pass driver over digits [dlo, dhi) of the top word.
@@ -579,16 +655,7 @@ bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStat
   CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
   k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, off.p);
   CG_LAUNCH_CHECK();
-  // shared-memory capacity: 2x the mean bucket, 2048..4096 rows
-  const int64_t avg = (n + nb - 1) / nb;
-  const int cap = avg <= 1024 ? 2048 : 4096;
-  const size_t smem = size_t(cap) * (sizeof(K) + 4);
-  CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  const int per_sm = std::max(1, int((200 << 10) / (smem + 12 * 1024)));
-  const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
-  k_bucket_sort<K><<<grid, kBktThreads, smem, s>>>(ko, off.p, nb, cap, B, flag.p);
-  CG_LAUNCH_CHECK();
+  launch_bucket_sort<K>(ko, off.p, n, nb, B, flag.p, nullptr, s);
   uint32_t* hf = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(hf, flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
@@ -596,6 +663,78 @@ bool msd_sort_impl(K* keys, K* alt, int64_t n, K** out, cudaStream_t s, SortStat
   return hf[0] == 0;
 }
 }  // namespace
+
+namespace {
+// one warp per bucket: move its ucnt[b] unique rows from src + off[b] to
+// dst + uoff[b] (only needed when duplicates were removed)
+template <class K>
+__global__ void k_compact_buckets(const K* __restrict__ src, const uint32_t* __restrict__ off,
+                                  const uint32_t* __restrict__ ucnt, const uint32_t* __restrict__ uoff,
+                                  int64_t nb, K* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t b = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; b < nb; b += nw) {
+    const uint32_t c = ucnt[b], from = off[b], to = uoff[b];
+    for (uint32_t q = lane; q < c; q += 32) dst[to + q] = src[from + q];
+  }
+}
+
+template <class K>
+bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaStream_t s,
+                      SortStats* st, const uint32_t* top_hist) {
+  const int B = msd_prefix_bits(n);
+  K* ko = nullptr;
+  radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
+                  s, st, top_hist);
+  const int64_t nb = int64_t(1) << B;
+  DevBuf<uint32_t> off(size_t(nb) + 1, s);
+  DevBuf<uint32_t> ucnt(size_t(nb), s), uoff(size_t(nb), s);
+  DevBuf<uint32_t> flag(1, s);
+  CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
+  k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, off.p);
+  CG_LAUNCH_CHECK();
+  launch_bucket_sort<K>(ko, off.p, n, nb, B, flag.p, ucnt.p, s);
+  CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
+  launch_scan_u32(uoff.p, nb, s);
+  uint32_t* h = static_cast<uint32_t*>(host_stage(3 * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(h + 1, uoff.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(h + 2, ucnt.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  *cells = ko;
+  if (h[0]) return false;
+  const int64_t total = int64_t(h[1]) + int64_t(h[2]);
+  *nc = total;
+  if (total != n) {  // duplicates removed: close the gaps between buckets
+    K* dst = (ko == keys) ? alt : keys;
+    const int64_t blocks = std::min<int64_t>((nb * 32 + 255) / 256, int64_t(num_sms()) * 16);
+    k_compact_buckets<K><<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(ko, off.p, ucnt.p,
+                                                                                uoff.p, nb, dst);
+    CG_LAUNCH_CHECK();
+    *cells = dst;
+  }
+  return true;
+}
+}  // namespace
+
+bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
+                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist) {
+  if (W == 1) {
+    uint64_t* o = nullptr;
+    const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist);
+    *cells = o;
+    return ok;
+  }
+  if (W == 2) {
+    ulonglong2* o = nullptr;
+    const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
+                                                 reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
+                                                 st, top_hist);
+    *cells = reinterpret_cast<uint64_t*>(o);
+    return ok;
+  }
+  return false;
+}
 
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
                    cudaStream_t s, SortStats* st, const uint32_t* top_hist) {
