@@ -342,9 +342,62 @@ __global__ void __launch_bounds__(kBktThreads)
     }
     uint16_t* cur = ia;
     uint16_t* nxt = ib;
+    // ---- fast path: ONE unstable counting pass on the most significant
+    // varying byte P1 (shared-memory atomics give the slot), then the thread
+    // owning each digit insertion-sorts that digit's run on the whole key
+    // (runs hold ~S/256 keys).  A run longer than 32 (skewed data) sends the
+    // bucket to the stable two-byte path below.
+    bool fast_done = false;
+    if (P1 >= 0) {
+      uint32_t* h = &cnt[0][0];
+      h[tid] = 0;  // kBktThreads == 256 digits
+      __syncthreads();
+      uint32_t rk[MAXC], dg[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = c * kBktThreads + tid;
+        dg[c] = 256u;
+        if (i < S) {
+          dg[c] = key_byte(s[i], P1);
+          rk[c] = atomicAdd(&h[dg[c]], 1u);
+        }
+      }
+      __syncthreads();
+      const uint32_t rl = h[tid];
+      uint32_t all;
+      const uint32_t rb = block_excl_scan(rl, s_scan, &all);
+      cnt[1][tid] = rb;
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = c * kBktThreads + tid;
+        if (i < S) nxt[cnt[1][dg[c]] + rk[c]] = uint16_t(i);
+      }
+      __syncthreads();
+      int too_long = 0;
+      if (rl > 32) {
+        too_long = 1;
+      } else {
+        for (uint32_t a = rb + 1; a < rb + rl; ++a) {
+          const uint16_t v = nxt[a];
+          const K kv = s[v];
+          uint32_t q = a;
+          while (q > rb && key_less(kv, s[nxt[q - 1]])) {
+            nxt[q] = nxt[q - 1];
+            --q;
+          }
+          nxt[q] = v;
+        }
+      }
+      if (!__syncthreads_or(too_long)) {
+        cur = nxt;
+        nxt = ia;
+        fast_done = true;
+      }
+    }
     // ---- stable LSD passes: P2 then P1
     const int seg = ((S + kBktWarps * 32 - 1) / (kBktWarps * 32)) * 32;  // rows per warp
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 2 && !fast_done; ++pass) {
       const int P = pass == 0 ? P2 : P1;
       if (P < 0) continue;
       for (int i = tid; i < kBktWarps * kRadix; i += kBktThreads) (&cnt[0][0])[i] = 0;
@@ -397,7 +450,7 @@ __global__ void __launch_bounds__(kBktThreads)
     // thread at the head of each run insertion-sorts it on the whole key.
     // Runs longer than 32 (skewed data) fall back to odd-even rounds.
     int long_run = 0;
-    if (P2 >= 0) {
+    if (P2 >= 0 && !fast_done) {
       auto tb = [&](int i) -> uint32_t {
         const K k = s[cur[i]];
         return (key_byte(k, P1) << 8) | key_byte(k, P2);
