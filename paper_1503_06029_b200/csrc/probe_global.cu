@@ -59,8 +59,9 @@ __global__ void __launch_bounds__(kTileCells)
                    unsigned long long* total, unsigned long long* issued,
                    uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
                    uint4* __restrict__ ovf, uint32_t* ovf_n) {
-  __shared__ uint64_t ebuf[kTileEdgeCap];
-  __shared__ uint32_t s_cnt;
+  constexpr int kWarpEdgeCap = kTileEdgeCap / (kTileCells / 32);
+  __shared__ uint64_t ebuf[kTileCells / 32][kWarpEdgeCap];
+  __shared__ uint32_t s_wcnt[kTileCells / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_base;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -69,15 +70,14 @@ __global__ void __launch_bounds__(kTileCells)
   const int b = g.b;
   const int fb = g.b + g.fextra;
   unsigned long long my_issued = 0;
+  uint64_t* wbuf = ebuf[tid >> 5];
 
   while (true) {
-    if (tid == 0) {
-      s_tile = atomicAdd(ticket, 1u);
-      s_cnt = 0;
-    }
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
+    uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
     const int64_t i = i_lo + tile * kTileCells + tid;
     const bool valid = i < i_hi;
     // ---- the cell
@@ -125,13 +125,13 @@ __global__ void __launch_bounds__(kTileCells)
           }
           return;
         }
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&s_cnt, uint32_t(__popc(hb)));
-        base = __shfl_sync(kFull, base, leader);
+        // per-warp buffer: the warp owns 32 consecutive cells, so its list
+        // sorted on its own is a contiguous piece of the tile's sorted list
         if (hit) {
-          const uint32_t pos = base + __popc(hb & lt);
-          if (pos < kTileEdgeCap) ebuf[pos] = e;
+          const uint32_t pos = wfill + __popc(hb & lt);
+          if (pos < kWarpEdgeCap) wbuf[pos] = e;
         }
+        wfill += __popc(hb);
       }
     };
 
@@ -360,22 +360,57 @@ __global__ void __launch_bounds__(kTileCells)
       }
       emit(hit, e);
     }
+    if (spill) {  // spill mode: no ordered output
+      __syncthreads();
+      continue;
+    }
+    // ---- tile output.  Each warp sorts its own list (bitonic network in its
+    // shared buffer, warp-synchronous: no block barrier per stage); the
+    // tile's block of the scratch list is reserved with one atomicAdd and
+    // every warp writes its sorted list at its prefix inside the block.
+    // tile_cnt/tile_pos let a scan + copy place the blocks in canonical order
+    // afterwards (a look-back would make each tile wait for its predecessor).
+    {
+      const uint32_t n = min(wfill, uint32_t(kWarpEdgeCap));
+      int P = 1;
+      while (P < int(n)) P <<= 1;
+      for (int q = int(n) + lane; q < P; q += 32) wbuf[q] = ~0ull;
+      __syncwarp();
+      for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          const int lg = __ffs(jj) - 1;
+          for (int p = lane; p < (P >> 1); p += 32) {
+            const int a = ((p >> lg) << (lg + 1)) | (p & (jj - 1));
+            const int c = a + jj;
+            const bool up = (a & kk) == 0;
+            const uint64_t x = wbuf[a], y = wbuf[c];
+            if ((y < x) == up) {
+              wbuf[a] = y;
+              wbuf[c] = x;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) s_wcnt[tid >> 5] = wfill;
+    }
     __syncthreads();
-    if (spill) continue;  // spill mode: no ordered output
-    // ---- tile output: the tile's hits, sorted, go to a block of the
-    // scratch list reserved with one atomicAdd; tile_cnt/tile_pos let a
-    // scan + copy place every block at its canonical offset afterwards
-    // (a look-back here would make each tile wait for its predecessor's
-    // probes to finish).
-    const uint32_t cnt = s_cnt;
     if (tid == 0) {
+      uint32_t cnt = 0;
+      bool over = false;
+      for (int w = 0; w < kTileCells / 32; ++w) {
+        const uint32_t c = s_wcnt[w];
+        s_wcnt[w] = cnt;
+        cnt += c;
+        over |= c > uint32_t(kWarpEdgeCap);
+      }
       status[tile] = cnt;  // tile_cnt
-      if (cnt > kTileEdgeCap) {
-        // rare: hits beyond the shared buffer were dropped; the host re-runs
-        // this tile in spill mode and writes its range directly
+      if (over) {
+        // rare: hits beyond a warp buffer were dropped; the host re-runs this
+        // tile in spill mode and writes its range directly
         const uint32_t k = atomicAdd(ovf_n, 1u);
         ovf[k] = make_uint4(uint32_t(tile), 0u, cnt, 0u);
-        s_base = 0;
+        s_base = 0xffffffffu;
       } else {
         s_base = uint32_t(atomicAdd(total, (unsigned long long)cnt));
       }
@@ -383,29 +418,11 @@ __global__ void __launch_bounds__(kTileCells)
     }
     __syncthreads();
     const uint32_t base = s_base;
-    if (cnt <= kTileEdgeCap) {
-      int P = 1;
-      while (P < int(cnt)) P <<= 1;
-      for (int q = cnt + tid; q < P; q += kTileCells) ebuf[q] = ~0ull;
-      __syncthreads();
-      for (int kk = 2; kk <= P; kk <<= 1) {
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-          for (int p = tid; p < (P >> 1); p += kTileCells) {
-            const int a = 2 * j * (p / j) + (p % j);
-            const int c = a + j;
-            const bool up = (a & kk) == 0;
-            const uint64_t x = ebuf[a], y = ebuf[c];
-            if ((y < x) == up) {
-              ebuf[a] = y;
-              ebuf[c] = x;
-            }
-          }
-          __syncthreads();
-        }
-      }
-      for (uint32_t q = tid; q < cnt; q += kTileCells) {
-        const uint64_t pos = uint64_t(base) + q;
-        if (pos < cap) out[pos] = ebuf[q];  // sorted (i << 32 | j) keys
+    if (base != 0xffffffffu) {
+      const uint32_t woff = s_wcnt[tid >> 5];
+      for (uint32_t q = lane; q < wfill; q += 32) {
+        const uint64_t pos = uint64_t(base) + woff + q;
+        if (pos < cap) out[pos] = wbuf[q];  // sorted (i << 32 | j) keys
       }
     }
     __syncthreads();
@@ -449,7 +466,7 @@ __global__ void k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t t = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
     const uint32_t c = cntv[t];
-    if (c > kTileEdgeCap) continue;  // overflow tile: written by the spill path
+    if (pos[t] == 0xffffffffu) continue;  // overflow tile: written by the spill path
     const uint64_t* src = scratch + pos[t];
     uint64_t* dst = out + off[t];
     for (uint32_t q = lane; q < c; q += 32) {
