@@ -471,27 +471,25 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(mt, 1) * 8, s));
     launch_tile_copy(hits.p, toff.p, tinfo.p + ntiles, tinfo.p, ntiles, eout, s);
     if (novf) {
-      // tiles whose hits overflowed the shared buffer: re-run each in spill
-      // mode, sort its hits and write them at the tile's offset
-      std::vector<uint4> hv(novf);
-      CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
-      std::vector<uint32_t> hoff(ntiles);
-      CG_CUDA(cudaMemcpyAsync(hoff.data(), toff.p, size_t(ntiles) * 4, cudaMemcpyDeviceToHost, s));
-      CG_CUDA(cudaStreamSynchronize(s));
-      const int tc = probe_global_tile_cells();
-      for (const uint4& t : hv) {
-        const uint32_t cnt = t.z;
-        DevBuf<uint64_t> sp1(cnt, s), sp2(cnt, s);
-        DevBuf<uint32_t> st1(2, s);
-        CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
-        CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
-        const int64_t lo = i_lo + int64_t(t.x) * tc, hi = std::min<int64_t>(i_hi, lo + tc);
-        launch_probe_global(g, o.lcp_prune, lo, hi, nullptr, 0, st1.p, ticket.p, ctr.p + 3,
-                            ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, cnt, ctr.p + 2, s);
-        uint64_t* so = sp1.p;
-        if (cnt > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, cnt, 64, &so, nullptr, s, nullptr);
-        launch_rotate_edges(so, cnt, eout + hoff[t.x], s);
-      }
+      // tiles whose hits overflowed a warp buffer (dense graphs): re-run all
+      // of them at once in spill mode, sort the spilled hits (tiles cover
+      // disjoint source ranges, so the sorted list is the tiles' lists in
+      // tile order) and drop each tile's part at its canonical offset
+      const uint64_t ms = mt - m;
+      DevBuf<uint8_t> sel(size_t(ntiles), s);
+      DevBuf<uint32_t> sstart(size_t(ntiles), s);
+      CG_CUDA(cudaMemsetAsync(sel.p, 0, size_t(ntiles), s));
+      CG_CUDA(cudaMemsetAsync(sstart.p, 0, size_t(ntiles) * 4, s));
+      launch_spill_select(ovf.p, uint32_t(novf), sel.p, sstart.p, s);
+      launch_scan_u32(sstart.p, ntiles, s);
+      DevBuf<uint64_t> sp1(ms, s), sp2(ms, s);
+      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
+      CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tinfo.p, ticket.p, ctr.p + 3,
+                          ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
+      uint64_t* so = sp1.p;
+      if (ms > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, int64_t(ms), 64, &so, nullptr, s, nullptr);
+      launch_spill_place(so, int64_t(ms), i_lo, toff.p, sstart.p, eout, s);
     }
     m = mt;
     tm.mark();  // 7: edges (placement of the already sorted tile blocks)

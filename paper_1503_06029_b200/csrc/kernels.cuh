@@ -141,7 +141,14 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
                          uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                          unsigned long long* total, unsigned long long* issued, uint4* ovf,
                          uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
-                         unsigned long long* spill_n, cudaStream_t s);
+                         unsigned long long* spill_n, cudaStream_t s,
+                         const uint8_t* tile_sel = nullptr);
+// overflow tiles (batched spill path): selection mask + per-tile counts
+void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t* scnt,
+                         cudaStream_t s);
+// sorted spilled hits -> out[toff[t] + q - sstart[t]] as (i, j) pairs
+void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint32_t* toff,
+                        const uint32_t* sstart, uint64_t* out, cudaStream_t s);
 // place every tile block at its canonical offset off[t] as (i, j) pairs
 void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s);

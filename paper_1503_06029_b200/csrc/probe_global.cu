@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(kTileCells)
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                    unsigned long long* total, unsigned long long* issued,
                    uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
-                   uint4* __restrict__ ovf, uint32_t* ovf_n) {
+                   uint4* __restrict__ ovf, uint32_t* ovf_n,
+                   const uint8_t* __restrict__ tile_sel) {
   constexpr int kWarpEdgeCap = kTileEdgeCap / (kTileCells / 32);
   __shared__ uint64_t ebuf[kTileCells / 32][kWarpEdgeCap];
   __shared__ uint32_t s_wcnt[kTileCells / 32];
@@ -77,6 +78,10 @@ __global__ void __launch_bounds__(kTileCells)
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
+    if (tile_sel && !tile_sel[tile]) {  // spill re-run: only the overflow tiles
+      __syncthreads();
+      continue;
+    }
     uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
     const int64_t i = i_lo + tile * kTileCells + tid;
     const bool valid = i < i_hi;
@@ -445,15 +450,51 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
                          uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                          unsigned long long* total, unsigned long long* issued, uint4* ovf,
                          uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
-                         unsigned long long* spill_n, cudaStream_t s) {
+                         unsigned long long* spill_n, cudaStream_t s, const uint8_t* tile_sel) {
   const int64_t ntiles = (i_hi - i_lo + kTileCells - 1) / kTileCells;
   if (ntiles <= 0) return;
   const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms()) * 8));
   switch (g.W) {
-    case 1: k_probe_global<1><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
-    case 2: k_probe_global<2><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
-    default: k_probe_global<0><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n); break;
+    case 1: k_probe_global<1><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 2: k_probe_global<2><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    default: k_probe_global<0><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
   }
+  CG_LAUNCH_CHECK();
+}
+
+// overflow tiles: sel[t] = 1, scnt[t] = their hit count (0 elsewhere)
+__global__ void k_spill_select(const uint4* __restrict__ ovf, uint32_t novf, uint8_t* __restrict__ sel,
+                               uint32_t* __restrict__ scnt) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < novf; q += gridDim.x * blockDim.x) {
+    sel[ovf[q].x] = 1;
+    scnt[ovf[q].x] = ovf[q].z;
+  }
+}
+
+// sorted spilled hits -> their tiles' canonical ranges:
+// dst = toff[t] + (q - sstart[t]) with t the tile of the hit's source cell
+__global__ void k_spill_place(const uint64_t* __restrict__ sorted, int64_t m, int64_t i_lo,
+                              const uint32_t* __restrict__ toff, const uint32_t* __restrict__ sstart,
+                              uint64_t* __restrict__ out) {
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < m;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = sorted[q];
+    const int64_t t = (int64_t(k >> 32) - i_lo) / kTileCells;
+    out[toff[t] + (q - sstart[t])] = (k >> 32) | (k << 32);
+  }
+}
+
+void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t* scnt,
+                         cudaStream_t s) {
+  k_spill_select<<<std::max(1u, std::min((novf + 255) / 256, 1024u)), 256, 0, s>>>(ovf, novf, sel, scnt);
+  CG_LAUNCH_CHECK();
+}
+
+void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint32_t* toff,
+                        const uint32_t* sstart, uint64_t* out, cudaStream_t s) {
+  if (m <= 0) return;
+  const int64_t blocks = std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 16);
+  k_spill_place<<<unsigned(blocks), 256, 0, s>>>(sorted, m, i_lo, toff, sstart, out);
   CG_LAUNCH_CHECK();
 }
 
