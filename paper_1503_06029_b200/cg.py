@@ -391,16 +391,19 @@ def dist_merge_probe(runs: torch.Tensor, counts, rank: int, ell: int, *, stream=
             _stats_dict(st) if want_stats else {})
 
 
-def dist_finalize(gathered: torch.Tensor, counts, *, stream=None) -> torch.Tensor:
+def dist_finalize(gathered: torch.Tensor, counts, *, stream=None,
+                  dict_kind="global") -> torch.Tensor:
     """cg_dist_finalize: gathered = int32 [G, stride, 2] per-rank edge lists
-    (counts[g] valid pairs each) -> canonical edge list int32 [m, 2]."""
+    (counts[g] valid pairs each) -> canonical edge list int32 [m, 2].
+    dict_kind must match the one the lists were probed with ("global": the
+    lists are canonical ranges -> concatenation; else a sort)."""
     if gathered.dtype != torch.int32 or gathered.dim() != 3 or not gathered.is_cuda:
         raise CgError(CG_EINVAL, "gathered must be a CUDA int32 tensor [G, stride, 2]")
     gathered = gathered.contiguous()
     G, stride, _ = gathered.shape
     cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
     stream = stream or torch.cuda.current_stream(gathered.device)
-    o, _, _ = _opts(stream, "sorted", True, -1, False, False)
+    o, _, _ = _opts(stream, dict_kind, True, -1, False, False)
     e = cg_edges()
     with torch.cuda.device(gathered.device):
         _check(lib().cg_dist_finalize(ctypes.c_void_p(gathered.data_ptr()), cnt, G, stride,

@@ -380,8 +380,9 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
     cellbuf.alloc(size_t(n) * W, s, Mem::Persist);
     launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
-  } else {
-    // cells came out of the fused MSD pass: per-cell popcount and LCP
+  } else if (!sh.cells_only && (o.dict_kind != CG_DICT_GLOBAL || o.index_out)) {
+    // cells came out of the fused MSD pass: per-cell popcount and LCP for the
+    // layered dictionary (the global-dictionary probe derives lcp itself)
     launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
   }
   uint32_t* hf = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
@@ -1112,7 +1113,11 @@ int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G,
       at += counts[g];
     }
     eout = static_cast<uint64_t*>(dev_alloc(size_t(std::max<int64_t>(m, 1)) * 8, s));
-    if (m > 0) {
+    if (m > 0 && o.dict_kind == CG_DICT_GLOBAL) {
+      // global dictionary: rank g probed the g-th contiguous canonical range
+      // and its list is sorted, so the concatenation is the canonical list
+      CG_CUDA(cudaMemcpyAsync(eout, cat.p, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+    } else if (m > 0) {
       launch_rotate_edges(cat.p, m, k1.p, s);
       uint64_t* ko = k1.p;
       if (m > 1) radix_sort<uint64_t>(k1.p, k2.p, nullptr, nullptr, nullptr, false, m, 64, &ko, nullptr, s, nullptr);

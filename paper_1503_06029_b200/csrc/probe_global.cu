@@ -105,8 +105,18 @@ __global__ void __launch_bounds__(kTileCells)
     int kmax = -1;
     if (valid) {
       if (lcp_prune) {
-        const int l = g.lcp[i];
-        kmax = (l == 0xffff) ? -1 : min(l, g.ell - 1);
+        // lcp(V_i, V_{i+1}) from the next row (the neighbouring lane's cell,
+        // so an L1 hit); the last cell has no successor and probes nothing
+        if (i + 1 < g.n_cells) {
+          const uint64_t* Np = g.keys + (i + 1) * W;
+          int l = -1;
+          const int n = WC > 0 ? WC : W;
+          for (int w = 0; w < n && l < 0; ++w) {
+            const uint64_t x = Np[w] ^ V(w);
+            if (x) l = 64 * w + __clzll(x);
+          }
+          kmax = (l < 0) ? g.ell - 1 : min(l, g.ell - 1);
+        }
       } else {
         kmax = g.ell - 1;
       }

@@ -49,7 +49,7 @@ def logical_ranks(cg, x: np.ndarray, G: int, dict_kind="global"):
     for t in tables[1:]:
         assert torch.equal(t, tables[0])
     ecounts = [e.shape[0] for e in edges]
-    final = cg.dist_finalize(_pad_stack(edges, torch.int32, (2,)), ecounts)
+    final = cg.dist_finalize(_pad_stack(edges, torch.int32, (2,)), ecounts, dict_kind=dict_kind)
     torch.cuda.synchronize()
     return (tables[0].cpu().numpy().view(np.uint64), final.cpu().numpy().view(np.uint32),
             ecounts)
