@@ -248,6 +248,15 @@ __device__ __forceinline__ uint32_t key_byte(const uint64_t& k, int P) {
 __device__ __forceinline__ uint32_t key_byte(const ulonglong2& k, int P) {
   return P < 8 ? uint32_t(k.x >> (56 - 8 * P)) & 255u : uint32_t(k.y >> (56 - 8 * (P - 8))) & 255u;
 }
+// the key's bits from (MSB-first) position f on, left-aligned in 64 bits
+__device__ __forceinline__ uint64_t key_bits_at(const uint64_t& k, int f) {
+  return f < 64 ? (k << f) : 0ull;
+}
+__device__ __forceinline__ uint64_t key_bits_at(const ulonglong2& k, int f) {
+  if (f == 0) return k.x;
+  if (f < 64) return (k.x << f) | (k.y >> (64 - f));
+  return f < 128 ? (k.y << (f - 64)) : 0ull;
+}
 __device__ __forceinline__ void key_andor(const uint64_t& k, uint64_t* a, uint64_t* o) {
   a[0] &= k;
   o[0] |= k;
@@ -349,44 +358,71 @@ __global__ void __launch_bounds__(kBktThreads)
     // bucket to the stable two-byte path below.
     bool fast_done = false;
     if (P1 >= 0) {
-      uint32_t* h = &cnt[0][0];
-      h[tid] = 0;  // kBktThreads == 256 digits
+      // 11-bit digit starting at the most significant varying bit: with
+      // ~1024 keys per bucket the runs are 0-2 keys long
+      constexpr int kDBits = 11, kBins = 1 << kDBits, kPer = kBins / kBktThreads;
+      int f = 0;
+      if (dif[0]) f = __clzll(dif[0]);
+      else if (NW > 1) f = 64 + __clzll(dif[NW > 1 ? 1 : 0]);
+      auto dig = [&](const K& k) -> uint32_t { return key_bits_at(k, f) >> (64 - kDBits); };
+      uint32_t* h = &cnt[0][0];  // 8 * 256 = 2048 counters
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) h[tid * kPer + q] = 0;
       __syncthreads();
       uint32_t rk[MAXC], dg[MAXC];
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
-        dg[c] = 256u;
+        dg[c] = kBins;
         if (i < S) {
-          dg[c] = key_byte(s[i], P1);
+          dg[c] = dig(s[i]);
           rk[c] = atomicAdd(&h[dg[c]], 1u);
         }
       }
       __syncthreads();
-      const uint32_t rl = h[tid];
+      uint32_t rl[kPer];
+      uint32_t loc = 0;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        rl[q] = h[tid * kPer + q];
+        loc += rl[q];
+      }
       uint32_t all;
-      const uint32_t rb = block_excl_scan(rl, s_scan, &all);
-      cnt[1][tid] = rb;
+      const uint32_t rb0 = block_excl_scan(loc, s_scan, &all);
+      uint32_t rbq[kPer];
+      {
+        uint32_t run = rb0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          rbq[q] = run;
+          h[tid * kPer + q] = run;
+          run += rl[q];
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
-        if (i < S) nxt[cnt[1][dg[c]] + rk[c]] = uint16_t(i);
+        if (i < S) nxt[h[dg[c]] + rk[c]] = uint16_t(i);
       }
       __syncthreads();
       int too_long = 0;
-      if (rl > 32) {
-        too_long = 1;
-      } else {
-        for (uint32_t a = rb + 1; a < rb + rl; ++a) {
-          const uint16_t v = nxt[a];
-          const K kv = s[v];
-          uint32_t q = a;
-          while (q > rb && key_less(kv, s[nxt[q - 1]])) {
-            nxt[q] = nxt[q - 1];
-            --q;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint32_t rb = rbq[q], len = rl[q];
+        if (len > 32) {
+          too_long = 1;
+        } else {
+          for (uint32_t a = rb + 1; a < rb + len; ++a) {
+            const uint16_t v = nxt[a];
+            const K kv = s[v];
+            uint32_t z = a;
+            while (z > rb && key_less(kv, s[nxt[z - 1]])) {
+              nxt[z] = nxt[z - 1];
+              --z;
+            }
+            nxt[z] = v;
           }
-          nxt[q] = v;
         }
       }
       if (!__syncthreads_or(too_long)) {
@@ -508,22 +544,49 @@ __global__ void __launch_bounds__(kBktThreads)
       // compacted at the front of the bucket's range; ucnt[b] = unique count.
       // (Keys of different buckets differ in their prefix, so the first key
       // of a bucket is always new.)
-      const int nchunk = (S + kBktThreads - 1) / kBktThreads;
-      uint32_t run = 0;
-      for (int c = 0; c < nchunk; ++c) {
+      // chunk c, thread t -> sorted position c*256 + t (coalesced writes);
+      // per-(chunk, warp) ballot counts, one scan over them in (c, w) order
+      uint32_t* wc = &cnt[1][0];  // MAXC * 8 <= 128 counters
+      uint32_t bl[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
-        bool f = false;
-        K k{};
-        if (i < S) {
-          k = s[cur[i]];
-          f = (i == 0) || key_less(s[cur[i - 1]], k);
-        }
-        uint32_t tot;
-        const uint32_t r = block_excl_scan(f ? 1u : 0u, s_scan, &tot);
-        if (f) keys[lo + run + r] = k;
-        run += tot;
+        const bool f = i < S && (i == 0 || key_less(s[cur[i - 1]], s[cur[i]]));
+        bl[c] = __ballot_sync(kFull, f);
+        if (lane == 0) wc[c * kBktWarps + wid] = __popc(bl[c]);
       }
-      if (tid == 0) ucnt[bk] = run;
+      __syncthreads();
+      if (tid < 32) {  // exclusive scan of MAXC * 8 counts by one warp
+        constexpr int NWC = MAXC * kBktWarps;
+        constexpr int PER = (NWC + 31) / 32;
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          v[q] = (tid * PER + q < NWC) ? wc[tid * PER + q] : 0u;
+          sum += v[q];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
+          if (tid >= o) inc += y;
+        }
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          if (tid * PER + q < NWC) wc[tid * PER + q] = run;
+          run += v[q];
+        }
+        if (tid == 31) ucnt[bk] = inc;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        if ((bl[c] >> lane) & 1u) {
+          const int i = c * kBktThreads + tid;
+          keys[lo + wc[c * kBktWarps + wid] + __popc(bl[c] & lt)] = s[cur[i]];
+        }
+      }
     }
     __syncthreads();
   }
