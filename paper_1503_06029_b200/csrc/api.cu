@@ -413,11 +413,14 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   if (o.dict_kind == CG_DICT_GLOBAL && !o.index_out) {
     tm.mark();  // 4: layers (implicit in the global dictionary)
     // ---- a5 one prefix index + filter over the canonical table
-    const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 2;
+    // defaults measured on C5 (tools/tune_probe.sh): 1-2 cells per bucket and
+    // a b+5-bit filter (probe 4.51 ms vs 5.00 ms at 4-8 cells / b+7 bits)
+    const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 0;
     int b = 0;
     while (b < 28 && (uint64_t(nc) >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
-    int fextra = kFilterExtra;
+    int fextra = 5;
     if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
+    fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
     DevBuf<uint32_t> T((size_t(1) << b) + 1, s);
     DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s);
     CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));

@@ -19,7 +19,7 @@ x, d = bench.make_c5_device(torch, lg, dev)
 for i in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = cg.build(x, want_stats=True)
+    r = cg.build(x, want_stats=True, bucket_log2=int(os.environ.get('CG_BUCKET_LOG2', '-1')))
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
     st = {k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.stats.items()}
@@ -31,7 +31,7 @@ import cProfile, pstats  # noqa: E402
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 pr.enable()
-r = cg.build(x, want_stats=True)
+r = cg.build(x, want_stats=True, bucket_log2=int(os.environ.get('CG_BUCKET_LOG2', '-1')))
 torch.cuda.synchronize()
 pr.disable()
 print(json.dumps({k: round(v, 1) for k, v in r.stats.items() if k.startswith("us_host")}))
