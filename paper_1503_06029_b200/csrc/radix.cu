@@ -491,15 +491,25 @@ __global__ void __launch_bounds__(kBktThreads)
         const K k = s[cur[i]];
         return (key_byte(k, P1) << 8) | key_byte(k, P2);
       };
-      for (int i = tid; i + 1 < S; i += kBktThreads) {
+      // find the run heads first (read-only), then sort after a barrier
+      int hd[MAXC], hl[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        hl[c] = 0;
+        const int i = c * kBktThreads + tid;
+        hd[c] = i;
+        if (i + 1 >= S) continue;
         const uint32_t bi = tb(i);
         if (bi != tb(i + 1) || (i > 0 && tb(i - 1) == bi)) continue;  // not a run head
         int j = i + 2;
         while (j < S && j - i <= 32 && tb(j) == bi) ++j;
-        if (j - i > 32) {
-          long_run = 1;
-          continue;
-        }
+        if (j - i > 32) long_run = 1;
+        else hl[c] = j - i;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = hd[c], j = hd[c] + hl[c];
         for (int a = i + 1; a < j; ++a) {
           const uint16_t v = cur[a];
           const K kv = s[v];

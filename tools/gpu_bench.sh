@@ -1,11 +1,15 @@
-# full bench line + launch list of the same command + ncu full captures of the top kernels
+# full bench line + launch list of the same command + ncu full captures of the top kernels + sanitizers
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
 cat gpurun_out/bench.json
 CG_BENCH_ALLOW_SHORT=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-for k in k_probe k_bucket_sort k_onesweep k_pack k_gather_rows k_dedupe; do
+for k in k_probe_global k_bucket_sort k_onesweep k_pack k_global_index k_tile_copy; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/prof_$k -f python tools/diag_stages.py 26 1 > gpurun_out/ncu_$k.log 2>&1
 done
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t --error-exitcode 7 python tools/sanitize_run.py > gpurun_out/sanitize_$t.log 2>&1; echo "sanitizer $t rc=$?" >> gpurun_out/sanitize_summary.txt
+done
+cat gpurun_out/sanitize_summary.txt
 ls gpurun_out

@@ -1,0 +1,26 @@
+"""Small builds for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): every default-path kernel plus the layered path, the spill path
+and cg_query on tiny inputs."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1503_06029_b200 import cg  # noqa: E402
+
+cases = [synth.config("C1")["bytes"], synth.clustered_bytes(3, 3000, 100, 4, 3),
+         synth.hypercube(10), synth.random_bytes(1, 5000, 200, dup_frac=0.5)]
+for x in cases:
+    xt = torch.from_numpy(x).cuda()
+    for kw in (dict(), dict(dict_kind="sorted", want_index=True), dict(sort_kind="lsd")):
+        r = cg.build(xt, **kw)
+        if r.index is not None:
+            q = r.cells[:64].contiguous()
+            r.index.query(q)
+        torch.cuda.synchronize()
+        del r
+print("sanitize run ok")
