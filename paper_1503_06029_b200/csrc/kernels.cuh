@@ -47,8 +47,19 @@ int msd_prefix_bits(int64_t n);
 // end up in keys or alt (*cells), *nc of them.  false = a bucket overflowed
 // (keys/alt then hold the same SET of keys, bucket-ordered; run the full
 // sort + dedupe instead).
+// pre_off (device, 2^pre_B + 1 entries): keys already grouped by their top
+// pre_B bits (launch_pack_scatter) -> no global radix pass.
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
-                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist);
+                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
+                     const uint32_t* pre_off = nullptr, int pre_B = 0);
+// MSD scatter pack (W <= 2, ell % 16 == 0, 16-byte aligned rows): histogram of
+// the top B bits from the first 16 bytes of each row, then pack straight into
+// the prefix buckets (start = exclusive scan of the histogram, cursor zeroed).
+bool pack_scatter_ok(const uint8_t* vecs, int ell);
+void launch_prefix_hist(const uint8_t* vecs, int64_t n, int ell, int B, uint32_t* hist,
+                        cudaStream_t s);
+void launch_pack_scatter(const uint8_t* vecs, int64_t n, int ell, int B, const uint32_t* start,
+                         uint32_t* cursor, uint64_t* keys, uint32_t* err, cudaStream_t s);
 // popcount (optional) and lcp with the next cell, for a canonical table
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
                       cudaStream_t s);

@@ -807,19 +807,26 @@ __global__ void k_compact_buckets(const K* __restrict__ src, const uint32_t* __r
 
 template <class K>
 bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaStream_t s,
-                      SortStats* st, const uint32_t* top_hist) {
-  const int B = msd_prefix_bits(n);
-  K* ko = nullptr;
-  radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
-                  s, st, top_hist);
+                      SortStats* st, const uint32_t* top_hist, const uint32_t* pre_off = nullptr,
+                      int pre_B = 0) {
+  // pre_off: keys are already grouped by their top pre_B bits (scatter pack),
+  // pre_off[b] = first row of bucket b -- no global pass needed
+  const int B = pre_off ? pre_B : msd_prefix_bits(n);
+  K* ko = keys;
+  if (!pre_off)
+    radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
+                    s, st, top_hist);
   const int64_t nb = int64_t(1) << B;
-  DevBuf<uint32_t> off(size_t(nb) + 1, s);
+  DevBuf<uint32_t> offb(pre_off ? 1 : size_t(nb) + 1, s);
+  const uint32_t* offp = pre_off ? pre_off : offb.p;
   DevBuf<uint32_t> ucnt(size_t(nb), s), uoff(size_t(nb), s);
   DevBuf<uint32_t> flag(1, s);
   CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
-  k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, off.p);
-  CG_LAUNCH_CHECK();
-  launch_bucket_sort<K>(ko, off.p, n, nb, B, flag.p, ucnt.p, s);
+  if (!pre_off) {
+    k_bucket_bounds<K><<<grid_for(n, 256, 16), 256, 0, s>>>(ko, n, B, offb.p);
+    CG_LAUNCH_CHECK();
+  }
+  launch_bucket_sort<K>(ko, offp, n, nb, B, flag.p, ucnt.p, s);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
   uint32_t* h = static_cast<uint32_t*>(host_stage(3 * sizeof(uint32_t)));
@@ -834,7 +841,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   if (total != n) {  // duplicates removed: close the gaps between buckets
     K* dst = (ko == keys) ? alt : keys;
     const int64_t blocks = std::min<int64_t>((nb * 32 + 255) / 256, int64_t(num_sms()) * 16);
-    k_compact_buckets<K><<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(ko, off.p, ucnt.p,
+    k_compact_buckets<K><<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(ko, offp, ucnt.p,
                                                                                 uoff.p, nb, dst);
     CG_LAUNCH_CHECK();
     *cells = dst;
@@ -844,10 +851,12 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
 }  // namespace
 
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
-                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist) {
+                     int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
+                     const uint32_t* pre_off, int pre_B) {
   if (W == 1) {
     uint64_t* o = nullptr;
-    const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist);
+    const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist, pre_off,
+                                               pre_B);
     *cells = o;
     return ok;
   }
@@ -855,7 +864,7 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
     ulonglong2* o = nullptr;
     const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
                                                  reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
-                                                 st, top_hist);
+                                                 st, top_hist, pre_off, pre_B);
     *cells = reinterpret_cast<uint64_t*>(o);
     return ok;
   }
