@@ -93,7 +93,7 @@ enum {
   CG_DICT_BSEARCH = 1, /* popcount layers, plain per-layer binary search (no prefix index) */
   CG_DICT_GLOBAL = 2   /* one prefix index + filter over the canonical table; the probe
                           writes the edge list in canonical order (no edge sort).  Default
-                          of cg_opts_init; an index_out request uses CG_DICT_SORTED. */
+                          of cg_opts_init; its cg_index holds a copy of the table. */
 };
 
 typedef struct {

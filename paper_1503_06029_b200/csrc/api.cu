@@ -27,6 +27,8 @@ struct cg_index {
   uint8_t* tbits = nullptr;
   uint32_t* F = nullptr;
   int device = 0;
+  bool global = false;     // CG_DICT_GLOBAL index: gview over keys/T/F
+  cgk::GlobalDict gview{};
 };
 
 namespace cgk {
@@ -381,7 +383,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
     cellbuf.alloc(size_t(n) * W, s, Mem::Persist);
     launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
-  } else if (!sh.cells_only && (o.dict_kind != CG_DICT_GLOBAL || o.index_out)) {
+  } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the
     // layered dictionary (the global-dictionary probe derives lcp itself)
     launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
@@ -411,7 +413,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
     return;
   }
-  if (o.dict_kind == CG_DICT_GLOBAL && !o.index_out) {
+  if (o.dict_kind == CG_DICT_GLOBAL) {
     tm.mark();  // 4: layers (implicit in the global dictionary)
     // ---- a5 one prefix index + filter over the canonical table
     // defaults measured on C5 (tools/tune_probe.sh): 1-2 cells per bucket and
@@ -422,8 +424,9 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     int fextra = 5;
     if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
     fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
-    DevBuf<uint32_t> T((size_t(1) << b) + 1, s);
-    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s);
+    const Mem gix = o.index_out ? Mem::Persist : Mem::Scratch;  // T/F outlive the build
+    DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
+    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
     CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
     build_global_index(cellbuf.p, nc, W, b, fextra, T.p, F.p, s);
     tm.mark();  // 5: dict
@@ -498,6 +501,18 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
     m = mt;
     tm.mark();  // 7: edges (placement of the already sorted tile blocks)
+    if (o.index_out) {
+      // the index owns its own copy of the table plus T and F
+      cg_index* ixp = new cg_index();
+      ixp->global = true;
+      ixp->keys = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
+      CG_CUDA(cudaMemcpyAsync(ixp->keys, cellbuf.p, size_t(nc) * W * 8, cudaMemcpyDeviceToDevice, s));
+      ixp->T = T.release();
+      ixp->F = F.release();
+      cudaGetDevice(&ixp->device);
+      ixp->gview = GlobalDict{ixp->keys, nullptr, ixp->T, ixp->F, b, fextra, W, ell, nc};
+      out->index = ixp;
+    }
     uint64_t* cout = nullptr;
     if (nc * 2 < n) {
       cout = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
@@ -931,7 +946,10 @@ int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_i
     if (nq < 0) throw CgError{CG_EINVAL, "nq < 0"};
     if (nq == 0) return CG_OK;
     if (!q || !self_idx || !nbr_idx) throw CgError{CG_EINVAL, "NULL query/output pointer"};
-    launch_query(idx->view, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
+    if (idx->global)
+      launch_query_global(idx->gview, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
+    else
+      launch_query(idx->view, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
     return CG_OK;
   } catch (const CgError& e) {
     set_last_error(e.msg);
@@ -941,8 +959,8 @@ int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_i
 
 int cg_index_info(const cg_index* idx, int64_t* n_cells, int32_t* ell) {
   if (!idx) return CG_EINVAL;
-  if (n_cells) *n_cells = idx->view.n_cells;
-  if (ell) *ell = idx->view.ell;
+  if (n_cells) *n_cells = idx->global ? idx->gview.n_cells : idx->view.n_cells;
+  if (ell) *ell = idx->global ? idx->gview.ell : idx->view.ell;
   return CG_OK;
 }
 

@@ -172,5 +172,7 @@ void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s);
 // ---------------------------------------------------------------- cg_query
 void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,
                   int32_t* nbr_idx, cudaStream_t s);
+void launch_query_global(const GlobalDict& g, const uint64_t* q, int64_t nq, int32_t* self_idx,
+                         int32_t* nbr_idx, cudaStream_t s);
 
 }  // namespace cgk

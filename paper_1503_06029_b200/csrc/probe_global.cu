@@ -17,12 +17,14 @@
 //     popc(R ^ V_i) = 1.
 //   far (k < b): filter bit of the target's (b+E)-prefix, then the bucket
 //     T[x]..T[x+1] of the survivors is compared (warp-flattened rounds).
-// Output (a7): a CTA owns a contiguous tile of cells; its hits are collected
-// in shared memory, sorted there by (i, j), and written at the tile's global
-// offset found by decoupled look-back in tile order -- so the concatenation
-// over tiles IS the canonical edge list.  A tile with more hits than the
-// shared buffer spills them (unordered) and records its slot range; the host
-// fixes those ranges after the kernel (sort of the spilled hits).
+// Output (a7): a CTA owns a contiguous tile of 256 cells, each warp 32 of
+// them; a warp's hits go to its shared-memory buffer and the warp sorts them
+// by (i, j) with a warp-synchronous bitonic network.  The tile reserves one
+// block of a scratch list with a single atomicAdd and records (count,
+// position); a scan of the counts + k_tile_copy then place the blocks in tile
+// order, so the concatenation IS the canonical edge list (no global sort).
+// Tiles whose hits overflow a warp buffer (dense graphs) are re-run together
+// in spill mode; their hits are sorted and dropped into their ranges.
 #include "kernels.cuh"
 
 namespace cgk {
@@ -532,6 +534,66 @@ void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32
   if (ntiles <= 0) return;
   const int64_t blocks = std::min<int64_t>((ntiles * 32 + 255) / 256, int64_t(num_sms()) * 16);
   k_tile_copy<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(scratch, off, pos, cnt, ntiles, out);
+  CG_LAUNCH_CHECK();
+}
+
+// cg_query on the global dictionary: one thread per (query r, slot s),
+// s < ell: the query with bit s negated, s == ell: the query itself; the
+// target's b-prefix bucket of the canonical table is searched (the row index
+// IS the canonical index)
+__global__ void __launch_bounds__(256)
+    k_query_global(GlobalDict g, const uint64_t* __restrict__ qv, int64_t nq,
+                   int32_t* __restrict__ self_idx, int32_t* __restrict__ nbr) {
+  const int ell = g.ell, W = g.W, b = g.b;
+  const int64_t total = nq * (ell + 1);
+  const uint64_t lastmask = (ell % 64) ? ~(~0ull >> (ell % 64)) : ~0ull;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / (ell + 1);
+    const int s = int(t - r * (ell + 1));
+    const uint64_t* Q = qv + r * W;
+    const int fw = s < ell ? (s >> 6) : -1;
+    const uint64_t bm = s < ell ? (1ull << (63 - (s & 63))) : 0ull;
+    auto tw = [&](int w) -> uint64_t {
+      const uint64_t x = (w == W - 1) ? (Q[w] & lastmask) : Q[w];
+      return x ^ (w == fw ? bm : 0ull);
+    };
+    const uint64_t t0 = tw(0);
+    const int64_t x = b ? int64_t(t0 >> (64 - b)) : 0;
+    uint32_t lo = g.T[x];
+    uint32_t len = g.T[x + 1] - lo;
+    while (len > 0) {  // lower bound of t in the bucket
+      const uint32_t half = len >> 1;
+      const uint64_t* R = g.keys + int64_t(lo + half) * W;
+      int c = 0;
+      for (int w = 0; w < W && c == 0; ++w) {
+        const uint64_t a = R[w], tv = tw(w);
+        c = a < tv ? -1 : (a > tv ? 1 : 0);
+      }
+      if (c < 0) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    int32_t found = -1;
+    if (lo < g.T[x + 1]) {
+      const uint64_t* R = g.keys + int64_t(lo) * W;
+      bool eq = true;
+      for (int w = 0; w < W && eq; ++w) eq = R[w] == tw(w);
+      if (eq) found = int32_t(lo);
+    }
+    if (s < ell) nbr[r * ell + s] = found;
+    else self_idx[r] = found;
+  }
+}
+
+void launch_query_global(const GlobalDict& g, const uint64_t* q, int64_t nq, int32_t* self_idx,
+                         int32_t* nbr_idx, cudaStream_t s) {
+  if (nq <= 0) return;
+  const int64_t blocks = std::min<int64_t>((nq * (g.ell + 1) + 255) / 256, int64_t(num_sms()) * 16);
+  k_query_global<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(g, q, nq, self_idx, nbr_idx);
   CG_LAUNCH_CHECK();
 }
 

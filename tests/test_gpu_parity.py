@@ -270,9 +270,10 @@ def test_host_entry(cg):
 
 
 # ---------------------------------------------------------------- cg_query
-def test_query_against_oracle(cg):
+@pytest.mark.parametrize("dict_kind", ["global", "sorted"])
+def test_query_against_oracle(cg, dict_kind):
     x = synth.clustered_bytes(21, 8000, 77, n_centers=4, max_flips=3)
-    cells, edges, res = gpu_build(cg, x, want_index=True)
+    cells, edges, res = gpu_build(cg, x, want_index=True, dict_kind=dict_kind)
     idx = res.index
     assert idx is not None and idx.n_cells == cells.shape[0]
     rng = np.random.default_rng(2)
