@@ -107,7 +107,7 @@ typedef struct {
   cg_stats* stats;      /* if non-NULL, stage times and counters */
 } cg_opts;
 
-/* Fill *o with defaults: stream NULL, CG_DICT_SORTED, lcp_prune 1,
+/* Fill *o with defaults: stream NULL, CG_DICT_GLOBAL, lcp_prune 1,
  * bucket_log2 -1, no index, no stats. */
 void cg_opts_init(cg_opts* o);
 
