@@ -250,32 +250,29 @@ __global__ void __launch_bounds__(kTileCells)
         emit(hit, e);
       }
     }
-    // ---- far: zero bits k < min(b, kmax + 1) (word 0, b <= 28): filter
+    // ---- far: zero bits k < min(b, kmax + 1) (word 0, b <= 28): filter.
+    // 32-bit arithmetic: bit k of the key is bit 31 - k of its top word, the
+    // filter prefix (fb <= 32 bits) fits in a u32; surv marks the survivors
+    // in the same top-word bit positions.
     uint32_t surv = 0;
     const int kfar = min(b - 1, kmax);
     if (kfar >= 0) {
-      const uint64_t y0 = v0 >> (64 - fb);
-      uint64_t z = ~v0 & (~0ull << (63 - kfar));
+      const uint32_t y0 = uint32_t(v0 >> (64 - fb));
+      const int fsh = 32 - fb;
+      uint32_t z = ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar));
       while (z) {
-        int ks[4];
-        uint32_t fw[4];
+        uint32_t bm[4], fw[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          ks[u] = -1;
-          fw[u] = 0;
-          if (z) {
-            const int c = __clzll(z);
-            z &= ~(1ull << (63 - c));
-            ks[u] = c;
-            fw[u] = __ldg(g.F + ((y0 | (1ull << (fb - 1 - c))) >> 5));
-          }
+          bm[u] = z & (0u - z);
+          z ^= bm[u];
+          fw[u] = bm[u] ? __ldg(g.F + ((y0 | (bm[u] >> fsh)) >> 5)) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (ks[u] >= 0) {
-            const uint64_t y = y0 | (1ull << (fb - 1 - ks[u]));
+          if (bm[u]) {
             ++my_issued;
-            if ((fw[u] >> (y & 31)) & 1u) surv |= 1u << ks[u];
+            if ((fw[u] >> ((y0 | (bm[u] >> fsh)) & 31)) & 1u) surv |= bm[u];
           }
         }
       }
@@ -318,7 +315,7 @@ __global__ void __launch_bounds__(kTileCells)
             k += s2;
           }
         }
-        const uint64_t bm = 1ull << (63 - k);
+        const uint64_t bm = 1ull << (32 + k);  // top-word bit k = key bit 31 - k
         const uint64_t t0 = o_v0 | bm;
         const int64_t x = int64_t(t0 >> (64 - b));
         const uint32_t lo = g.T[x], hi = g.T[x + 1];
@@ -381,17 +378,19 @@ __global__ void __launch_bounds__(kTileCells)
       __syncthreads();
       continue;
     }
-    // ---- tile output.  Each warp sorts its own list (bitonic network in its
-    // shared buffer, warp-synchronous: no block barrier per stage); the
-    // tile's block of the scratch list is reserved with one atomicAdd and
-    // every warp writes its sorted list at its prefix inside the block.
-    // tile_cnt/tile_pos let a scan + copy place the blocks in canonical order
-    // afterwards (a look-back would make each tile wait for its predecessor).
-    {
-      const uint32_t n = min(wfill, uint32_t(kWarpEdgeCap));
+    // ---- tile output.  Each warp orders its own list: short lists (<= 64,
+    // the common case) by rank counting straight into the output, longer ones
+    // by a warp-synchronous bitonic network in the shared buffer.  The tile's
+    // block of the scratch list is reserved with one atomicAdd and every warp
+    // writes its list at its prefix inside the block.  tile_cnt/tile_pos let
+    // a scan + copy place the blocks in canonical order afterwards (a
+    // look-back would make each tile wait for its predecessor).
+    const uint32_t wn = min(wfill, uint32_t(kWarpEdgeCap));
+    __syncwarp();
+    if (wn > 64) {
       int P = 1;
-      while (P < int(n)) P <<= 1;
-      for (int q = int(n) + lane; q < P; q += 32) wbuf[q] = ~0ull;
+      while (P < int(wn)) P <<= 1;
+      for (int q = int(wn) + lane; q < P; q += 32) wbuf[q] = ~0ull;
       __syncwarp();
       for (int kk = 2; kk <= P; kk <<= 1) {
         for (int jj = kk >> 1; jj > 0; jj >>= 1) {
@@ -409,8 +408,8 @@ __global__ void __launch_bounds__(kTileCells)
           __syncwarp();
         }
       }
-      if (lane == 0) s_wcnt[tid >> 5] = wfill;
     }
+    if (lane == 0) s_wcnt[tid >> 5] = wfill;
     __syncthreads();
     if (tid == 0) {
       uint32_t cnt = 0;
@@ -435,11 +434,24 @@ __global__ void __launch_bounds__(kTileCells)
     }
     __syncthreads();
     const uint32_t base = s_base;
-    if (base != 0xffffffffu) {
-      const uint32_t woff = s_wcnt[tid >> 5];
-      for (uint32_t q = lane; q < wfill; q += 32) {
-        const uint64_t pos = uint64_t(base) + woff + q;
-        if (pos < cap) out[pos] = wbuf[q];  // sorted (i << 32 | j) keys
+    if (base != 0xffffffffu && wn > 0) {
+      const uint64_t wpos = uint64_t(base) + s_wcnt[tid >> 5];
+      if (wn <= 64) {
+        // rank = number of smaller keys (the (i, j) keys are distinct);
+        // every lane reads the same word per step (broadcast)
+        const bool h0 = lane < int(wn), h1 = lane + 32 < int(wn);
+        const uint64_t e0 = h0 ? wbuf[lane] : 0ull, e1 = h1 ? wbuf[lane + 32] : 0ull;
+        uint32_t r0 = 0, r1 = 0;
+        for (uint32_t p = 0; p < wn; ++p) {
+          const uint64_t x = wbuf[p];
+          r0 += x < e0;
+          r1 += x < e1;
+        }
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = e0;
+        if (h1 && wpos + r1 < cap) out[wpos + r1] = e1;
+      } else {
+        for (uint32_t q = lane; q < wn; q += 32)
+          if (wpos + q < cap) out[wpos + q] = wbuf[q];  // sorted (i << 32 | j) keys
       }
     }
     __syncthreads();
