@@ -62,7 +62,7 @@ __device__ __forceinline__ uint32_t digit_of(const K& k, int shift) {
 
 template <class K, bool V>
 struct TileCfg {
-  static constexpr int IPT = sizeof(K) == 16 ? 8 : (V ? 12 : 16);
+  static constexpr int IPT = sizeof(K) == 16 ? 12 : (V ? 12 : 16);
   static constexpr int TILE = kSortThreads * IPT;
   static constexpr size_t SMEM = size_t(TILE) * (sizeof(K) + (V ? 4 : 0));
 };
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
 }
 
 template <class K, bool V>
-__global__ void __launch_bounds__(kSortThreads, 4)
+__global__ void __launch_bounds__(kSortThreads, 3)
     k_onesweep(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                uint32_t* __restrict__ vout, int64_t n, int shift,
                const uint32_t* __restrict__ bucket_base, uint64_t* status,
@@ -284,7 +284,8 @@ constexpr int kBktMaxRounds = 64;
 template <class K, int MAXC>  // MAXC chunks of 32 rows per warp: CAP <= 8 * 32 * MAXC
 __global__ void __launch_bounds__(kBktThreads)
     k_bucket_sort(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets,
-                  int CAP, int B, uint32_t* __restrict__ overflow, uint32_t* __restrict__ ucnt) {
+                  int CAP, int B, uint32_t* __restrict__ overflow, uint32_t* __restrict__ ucnt,
+                  const uint32_t* __restrict__ blist, const uint32_t* __restrict__ nlist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s = reinterpret_cast<K*>(smem_raw);
   uint16_t* ia = reinterpret_cast<uint16_t*>(smem_raw + size_t(CAP) * sizeof(K));
@@ -296,7 +297,10 @@ __global__ void __launch_bounds__(kBktThreads)
   constexpr int NBYTES = sizeof(K);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t lt = lanemask_lt();
-  for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x) {
+  // blist: only the listed buckets (the ones k_bucket_rank handed over)
+  const int64_t nwork = blist ? int64_t(*nlist) : nbuckets;
+  for (int64_t x = blockIdx.x; x < nwork; x += gridDim.x) {
+    const int64_t bk = blist ? int64_t(blist[x]) : x;
     const uint32_t lo = off[bk], hi = off[bk + 1];
     const int S = int(hi - lo);
     if (S <= 1) {
@@ -602,27 +606,297 @@ __global__ void __launch_bounds__(kBktThreads)
   }
 }
 
+// ---------------------------------------------------------------- bucket rank sort
+// The default bucket pass.  One CTA per prefix bucket (persistent loop), the
+// NEXT bucket prefetched into the other half of a double buffer with
+// cp.async while the current one is sorted:
+//   1. AND/OR reduction -> f, the first bit that varies inside the bucket;
+//   2. one counting pass on the 11-bit digit starting at f (shared atomics
+//      give each key a slot inside its digit's range);
+//   3. each key's final position = its digit's offset + the number of keys
+//      of the same digit that are smaller (equal keys: lower index first);
+//      digits hold ~S/2048 keys, so this is ~1 full-key compare per key;
+//   4. (ucnt) first key of each run of equal keys kept, written compacted at
+//      the front of the bucket's range, ucnt[b] = unique count.
+// A digit holding more than kRankRun keys (skewed data) or a bucket larger
+// than CAP is listed in blist for k_bucket_sort (stable byte passes).
+constexpr int kRankRun = 24;
+constexpr int kRankBits = 11;
+
+template <class K>
+__device__ __forceinline__ void cp_async_key(K* dst, const K* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if (sizeof(K) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ bool key_eq(const uint64_t& a, const uint64_t& b) { return a == b; }
+__device__ __forceinline__ bool key_eq(const ulonglong2& a, const ulonglong2& b) {
+  return a.x == b.x && a.y == b.y;
+}
+
+// (a, ia) before (b, ib): key order, equal keys by index (branch-free)
+__device__ __forceinline__ uint32_t key_before(const uint64_t& a, int ia, const uint64_t& b, int ib) {
+  return uint32_t(a < b) | (uint32_t(a == b) & uint32_t(ia < ib));
+}
+__device__ __forceinline__ uint32_t key_before(const ulonglong2& a, int ia, const ulonglong2& b,
+                                               int ib) {
+  const uint32_t ex = uint32_t(a.x == b.x);
+  return uint32_t(a.x < b.x) | (ex & uint32_t(a.y < b.y)) | (ex & uint32_t(a.y == b.y) & uint32_t(ia < ib));
+}
+
+template <class K, int MAXC>
+__global__ void __launch_bounds__(kBktThreads)
+    k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
+                  uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
+                  uint32_t* __restrict__ nlist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* buf0 = reinterpret_cast<K*>(smem_raw);
+  K* buf1 = buf0 + CAP;
+  uint16_t* nxt = reinterpret_cast<uint16_t*>(buf1 + CAP);
+  uint16_t* fin = nxt + CAP;
+  constexpr int kBins = 1 << kRankBits, kPer = kBins / kBktThreads;
+  __shared__ uint32_t h[kBins + 1];
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint64_t s_red[2][kBktWarps][2];
+  __shared__ uint32_t s_wc[MAXC * kBktWarps];
+  constexpr int NW = sizeof(K) / 8;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+
+  auto prefetch = [&](int64_t bk, K* dst) {
+    if (bk < nbuckets) {
+      const uint32_t lo = off[bk];
+      const int S = int(off[bk + 1] - lo);
+      if (S <= CAP)
+        for (int i = tid; i < S; i += kBktThreads) cp_async_key(dst + i, keys + lo + i);
+    }
+    cp_async_commit();
+  };
+  prefetch(blockIdx.x, buf0);
+  int it = 0;
+  for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x, ++it) {
+    K* s = (it & 1) ? buf1 : buf0;
+    prefetch(bk + gridDim.x, (it & 1) ? buf0 : buf1);
+    cp_async_wait1();
+    __syncthreads();
+    const uint32_t lo = off[bk], hi = off[bk + 1];
+    const int S = int(hi - lo);
+    if (S <= 1) {
+      if (ucnt && tid == 0) ucnt[bk] = uint32_t(S);
+      __syncthreads();
+      continue;
+    }
+    if (S > CAP) {
+      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
+      __syncthreads();
+      continue;
+    }
+    // ---- 1. bits that vary inside the bucket
+    uint64_t av[2] = {~0ull, ~0ull}, ov[2] = {0ull, 0ull};
+    for (int i = tid; i < S; i += kBktThreads) key_andor(s[i], av, ov);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        av[w] &= __shfl_xor_sync(kFull, av[w], o);
+        ov[w] |= __shfl_xor_sync(kFull, ov[w], o);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        s_red[0][wid][w] = av[w];
+        s_red[1][wid][w] = ov[w];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) h[tid * kPer + q] = 0u;
+    __syncthreads();
+    uint64_t dif[2] = {0ull, 0ull};
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      uint64_t a = ~0ull, o = 0ull;
+#pragma unroll
+      for (int ww = 0; ww < kBktWarps; ++ww) {
+        a &= s_red[0][ww][w];
+        o |= s_red[1][ww][w];
+      }
+      dif[w] = a ^ o;
+    }
+    int f = 0;
+    if (dif[0]) f = __clzll(dif[0]);
+    else if (NW > 1 && dif[NW > 1 ? 1 : 0]) f = 64 + __clzll(dif[NW > 1 ? 1 : 0]);
+    else f = -1;  // all keys equal
+    if (f < 0) {
+      if (ucnt) {
+        if (tid == 0) {
+          ucnt[bk] = 1u;
+          keys[lo] = s[0];
+        }
+      } else {
+        for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[i];
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- 2. counting pass on the digit at f
+    uint32_t dg[MAXC], rk[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = c * kBktThreads + tid;
+      dg[c] = 0;
+      rk[c] = 0;
+      if (i < S) {
+        dg[c] = uint32_t(key_bits_at(s[i], f) >> (64 - kRankBits));
+        rk[c] = atomicAdd(&h[dg[c]], 1u);
+      }
+    }
+    __syncthreads();
+    uint32_t cl[kPer], loc = 0;
+    int too_long = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      cl[q] = h[tid * kPer + q];
+      loc += cl[q];
+      too_long |= cl[q] > uint32_t(kRankRun);
+    }
+    uint32_t all;
+    uint32_t run = block_excl_scan(loc, s_scan, &all);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      h[tid * kPer + q] = run;
+      run += cl[q];
+    }
+    if (tid == 0) h[kBins] = uint32_t(S);
+    if (__syncthreads_or(too_long)) {
+      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
+      __syncthreads();
+      continue;
+    }
+    // ---- 3. scatter, then rank inside the digit
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = c * kBktThreads + tid;
+      if (i < S) nxt[h[dg[c]] + rk[c]] = uint16_t(i);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = c * kBktThreads + tid;
+      if (i < S) {
+        const uint32_t base = h[dg[c]], cnt = h[dg[c] + 1] - base;
+        uint32_t r = 0;
+        if (cnt == 2) {  // the common tie (e.g. a planted Hamming-1 partner)
+          const int j = nxt[base + (rk[c] ^ 1u)];
+          r = key_before(s[j], j, s[i], i);
+        } else if (cnt > 2) {
+          const K ki = s[i];
+          for (uint32_t m = 0; m < cnt; ++m) {
+            const int j = nxt[base + m];
+            r += (j != i) && key_before(s[j], j, ki, i);
+          }
+        }
+        fin[base + r] = uint16_t(i);
+      }
+    }
+    __syncthreads();
+    // ---- 4. write (deduplicated and compacted when ucnt is given)
+    if (!ucnt) {
+      for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[fin[i]];
+    } else {
+      uint32_t bl[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = c * kBktThreads + tid;
+        const bool fl = i < S && (i == 0 || !key_eq(s[fin[i - 1]], s[fin[i]]));
+        bl[c] = __ballot_sync(kFull, fl);
+        if (lane == 0) s_wc[c * kBktWarps + wid] = __popc(bl[c]);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        constexpr int NWC = MAXC * kBktWarps;
+        constexpr int PER = (NWC + 31) / 32;
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          v[q] = (tid * PER + q < NWC) ? s_wc[tid * PER + q] : 0u;
+          sum += v[q];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, inc, o);
+          if (tid >= o) inc += y;
+        }
+        uint32_t rr = inc - sum;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          if (tid * PER + q < NWC) s_wc[tid * PER + q] = rr;
+          rr += v[q];
+        }
+        if (tid == 31) ucnt[bk] = inc;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        if ((bl[c] >> lane) & 1u) {
+          const int i = c * kBktThreads + tid;
+          keys[lo + s_wc[c * kBktWarps + wid] + __popc(bl[c] & lt)] = s[fin[i]];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait0();
+}
+
 int grid_for(int64_t n, int threads, int per_sm = 8) {
   int64_t b = (n + threads - 1) / threads;
   int64_t cap = int64_t(num_sms()) * per_sm;
   return int(std::max<int64_t>(1, std::min(b, cap)));
 }
 
-// shared-memory capacity 2x the mean bucket (2048 or 4096 rows)
+// shared-memory capacity 2x the mean bucket (2048 or 4096 rows).  The rank
+// pass handles the buckets it can; the ones it lists (skewed digits, or
+// larger than its capacity) go through the stable byte-pass kernel.
 template <class K>
 void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
                         uint32_t* ucnt, cudaStream_t s) {
   const int64_t avg = (n + nb - 1) / nb;
   const int cap = avg <= 1024 ? 2048 : 4096;
+  DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
+  CG_CUDA(cudaMemsetAsync(nlist.p, 0, sizeof(uint32_t), s));
+  {
+    // rank pass: double-buffered keys + two u16 orders; 1.5x the mean bucket
+    // (3 CTAs per SM at 16-byte keys); larger buckets go to the byte passes
+    const int rcap = avg <= 1024 ? 1536 : 2048;
+    const size_t smem = size_t(rcap) * (2 * sizeof(K) + 4);
+    const int per_sm = std::max(1, int((224 << 10) / (smem + 10 * 1024)));
+    const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
+    if (rcap == 1536) {
+      CG_CUDA(cudaFuncSetAttribute(k_bucket_rank<K, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_bucket_rank<K, 6><<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+    } else {
+      CG_CUDA(cudaFuncSetAttribute(k_bucket_rank<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k_bucket_rank<K, 8><<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+    }
+    CG_LAUNCH_CHECK();
+  }
   const size_t smem = size_t(cap) * (sizeof(K) + 4);
   const int per_sm = std::max(1, int((200 << 10) / (smem + 12 * 1024)));
   const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
   if (cap == 2048) {
     CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_bucket_sort<K, 8><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt);
+    k_bucket_sort<K, 8><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt, blist.p, nlist.p);
   } else {
     CG_CUDA(cudaFuncSetAttribute(k_bucket_sort<K, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_bucket_sort<K, 16><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt);
+    k_bucket_sort<K, 16><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt, blist.p, nlist.p);
   }
   CG_LAUNCH_CHECK();
 }
@@ -687,8 +961,13 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
                           cudaMemcpyHostToDevice, s));
   const bool V = want_vals;
   // as many resident tiles per SM as registers allow: prefer shared memory
-  if (V) CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  else CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (V) {
+    CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TileCfg<K, true>::SMEM)));
+  } else {
+    CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CG_CUDA(cudaFuncSetAttribute(k_onesweep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TileCfg<K, false>::SMEM)));
+  }
   const int TILE = V ? TileCfg<K, true>::TILE : TileCfg<K, false>::TILE;
   const int64_t tiles = (n + TILE - 1) / TILE;
   DevBuf<uint64_t> status(size_t(tiles) * kRadix, s);
