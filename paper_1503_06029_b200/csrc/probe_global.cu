@@ -260,21 +260,20 @@ __global__ void __launch_bounds__(kTileCells)
       const uint32_t y0 = uint32_t(v0 >> (64 - fb));
       const int fsh = 32 - fb;
       uint32_t z = ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar));
+      my_issued += __popc(z);
+      // branch-free rounds of 4 filter loads in flight; an exhausted slot
+      // (bm = 0) re-reads the cell's own filter word and is masked out
       while (z) {
-        uint32_t bm[4], fw[4];
+        uint32_t bm[4], fa[4], fw[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           bm[u] = z & (0u - z);
           z ^= bm[u];
-          fw[u] = bm[u] ? __ldg(g.F + ((y0 | (bm[u] >> fsh)) >> 5)) : 0u;
+          fa[u] = y0 | (bm[u] >> fsh);
+          fw[u] = __ldg(g.F + (fa[u] >> 5));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (bm[u]) {
-            ++my_issued;
-            if ((fw[u] >> ((y0 | (bm[u] >> fsh)) & 31)) & 1u) surv |= bm[u];
-          }
-        }
+        for (int u = 0; u < 4; ++u) surv |= bm[u] & (0u - ((fw[u] >> (fa[u] & 31)) & 1u));
       }
     }
     // ---- far survivors, flattened over the warp
