@@ -435,7 +435,17 @@ __global__ void __launch_bounds__(kTileCells)
     const uint32_t base = s_base;
     if (base != 0xffffffffu && wn > 0) {
       const uint64_t wpos = uint64_t(base) + s_wcnt[tid >> 5];
-      if (wn <= 64) {
+      if (wn <= 32 && g.n_cells <= (int64_t(1) << 27)) {
+        // one hit per lane: rank on a 32-bit key (source lane << 27 | j),
+        // the keys exchanged by shuffles
+        const uint64_t e0 = lane < int(wn) ? wbuf[lane] : ~0ull;
+        const uint32_t k0 = lane < int(wn)
+            ? ((uint32_t(e0 >> 32) - uint32_t(i - lane)) << 27) | uint32_t(e0)
+            : 0xffffffffu;
+        uint32_t r0 = 0;
+        for (uint32_t p = 0; p < wn; ++p) r0 += __shfl_sync(kFull, k0, p) < k0;
+        if (lane < int(wn) && wpos + r0 < cap) out[wpos + r0] = e0;
+      } else if (wn <= 64) {
         // rank = number of smaller keys (the (i, j) keys are distinct);
         // every lane reads the same word per step (broadcast)
         const bool h0 = lane < int(wn), h1 = lane + 32 < int(wn);
