@@ -51,16 +51,19 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 50):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
 
     def start(self):
+        if self.period_ms <= 0:
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -71,17 +74,30 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    def mark(self):
+        """Start of the timed region.  The sampler is started before the
+        warm-up: nvidia-smi's first query initialises NVML and can hold the
+        driver for ~0.2 s, which must not land inside the timed steps."""
+        self.t0 = time.perf_counter()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.perf_counter()
+        time.sleep(2.5 * self.period_ms / 1e3)  # one more sample after the region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
+        t0 = getattr(self, "t0", 0.0)
+        inside = [r for t, r in self.rows if t0 <= t <= t1 + 1.5 * self.period_ms / 1e3]
+        # the region can be shorter than the sampling period: then the samples
+        # closest to it stand in
+        self.rows = inside or [r for _, r in sorted(self.rows, key=lambda tr: abs(tr[0] - t0))[:2]]
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -109,26 +125,31 @@ def make_c5_device(torch, lg: int, device):
 
 
 def alg_bytes(st: dict, n: int, ell: int) -> dict:
-    """Algorithmic bytes per stage: what the method
-    must move, independent of how the kernels move it."""
+    """Algorithmic (compulsory) HBM bytes per stage, DESIGN.md section 6:
+    every byte the stage must read or write at least once with the data
+    layout and number of passes of its algorithm; re-reads that caches could
+    avoid are NOT counted, so achieved/peak is an honest roofline fraction."""
     W = (ell + 63) // 64
     K = 8 * W
-    nc, m, issued = st["n_cells"], st["n_edges"], st["issued_probes"]
-    # MSD path (W <= 2): 2 top-digit passes + the bucket pass, each 2K per key;
-    # multi-word LSD (W > 2): per word 8 passes x 2 x 12 B + gathers
-    sort_key_bytes = 6 * K if W <= 2 else W * (192 + 16) + 2 * K
+    nc, m = st["n_cells"], st["n_edges"]
+    dict_b = st.get("dict_bytes", 0)
+    # MSD path (W <= 2): 2 top-digit one-sweep passes + the bucket pass, each
+    # reads and writes every key; multi-word LSD (W > 2): per word 8 passes
+    # over (u64 word, u32 index) pairs + gathers
+    sort_key_bytes = 6 * K if W <= 2 else W * (8 * 2 * 12 + 16) + 2 * K
+    tiles = (nc + 255) // 256
     return {
         "pack": n * (ell + K),
         "sort": n * sort_key_bytes,
-        "dedupe": n * K + nc * (K + 6),
-        "layers": nc * (K + 8) + nc * 8,
-        "dict": nc * 8,
-        "probe": nc * (K + 10) + issued * 32 + m * 8,
-        "edges": m * 8 * 2 * 8 + m * 16,
+        "dedupe": 0,
+        "layers": 0,
+        "dict": nc * K + dict_b,
+        "probe": nc * K + dict_b + m * 8 + tiles * 8,
+        "edges": m * 16,
     }
 
 
-STAGE_KERNEL = {"pack": "k_pack", "sort": "k_bucket_sort", "dedupe": "k_dedupe",
+STAGE_KERNEL = {"pack": "k_pack", "sort": "k_bucket_rank", "dedupe": "k_dedupe",
                 "dict": "k_global_index", "probe": "k_probe_global", "edges": "k_tile_copy",
                 "layers": "k_gather_rows"}
 
@@ -176,13 +197,18 @@ def run_ours(args):
     x, d = make_c5_device(torch, lg, dev)
     n, ell = x.shape
     stream = torch.cuda.current_stream(dev)
+    sampler = ClockSampler(dev.index or 0, period_ms=int(os.environ.get("CG_CLOCK_MS", "50")))
+    sampler.start()
+    time.sleep(0.5)  # let nvidia-smi initialise NVML before any timing
     # warm-up (also JIT-free: the kernels are precompiled sm_100a cubins)
+    # (same stream as the timed steps: the caching allocator keeps freed
+    # output blocks per stream, so a different warm-up stream would make the
+    # first timed step allocate)
     for _ in range(args.warmup):
-        r = cg.build(x, want_stats=True)
+        r = cg.build(x, stream=stream, want_stats=True)
         del r
     torch.cuda.synchronize(dev)
-    sampler = ClockSampler(dev.index or 0)
-    sampler.start()
+    sampler.mark()
     stats = []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -204,16 +230,27 @@ def run_ours(args):
     # recorded on the build stream)
     keys = ["us_pack", "us_sort", "us_dedupe", "us_layers", "us_dict", "us_probe", "us_edges"]
     stage_us = {k[3:]: float(np.mean([s[k] for s in stats])) for k in keys}
+    stage_us_max = {k[3:]: float(np.max([s[k] for s in stats])) for k in keys}
+    host_us = [round(s["us_host_total"], 1) for s in stats]
+    alloc_us = [round(s["us_host_alloc"], 1) for s in stats]
     ab = alg_bytes(st, n, ell)
     peak, peak_src = _peaks()
-    dom = max(stage_us, key=lambda k: stage_us[k])
+    stages = {}
+    for k, us in stage_us.items():
+        if ab.get(k) and us > 0:
+            gbs = ab[k] / (us * 1e-6) / 1e9
+            stages[k] = {"us": round(us, 1), "alg_bytes": int(ab[k]), "GBps": round(gbs, 1),
+                         "frac": round(gbs / peak, 4)}
+    # dominant KERNEL: the probe stage is one kernel (k_probe_global); the sort
+    # stage is several (2 one-sweep passes, bounds, bucket pass), each shorter
+    dom = max(("pack", "probe", "dict"), key=lambda k: stage_us[k])
     achieved = ab[dom] / (stage_us[dom] * 1e-6) / 1e9
     traffic, tsrc = _ncu_traffic(dom)
     roof = {"bound": "hbm", "kernel_stage": dom, "kernel": STAGE_KERNEL.get(dom),
             "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
             "traffic_source": tsrc, "alg_bytes_per_launch": int(ab[dom]),
-            "alg_bytes_def": "SURVEY 8.d.3 per-unit figures (DESIGN.md section 6)"}
+            "alg_bytes_def": "compulsory bytes, DESIGN.md section 6 (bench.alg_bytes)"}
     total_alg = sum(ab.values())
     whole = total_alg / (ms * 1e-3) / 1e9
     # ---- e2e through the host-buffer C-ABI entry
@@ -232,6 +269,10 @@ def run_ours(args):
         "issued_probes_per_s": round(st["issued_probes"] / (ms * 1e-3), 1),
         "issued_probes": st["issued_probes"],
         "stage_us": {k: round(v, 1) for k, v in stage_us.items()},
+        "stage_roofline": stages,
+        "stage_us_max": {k: round(v, 1) for k, v in stage_us_max.items()},
+        "host_us_per_step": host_us,
+        "host_alloc_us_per_step": alloc_us,
         "whole_path_alg_GBps": round(whole, 1),
         "whole_path_roofline_frac": round(whole / peak, 4),
         "roofline": roof,

@@ -86,6 +86,8 @@ typedef struct {
   int64_t n_allocs;        /* device allocations made for the call */
   double us_host_total;    /* host wall time of the whole call */
   double us_host_setup;    /* host wall time before the first stage event */
+  int64_t dict_bytes;      /* device bytes of the dictionary's index structures (prefix
+                              index T + filter F; the cell table itself not counted) */
 } cg_stats;
 
 enum {

@@ -49,7 +49,7 @@ class cg_stats(ctypes.Structure):
                [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int64), ("us_host_alloc", ctypes.c_double),
                 ("n_allocs", ctypes.c_int64), ("us_host_total", ctypes.c_double),
-                ("us_host_setup", ctypes.c_double)]
+                ("us_host_setup", ctypes.c_double), ("dict_bytes", ctypes.c_int64)]
 
 
 class cg_opts(ctypes.Structure):
@@ -114,8 +114,43 @@ def lib():
     L.cg_dist_finalize.argtypes = [P, ctypes.POINTER(i64), i32, i64, ctypes.POINTER(cg_opts),
                                    ctypes.POINTER(cg_edges)]
     L.cg_dist_finalize.restype = ctypes.c_int
+    _install_torch_allocator(L)
     _lib = L
     return L
+
+
+# Device memory for the library's outputs and scratch arena comes from
+# PyTorch's caching allocator (the cg_set_allocator hook): freed output
+# blocks are reused by the next build on the same stream without a driver
+# call, so steady-state builds never map memory.
+_ALLOC_T = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def _torch_alloc(size, stream, ctx):
+    try:
+        return torch._C._cuda_cudaCachingAllocator_raw_alloc(int(size), int(stream or 0))
+    except Exception:  # out of memory -> NULL -> CG_ENOMEM
+        return None
+
+
+def _torch_free(ptr, stream, ctx):
+    if ptr:
+        torch._C._cuda_cudaCachingAllocator_raw_delete(int(ptr))
+
+
+_ALLOC_CB = _ALLOC_T(_torch_alloc)
+_FREE_CB = _FREE_T(_torch_free)
+
+
+def _install_torch_allocator(L):
+    if os.environ.get("CG_NO_TORCH_ALLOC"):
+        return
+    L.cg_set_allocator.argtypes = [_ALLOC_T, _FREE_T, ctypes.c_void_p]
+    L.cg_set_allocator.restype = ctypes.c_int
+    rc = L.cg_set_allocator(_ALLOC_CB, _FREE_CB, None)
+    if rc != CG_OK:
+        raise CgError(rc, "cg_set_allocator failed")
 
 
 EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg_build_host",

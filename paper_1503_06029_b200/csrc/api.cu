@@ -71,14 +71,19 @@ static void store_counters(cg_stats* st) {
 
 struct AllocTimer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  size_t bytes = 0;
   ~AllocTimer() {
-    g_alloc_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    if (us > 500 && std::getenv("CG_TRACE"))
+      std::fprintf(stderr, "[cg] slow device allocation: %zu bytes, %.0f us\n", bytes, us);
+    g_alloc_us += us;
     ++g_nallocs;
   }
 };
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   AllocTimer at;
+  at.bytes = bytes;
   void* p = nullptr;
   if (g_alloc) {
     p = g_alloc(bytes, reinterpret_cast<cg_stream_t>(s), g_alloc_ctx);
@@ -130,6 +135,8 @@ WsScope::WsScope() {
   Arena& a = cur_arena();
   if (a.depth++ > 0) return;
   if (a.want > a.cap) {
+    if (std::getenv("CG_TRACE"))
+      std::fprintf(stderr, "[cg] arena %zu -> %zu bytes\n", a.cap, a.want);
     if (a.base) {
       cudaDeviceSynchronize();
       if (g_dealloc) g_dealloc(a.base, nullptr, g_alloc_ctx);
@@ -428,6 +435,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
     DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
     CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
+    const int64_t dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
     build_global_index(cellbuf.p, nc, W, b, fextra, T.p, F.p, s);
     tm.mark();  // 5: dict
     GlobalDict g{cellbuf.p, lcp.p, T.p, F.p, b, fextra, W, ell, nc};
@@ -532,6 +540,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       st->issued_probes = int64_t(issued);
       st->sort_passes = sst.passes;
       st->probe_reruns = reruns + int(novf);
+      st->dict_bytes = dict_bytes;
     }
     return;
   }

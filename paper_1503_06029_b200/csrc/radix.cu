@@ -698,8 +698,15 @@ __global__ void __launch_bounds__(kBktThreads)
       continue;
     }
     // ---- 1. bits that vary inside the bucket
+    // the thread's keys (positions c * 256 + tid) stay in registers
+    K kr[MAXC];
     uint64_t av[2] = {~0ull, ~0ull}, ov[2] = {0ull, 0ull};
-    for (int i = tid; i < S; i += kBktThreads) key_andor(s[i], av, ov);
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = c * kBktThreads + tid;
+      kr[c] = s[i < S ? i : 0];
+      key_andor(kr[c], av, ov);
+    }
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
 #pragma unroll
@@ -753,7 +760,7 @@ __global__ void __launch_bounds__(kBktThreads)
       dg[c] = 0;
       rk[c] = 0;
       if (i < S) {
-        dg[c] = uint32_t(key_bits_at(s[i], f) >> (64 - kRankBits));
+        dg[c] = uint32_t(key_bits_at(kr[c], f) >> (64 - kRankBits));
         rk[c] = atomicAdd(&h[dg[c]], 1u);
       }
     }
@@ -786,23 +793,37 @@ __global__ void __launch_bounds__(kBktThreads)
       if (i < S) nxt[h[dg[c]] + rk[c]] = uint16_t(i);
     }
     __syncthreads();
+    // digits of <= 2 keys (all but a few): one compare with the partner,
+    // branch-free so the chains of the thread's keys overlap
+    uint32_t bs[MAXC], ct[MAXC];
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
-      if (i < S) {
-        const uint32_t base = h[dg[c]], cnt = h[dg[c] + 1] - base;
-        uint32_t r = 0;
-        if (cnt == 2) {  // the common tie (e.g. a planted Hamming-1 partner)
-          const int j = nxt[base + (rk[c] ^ 1u)];
-          r = key_before(s[j], j, s[i], i);
-        } else if (cnt > 2) {
-          const K ki = s[i];
-          for (uint32_t m = 0; m < cnt; ++m) {
-            const int j = nxt[base + m];
-            r += (j != i) && key_before(s[j], j, ki, i);
+      bs[c] = h[dg[c]];
+      ct[c] = i < S ? h[dg[c] + 1] - bs[c] : 0u;
+    }
+    bool many = false;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = c * kBktThreads + tid;
+      const uint32_t pq = min(bs[c] + (rk[c] ^ 1u), uint32_t(CAP - 1));
+      const int j = nxt[pq];
+      const uint32_t r = ct[c] == 2u ? key_before(s[j], j, kr[c], i) : 0u;
+      if (ct[c] != 0u && ct[c] <= 2u) fin[bs[c] + r] = uint16_t(i);
+      many |= ct[c] > 2u;
+    }
+    if (many) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        if (ct[c] > 2u) {
+          const int i = c * kBktThreads + tid;
+          uint32_t r = 0;
+          for (uint32_t m = 0; m < ct[c]; ++m) {
+            const int j = nxt[bs[c] + m];
+            r += (j != i) && key_before(s[j], j, kr[c], i);
           }
+          fin[bs[c] + r] = uint16_t(i);
         }
-        fin[base + r] = uint16_t(i);
       }
     }
     __syncthreads();
