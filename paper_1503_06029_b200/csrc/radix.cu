@@ -650,17 +650,28 @@ __device__ __forceinline__ uint32_t key_before(const ulonglong2& a, int ia, cons
   return uint32_t(a.x < b.x) | (ex & uint32_t(a.y < b.y)) | (ex & uint32_t(a.y == b.y) & uint32_t(ia < ib));
 }
 
-template <class K, int MAXC>
-__global__ void __launch_bounds__(kBktThreads)
+template <class K, int MAXC, bool PREF>
+__global__ void __launch_bounds__(kBktThreads, PREF ? 3 : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
                   uint32_t* __restrict__ nlist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // PREF: the next bucket is prefetched (cp.async) into a second buffer;
+  // otherwise one buffer and more resident CTAs hide the load latency
   K* buf0 = reinterpret_cast<K*>(smem_raw);
-  K* buf1 = buf0 + CAP;
+  K* buf1 = PREF ? buf0 + CAP : buf0;
   uint16_t* nxt = reinterpret_cast<uint16_t*>(buf1 + CAP);
-  uint16_t* fin = nxt + CAP;
+  uint16_t* pos_of = nxt + CAP;
+  uint32_t* mlist = reinterpret_cast<uint32_t*>(pos_of + CAP);  // keys of digits holding > 2
+  const uint32_t mcap = PREF ? uint32_t(CAP) : uint32_t(CAP / 2);
   constexpr int kBins = 1 << kRankBits, kPer = kBins / kBktThreads;
+  // histogram slot of digit d: thread t owns digits kPer*t .. kPer*t+kPer-1
+  // for the scan; storing digit d at (d % kPer) * 256 + d / kPer makes those
+  // accesses conflict-free (one row per q, consecutive threads, banks)
+  auto hx = [](uint32_t d) -> uint32_t {
+    return d >= uint32_t(kBins) ? uint32_t(kBins) : (d % kPer) * kBktThreads + d / kPer;
+  };
+  __shared__ uint32_t s_nmany;
   __shared__ uint32_t h[kBins + 1];
   __shared__ uint32_t s_scan[33];
   __shared__ uint64_t s_red[2][kBktWarps][2];
@@ -670,7 +681,7 @@ __global__ void __launch_bounds__(kBktThreads)
   const uint32_t lt = lanemask_lt();
 
   auto prefetch = [&](int64_t bk, K* dst) {
-    if (bk < nbuckets) {
+    if (PREF && bk < nbuckets) {
       const uint32_t lo = off[bk];
       const int S = int(off[bk + 1] - lo);
       if (S <= CAP)
@@ -701,10 +712,18 @@ __global__ void __launch_bounds__(kBktThreads)
     // the thread's keys (positions c * 256 + tid) stay in registers
     K kr[MAXC];
     uint64_t av[2] = {~0ull, ~0ull}, ov[2] = {0ull, 0ull};
+    if (!PREF) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = c * kBktThreads + tid;
+        kr[c] = keys[lo + (i < S ? i : 0)];
+        if (i < S) s[i] = kr[c];
+      }
+    }
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
-      kr[c] = s[i < S ? i : 0];
+      if (PREF) kr[c] = s[i < S ? i : 0];
       key_andor(kr[c], av, ov);
     }
 #pragma unroll
@@ -723,7 +742,8 @@ __global__ void __launch_bounds__(kBktThreads)
       }
     }
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) h[tid * kPer + q] = 0u;
+    for (int q = 0; q < kPer; ++q) h[q * kBktThreads + tid] = 0u;
+    if (tid == 0) s_nmany = 0u;
     __syncthreads();
     uint64_t dif[2] = {0ull, 0ull};
 #pragma unroll
@@ -761,7 +781,7 @@ __global__ void __launch_bounds__(kBktThreads)
       rk[c] = 0;
       if (i < S) {
         dg[c] = uint32_t(key_bits_at(kr[c], f) >> (64 - kRankBits));
-        rk[c] = atomicAdd(&h[dg[c]], 1u);
+        rk[c] = atomicAdd(&h[hx(dg[c])], 1u);
       }
     }
     __syncthreads();
@@ -769,7 +789,7 @@ __global__ void __launch_bounds__(kBktThreads)
     int too_long = 0;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      cl[q] = h[tid * kPer + q];
+      cl[q] = h[q * kBktThreads + tid];
       loc += cl[q];
       too_long |= cl[q] > uint32_t(kRankRun);
     }
@@ -777,7 +797,7 @@ __global__ void __launch_bounds__(kBktThreads)
     uint32_t run = block_excl_scan(loc, s_scan, &all);
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      h[tid * kPer + q] = run;
+      h[q * kBktThreads + tid] = run;
       run += cl[q];
     }
     if (tid == 0) h[kBins] = uint32_t(S);
@@ -790,7 +810,7 @@ __global__ void __launch_bounds__(kBktThreads)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
-      if (i < S) nxt[h[dg[c]] + rk[c]] = uint16_t(i);
+      if (i < S) nxt[h[hx(dg[c])] + rk[c]] = uint16_t(i);
     }
     __syncthreads();
     // digits of <= 2 keys (all but a few): one compare with the partner,
@@ -799,43 +819,67 @@ __global__ void __launch_bounds__(kBktThreads)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
-      bs[c] = h[dg[c]];
-      ct[c] = i < S ? h[dg[c] + 1] - bs[c] : 0u;
+      bs[c] = h[hx(dg[c])];
+      ct[c] = i < S ? h[hx(dg[c] + 1)] - bs[c] : 0u;
     }
-    bool many = false;
+    // keys of longer digits are listed and ranked afterwards by all threads
+    // together (one list entry per thread: no lanes idle behind a long loop);
+    // their positions come back through pos_of[]
+    uint32_t ps[MAXC];
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
       const uint32_t pq = min(bs[c] + (rk[c] ^ 1u), uint32_t(CAP - 1));
       const int j = nxt[pq];
-      const uint32_t r = ct[c] == 2u ? key_before(s[j], j, kr[c], i) : 0u;
-      if (ct[c] != 0u && ct[c] <= 2u) fin[bs[c] + r] = uint16_t(i);
-      many |= ct[c] > 2u;
-    }
-    if (many) {
-#pragma unroll
-      for (int c = 0; c < MAXC; ++c) {
-        if (ct[c] > 2u) {
-          const int i = c * kBktThreads + tid;
-          uint32_t r = 0;
-          for (uint32_t m = 0; m < ct[c]; ++m) {
-            const int j = nxt[bs[c] + m];
-            r += (j != i) && key_before(s[j], j, kr[c], i);
-          }
-          fin[bs[c] + r] = uint16_t(i);
-        }
+      ps[c] = bs[c] + (ct[c] == 2u ? key_before(s[j], j, kr[c], i) : 0u);
+      if (ct[c] > 2u) {
+        const uint32_t q = atomicAdd(&s_nmany, 1u);
+        if (q < mcap) mlist[q] = uint32_t(i) | (dg[c] << 16);
       }
     }
     __syncthreads();
-    // ---- 4. write (deduplicated and compacted when ucnt is given)
+    const uint32_t nmany = s_nmany;
+    if (nmany > mcap) {  // (skewed digits) the byte-pass kernel takes the bucket
+      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
+      __syncthreads();
+      continue;
+    }
+    if (nmany) {
+      for (uint32_t q = tid; q < nmany; q += kBktThreads) {
+        const uint32_t e = mlist[q];
+        const int i = int(e & 0xffffu);
+        const uint32_t d = e >> 16, b0 = h[hx(d)], cn = h[hx(d + 1)] - b0;
+        const K ki = s[i];
+        uint32_t r = 0;
+        for (uint32_t m = 0; m < cn; ++m) {
+          const int j = nxt[b0 + m];
+          r += (j != i) && key_before(s[j], j, ki, i);
+        }
+        pos_of[i] = uint16_t(b0 + r);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+        if (ct[c] > 2u) ps[c] = pos_of[c * kBktThreads + tid];
+    }
+    // ---- permute in place: every key is in a register, so after the
+    // barrier each thread stores its keys at their sorted positions
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (ct[c] != 0u) s[ps[c]] = kr[c];
+    __syncthreads();
+    // ---- 4. write (deduplicated and compacted when ucnt is given); the
+    // sorted keys are read contiguously
     if (!ucnt) {
-      for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[fin[i]];
+      for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[i];
     } else {
       uint32_t bl[MAXC];
+      K sv[MAXC];
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
-        const bool fl = i < S && (i == 0 || !key_eq(s[fin[i - 1]], s[fin[i]]));
+        sv[c] = s[i < S ? i : 0];
+        const bool fl = i < S && (i == 0 || !key_eq(s[i - 1], sv[c]));
         bl[c] = __ballot_sync(kFull, fl);
         if (lane == 0) s_wc[c * kBktWarps + wid] = __popc(bl[c]);
       }
@@ -866,10 +910,8 @@ __global__ void __launch_bounds__(kBktThreads)
       __syncthreads();
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
-        if ((bl[c] >> lane) & 1u) {
-          const int i = c * kBktThreads + tid;
-          keys[lo + s_wc[c * kBktWarps + wid] + __popc(bl[c] & lt)] = s[fin[i]];
-        }
+        if ((bl[c] >> lane) & 1u)
+          keys[lo + s_wc[c * kBktWarps + wid] + __popc(bl[c] & lt)] = sv[c];
       }
     }
     __syncthreads();
@@ -894,18 +936,24 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
   DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
   CG_CUDA(cudaMemsetAsync(nlist.p, 0, sizeof(uint32_t), s));
   {
-    // rank pass: double-buffered keys + two u16 orders; 1.5x the mean bucket
-    // (3 CTAs per SM at 16-byte keys); larger buckets go to the byte passes
+    // rank pass: keys (double-buffered with PREF) + two u16 orders + the
+    // long-digit list; 1.5x the mean bucket; larger buckets go to the byte passes
     const int rcap = avg <= 1024 ? 1536 : 2048;
-    const size_t smem = size_t(rcap) * (2 * sizeof(K) + 4);
-    const int per_sm = std::max(1, int((224 << 10) / (smem + 10 * 1024)));
+    static const bool pref = !(std::getenv("CG_RANK_PREF") && std::atoi(std::getenv("CG_RANK_PREF")) == 0);
+    const size_t smem = pref ? size_t(rcap) * (2 * sizeof(K) + 8) : size_t(rcap) * (sizeof(K) + 6);
+    const int per_sm = std::max(1, int((222 << 10) / (smem + 10 * 1024)));
     const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
+    auto go = [&](auto kern) {
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+    };
     if (rcap == 1536) {
-      CG_CUDA(cudaFuncSetAttribute(k_bucket_rank<K, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      k_bucket_rank<K, 6><<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+      if (pref) go(k_bucket_rank<K, 6, true>);
+      else go(k_bucket_rank<K, 6, false>);
     } else {
-      CG_CUDA(cudaFuncSetAttribute(k_bucket_rank<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      k_bucket_rank<K, 8><<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+      if (pref) go(k_bucket_rank<K, 8, true>);
+      else go(k_bucket_rank<K, 8, false>);
     }
     CG_LAUNCH_CHECK();
   }
