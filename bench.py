@@ -188,9 +188,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus > 1 or world > 1 or args.dist:
-        from paper_1503_06029_b200 import dist as cgdist
-
-        return cgdist.bench_main(args, METRIC)
+        return run_dist(args)
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     lg = args.scale_log2
@@ -213,6 +211,7 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
+    l0 = cg.kernel_launches()
     ev0.record(stream)
     for _ in range(args.steps):
         r = cg.build(x, stream=stream, want_stats=True)
@@ -220,6 +219,7 @@ def run_ours(args):
         del r
     ev1.record(stream)
     torch.cuda.synchronize(dev)
+    launches = cg.kernel_launches() - l0
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     st = stats[-1]
@@ -276,12 +276,144 @@ def run_ours(args):
         "whole_path_alg_GBps": round(whole, 1),
         "whole_path_roofline_frac": round(whole / peak, 4),
         "roofline": roof,
-        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
     print(json.dumps(out))
+
+
+def run_dist(args):
+    """N ranks under torchrun (one GPU each): CFG5 split n/N rows per rank,
+    the distributed phases of DESIGN.md section 8 (NCCL all-gather of the
+    sorted runs, contiguous canonical probe ranges, edge all-gather).  Strong
+    scaling; device time per step = max over ranks of CUDA-event time."""
+    import torch
+    import torch.distributed as tdist
+
+    import synth
+    from paper_1503_06029_b200 import cg
+    from paper_1503_06029_b200 import dist as cgdist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if not tdist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        tdist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    lg = args.scale_log2
+    d = synth.config("C5", scale_log2=lg)
+    n, ell = d["n"], d["ell"]
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    wt = torch.from_numpy(np.ascontiguousarray(d["words"][lo:hi]).view(np.int64)).to(dev)
+    x = synth.unpack_words_torch(wt, ell)
+    del wt, d
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    ops = cgdist.CudaOps(stream, want_stats=True)
+    sampler = ClockSampler(dev.index or 0) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.5)
+    for _ in range(args.warmup):
+        cgdist.build_distributed(x, ell, ops=ops)
+    torch.cuda.synchronize(dev)
+    tdist.barrier()
+    if sampler:
+        sampler.mark()
+    l0 = cg.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        table, edges = cgdist.build_distributed(x, ell, ops=ops)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    tdist.barrier()
+    launches = cg.kernel_launches() - l0
+    clocks = sampler.stop() if sampler else None
+    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = float(ms.item())
+    lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+    tdist.all_reduce(lt)
+    nc, m = int(table.shape[0]), int(edges.shape[0])
+    st = dict(ops.last_stats)
+    # the rank's probe stage (its contiguous canonical range) as the dominant kernel
+    peak, peak_src = _peaks()
+    roof = None
+    if st.get("us_probe"):
+        nr = (nc + world - 1) // world
+        ab = alg_bytes(dict(st, n_cells=nr, dict_bytes=st.get("dict_bytes", 0) // world), n, ell)
+        a = ab["probe"] / (st["us_probe"] * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel_stage": "probe", "kernel": "k_probe_global",
+                "achieved": round(a, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": round(a / peak, 4), "traffic": None,
+                "alg_bytes_per_launch": int(ab["probe"]),
+                "alg_bytes_def": "compulsory bytes of rank 0's probe range (bench.alg_bytes)"}
+    e2e = run_dist_e2e(torch, tdist, cgdist, x, ell, ops, stream, dev, args, rank, world, nc)
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(nc / (ms * 1e-3), 1), "unit": "cells/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+               "config": {"workload": "C5" if lg == 26 else f"C5@2^{lg}", "n": n, "ell": ell,
+                          "n_cells": nc, "n_edges": m,
+                          "l2": "inputs larger than L2 (8.6 GB / N per rank), no flush",
+                          "parallelism": f"rows/{world} + NCCL all-gather of sorted runs + "
+                          "contiguous canonical probe ranges + NCCL edge all-gather"},
+               "flip_probes_per_s": round(nc * ell / (ms * 1e-3), 1),
+               "rank0_stage_us": {k[3:]: round(v, 1) for k, v in st.items()
+                                  if k.startswith("us_") and not k.startswith("us_host")},
+               "roofline": roof, "gpu_launches": int(lt.item()), "clocks": clocks,
+               "e2e": e2e, "cpu_baseline": None}
+        print(json.dumps(out))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def run_dist_e2e(torch, tdist, cgdist, x, ell, ops, stream, dev, args, rank, world, nc):
+    """e2e at N > 1: every step copies each rank's shard from pinned host
+    memory to its GPU, runs the distributed build and copies the result (cell
+    table + edge list) back to rank 0's host; max over ranks."""
+    if args.e2e_steps <= 0:
+        return None
+    xh = torch.empty(x.shape, dtype=torch.uint8, pin_memory=True)
+    xh.copy_(x)
+    torch.cuda.synchronize(dev)
+    tdist.barrier()
+    # pinned result buffers sized by one untimed build (allocation is not
+    # part of the measured work)
+    table, edges = cgdist.build_distributed(xh.to(dev), ell, ops=ops)
+    th = torch.empty(table.shape, dtype=table.dtype, pin_memory=True) if rank == 0 else None
+    eh = torch.empty(edges.shape, dtype=edges.dtype, pin_memory=True) if rank == 0 else None
+    del table, edges
+    torch.cuda.synchronize(dev)
+    tdist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d2h = 0
+    ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        xd = xh.to(dev, non_blocking=True)
+        table, edges = cgdist.build_distributed(xd, ell, ops=ops)
+        if rank == 0:
+            th.copy_(table, non_blocking=True)
+            eh.copy_(edges, non_blocking=True)
+            d2h = th.numel() * th.element_size() + eh.numel() * eh.element_size()
+        del xd
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([ev0.elapsed_time(ev1) / args.e2e_steps], device=dev)
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = float(ms.item())
+    h2d = torch.tensor([x.numel()], device=dev, dtype=torch.int64)
+    tdist.all_reduce(h2d)
+    return {"value": round(nc / (ms * 1e-3), 1), "unit": "cells/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": int(d2h),
+            "steps": args.e2e_steps, "api": "dist.build_distributed (pinned host shards)"}
 
 
 def run_e2e(torch, cg, x, args, dev):

@@ -168,6 +168,9 @@ void cg_index_free(cg_index* idx);
 const char* cg_strerror(int code);
 const char* cg_last_error(void); /* thread-local detail of the last failure */
 int cg_version(void);            /* (major << 16) | minor */
+/* CUDA kernels this library has launched in the process so far (all calls,
+ * all threads); the difference across a region counts its launches. */
+int64_t cg_kernel_launches(void);
 
 /* ---- distributed phases (one process per GPU; the caller runs the NCCL
  * collectives between them) ----------------- */

@@ -105,6 +105,8 @@ def lib():
     L.cg_last_error.restype = ctypes.c_char_p
     L.cg_version.argtypes = []
     L.cg_version.restype = ctypes.c_int
+    L.cg_kernel_launches.argtypes = []
+    L.cg_kernel_launches.restype = ctypes.c_int64
     L.cg_dist_local.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells)]
     L.cg_dist_local.restype = ctypes.c_int
     L.cg_dist_merge_probe.argtypes = [P, ctypes.POINTER(i64), i32, i64, i32, i32,
@@ -156,6 +158,7 @@ def _install_torch_allocator(L):
 EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg_build_host",
             "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
+            "cg_kernel_launches",
             "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
 
 
@@ -444,3 +447,8 @@ def dist_finalize(gathered: torch.Tensor, counts, *, stream=None,
         _check(lib().cg_dist_finalize(ctypes.c_void_p(gathered.data_ptr()), cnt, G, stride,
                                       ctypes.byref(o), ctypes.byref(e)))
     return _wrap_edges(e, gathered.device)
+
+
+def kernel_launches() -> int:
+    """Kernels the library has launched in this process (cg_kernel_launches)."""
+    return int(lib().cg_kernel_launches())

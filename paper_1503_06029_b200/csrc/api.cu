@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,7 +38,11 @@ namespace cgk {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
 static thread_local int64_t g_launches = 0;
-void note_launch() { ++g_launches; }
+static std::atomic<int64_t> g_launches_total{0};  // process lifetime, all threads
+void note_launch() {
+  ++g_launches;
+  g_launches_total.fetch_add(1, std::memory_order_relaxed);
+}
 
 // ---------------------------------------------------------------- allocator
 static void* (*g_alloc)(size_t, cg_stream_t, void*) = nullptr;
@@ -1021,6 +1026,8 @@ const char* cg_strerror(int code) {
 }
 
 const char* cg_last_error(void) { return g_last_error.c_str(); }
+
+int64_t cg_kernel_launches(void) { return g_launches_total.load(std::memory_order_relaxed); }
 
 int cg_version(void) { return (0 << 16) | 1; }
 

@@ -14,8 +14,6 @@ product ops (``CudaOps``) call the C ABI.  DESIGN.md section 8.
 """
 from __future__ import annotations
 
-import json
-import os
 import time
 
 import torch
@@ -25,8 +23,10 @@ import torch.distributed as dist
 class CudaOps:
     """The C-ABI phases (device tensors)."""
 
-    def __init__(self, stream=None):
+    def __init__(self, stream=None, want_stats=False):
         self.stream = stream
+        self.want_stats = want_stats
+        self.last_stats = {}
 
     def local(self, vecs):
         from . import cg
@@ -36,7 +36,9 @@ class CudaOps:
     def merge_probe(self, runs, counts, rank, ell):
         from . import cg
 
-        table, edges, _ = cg.dist_merge_probe(runs, counts, rank, ell, stream=self.stream)
+        table, edges, st = cg.dist_merge_probe(runs, counts, rank, ell, stream=self.stream,
+                                               want_stats=self.want_stats)
+        self.last_stats = st
         return table, edges
 
     def finalize(self, gathered, counts):
@@ -92,59 +94,3 @@ def build_distributed(vecs_local: torch.Tensor, ell: int | None = None, group=No
     if timings is not None:
         timings.update(t)
     return table, edges
-
-
-# ---------------------------------------------------------------- bench (N > 1)
-def bench_main(args, metric: str):
-    """bench.py --gpus N under torchrun: CFG5 (2^26 x 128) split over N ranks,
-    strong scaling; device time per step = max over ranks (CUDA events)."""
-    import numpy as np
-
-    import synth
-
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device(f"cuda:{local}")
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev)
-    lg = args.scale_log2
-    d = synth.config("C5", scale_log2=lg)
-    n = d["n"]
-    lo, hi = n * rank // world, n * (rank + 1) // world
-    wt = torch.from_numpy(np.ascontiguousarray(d["words"][lo:hi]).view(np.int64)).to(dev)
-    x = synth.unpack_words_torch(wt, d["ell"])
-    del wt, d
-    torch.cuda.synchronize(dev)
-    stream = torch.cuda.current_stream(dev)
-    ops = CudaOps(stream)
-    for _ in range(args.warmup):
-        build_distributed(x, 128, ops=ops)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        table, edges = build_distributed(x, 128, ops=ops)
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    nc, m = int(table.shape[0]), int(edges.shape[0])
-    if rank == 0:
-        out = {"metric": metric, "value": round(nc / (ms * 1e-3), 1), "unit": "cells/s",
-               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-               "config": {"workload": "C5" if lg == 26 else f"C5@2^{lg}", "n": n, "ell": 128,
-                          "n_cells": nc, "n_edges": m, "parallelism": f"rows/{world} + "
-                          "NCCL all-gather of sorted runs + popcount-layer query shards + "
-                          "edge all-gather"},
-               "flip_probes_per_s": round(nc * 128 / (ms * 1e-3), 1),
-               "gpu_launches": None, "roofline": None, "e2e": None, "cpu_baseline": None}
-        print(json.dumps(out))
-    dist.barrier()
-    dist.destroy_process_group()

@@ -1,4 +1,3 @@
-set -x
-mkdir -p gpurun_out
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 1 --dist --steps 5 --warmup 3 > gpurun_out/bench_dist1.json 2> gpurun_out/bench_dist1.err; tail -5 gpurun_out/bench_dist1.err
-cat gpurun_out/bench_dist1.json
+python -c "from paper_1503_06029_b200 import build_lib; build_lib.build()"
+timeout 600 python bench.py --dist --steps 5 --warmup 3 --e2e-steps 2 2>&1 | tail -3 | cut -c1-2500
+timeout 600 python bench.py --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.load(sys.stdin); print(d['ms_per_step'], d['gpu_launches'], d['roofline']['frac'])"
