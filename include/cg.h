@@ -130,6 +130,28 @@ int cg_build_ex(const uint8_t* vecs, int64_t n, int32_t ell, const cg_opts* o, c
 int cg_build_packed_ex(const uint64_t* words, int64_t n, int32_t ell, const cg_opts* o,
                        cg_cells* cells, cg_edges* edges);
 
+/* ---- f1: cell signatures computed on the device ----
+ * "the i-th bit of v_P is 1 iff P satisfies the inequality c_i" for
+ * sampled points P.  Constraint c_k is the half-space
+ * a_k . p + b_k >= 0 in R^dim (a tie counts as satisfied, DESIGN G12).
+ *   points = f64[n][dim] (device, row-major), dim in [1, 16];
+ *   planes = f64[ell][dim + 1] (device), row k = (a_k0 .. a_k(dim-1), b_k).
+ * The value is evaluated in one fixed IEEE-754 order, v = b_k;
+ * v = fma(a_kt, p_t, v) for t = 0 .. dim-1 (round to nearest, DESIGN G21),
+ * so results are bit-reproducible on any IEEE machine.  Inputs are borrowed.
+ * Errors: CG_EINVAL (NULL/host pointers, n < 1, ell or dim out of range),
+ * CG_EINPUT (a value is NaN or infinite). */
+
+/* Signatures only: words = u64[n][ceil(ell/64)] (device, caller-allocated),
+ * the packed format of cg_cells.  Blocks until done (the error flag). */
+int cg_signatures(const double* points, int64_t n, int32_t dim, const double* planes,
+                  int32_t ell, uint64_t* words, cg_stream_t stream);
+
+/* As cg_build_ex, with the signatures computed on the device and packed in
+ * the same kernel (the n*ell-byte signature matrix is never formed). */
+int cg_build_points(const double* points, int64_t n, int32_t dim, const double* planes,
+                    int32_t ell, const cg_opts* o, cg_cells* cells, cg_edges* edges);
+
 /* End-to-end entry with HOST buffers.  h_vecs = uint8[n][ell] in host memory
  * (pinned for full PCIe speed, pageable accepted).  The library copies it to
  * the device (chunked, overlapped with the pack kernel), builds, and copies

@@ -14,6 +14,7 @@ build(bytes_u8[n, ell])          ORACLE-A: std::set + single-bit-flip lookup (P:
 build_packed(words_u64[n, W], ell)
 brute(bytes_u8[n, ell])          ORACLE-B: sort/unique + all-pairs distance
 query(cells_u64[nc, W], ell, q_u64[nq, W])  self / neighbour indices
+signatures(points_f64[n, dim], planes_f64[ell, dim+1])  f1: bytes u8[n, ell]
 All return ``(rc, cells u64[nc, W], edges u32[m, 2])`` (query: ``(rc, self, nbr)``).
 """
 from __future__ import annotations
@@ -58,6 +59,8 @@ def _load():
         lib.oracle_build_packed.argtypes = [P, i64, i32, i32, pp, pi64, pp, pi64, pd]
         lib.oracle_brute.argtypes = [P, i64, i32, i32, pp, pi64, pp, pi64]
         lib.oracle_query.argtypes = [P, i64, i32, P, i64, P, P]
+        lib.oracle_signatures.argtypes = [P, i64, i32, P, i32, P]
+        lib.oracle_signatures.restype = ctypes.c_int
         lib.oracle_free.argtypes = [P]
         for f in (lib.oracle_build, lib.oracle_build_packed, lib.oracle_brute, lib.oracle_query):
             f.restype = ctypes.c_int
@@ -174,3 +177,17 @@ def timed_build(x: np.ndarray, nthreads: int | None = None):
     if rc != OK:
         raise RuntimeError(f"oracle_build failed rc={rc}")
     return cells, edges, dt, tm
+
+
+def signatures(points: np.ndarray, planes: np.ndarray):
+    """f1 cell signatures: ``(rc, bytes u8[n, ell])``; bit k of point r
+    is [fma-chain value of a_k . p_r + b_k >= 0] (DESIGN G12, G21)."""
+    lib = _load()
+    P = np.ascontiguousarray(points, dtype=np.float64)
+    A = np.ascontiguousarray(planes, dtype=np.float64)
+    n, dim = P.shape
+    ell = A.shape[0]
+    assert A.shape[1] == dim + 1
+    out = np.zeros((n, ell), dtype=np.uint8)
+    rc = lib.oracle_signatures(P.ctypes.data, n, dim, A.ctypes.data, ell, out.ctypes.data)
+    return rc, out

@@ -22,6 +22,11 @@
  *   ORACLE-B  oracle_brute : unpacked byte vectors, std::sort + std::unique,
  *             then all-pairs Hamming distance (the naive method).
  *   plus      oracle_query : self/neighbour lookup of query vectors.
+ *   and       oracle_signatures : the cell signature of sampled points (the
+ *             f1 row): bit k of point P is 1 iff P satisfies constraint c_k
+ *             (P:92), c_k being the half-space a_k . p + b_k >= 0 (a tie is
+ *             satisfied, DESIGN G12), evaluated as v = b_k, then
+ *             v = fma(a_kt, p_t, v) for t = 0..dim-1 (DESIGN G21).
  *
  * Output word format of oracle_build / oracle_brute (the C-ABI's format):
  *   W = ceil(ell/64) little-endian u64 words per cell; bit k of the vector is
@@ -35,6 +40,7 @@
  */
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -348,6 +354,28 @@ int oracle_query(const uint64_t* cells, int64_t nc, int32_t ell, const uint64_t*
     }
   }
   return kOK;
+}
+
+// f1: signatures of n points (row-major f64[n][dim]) against ell half-spaces
+// (f64[ell][dim+1], row k = a_k0 .. a_k(dim-1), b_k) as bytes u8[n][ell]
+// (the oracle's vector input form).  Returns 0, or -1 (bad sizes or
+// NULL), -2 (a non-finite constraint value).
+int oracle_signatures(const double* points, int64_t n, int32_t dim, const double* planes,
+                      int32_t ell, uint8_t* out) {
+  if (!points || !planes || !out || n < 1 || dim < 1 || dim > 16 || ell < 1 || ell > kMaxEll)
+    return kEINVAL;
+  int rc = kOK;
+  for (int64_t r = 0; r < n; ++r) {
+    const double* p = points + r * dim;
+    for (int k = 0; k < ell; ++k) {
+      const double* a = planes + int64_t(k) * (dim + 1);
+      double v = a[dim];
+      for (int t = 0; t < dim; ++t) v = std::fma(a[t], p[t], v);
+      if (!std::isfinite(v)) rc = kEINPUT;
+      out[r * ell + k] = v >= 0.0 ? 1 : 0;
+    }
+  }
+  return rc;
 }
 
 void oracle_free(void* p) { std::free(p); }

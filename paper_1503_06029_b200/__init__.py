@@ -5,9 +5,10 @@ hand-written sm_100a CUDA behind the C ABI of include/cg.h.
 
     from paper_1503_06029_b200 import build
     res = build(vecs_uint8_cuda)      # res.cells int64 [nc, W], res.edges int32 [m, 2]
+    res = build_points(points_f64_cuda, planes_f64_cuda)   # signatures on the device (f1)
 """
-from .cg import (BuildResult, CgError, Index, build, build_host, build_packed, lib,  # noqa: F401
-                 version)
+from .cg import (BuildResult, CgError, Index, build, build_host, build_packed,  # noqa: F401
+                 build_points, lib, signatures, version)
 
-__all__ = ["build", "build_packed", "build_host", "BuildResult", "Index", "CgError", "lib",
-           "version"]
+__all__ = ["build", "build_packed", "build_host", "build_points", "signatures", "BuildResult",
+           "Index", "CgError", "lib", "version"]

@@ -107,6 +107,11 @@ def lib():
     L.cg_version.restype = ctypes.c_int
     L.cg_kernel_launches.argtypes = []
     L.cg_kernel_launches.restype = ctypes.c_int64
+    L.cg_signatures.argtypes = [P, i64, i32, P, i32, P, P]
+    L.cg_signatures.restype = ctypes.c_int
+    L.cg_build_points.argtypes = [P, i64, i32, P, i32, ctypes.POINTER(cg_opts),
+                                  ctypes.POINTER(cg_cells), ctypes.POINTER(cg_edges)]
+    L.cg_build_points.restype = ctypes.c_int
     L.cg_dist_local.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells)]
     L.cg_dist_local.restype = ctypes.c_int
     L.cg_dist_merge_probe.argtypes = [P, ctypes.POINTER(i64), i32, i64, i32, i32,
@@ -158,7 +163,7 @@ def _install_torch_allocator(L):
 EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg_build_host",
             "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
-            "cg_kernel_launches",
+            "cg_kernel_launches", "cg_signatures", "cg_build_points",
             "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
 
 
@@ -323,6 +328,57 @@ def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="globa
         res.stats = _stats_dict(st)
     if want_index and ih.value:
         res.index = Index(ih.value, words.device)
+    return res
+
+
+def _check_points(points: torch.Tensor, planes: torch.Tensor):
+    if (not isinstance(points, torch.Tensor) or points.dim() != 2 or points.dtype != torch.float64
+            or not points.is_cuda):
+        raise CgError(CG_EINVAL, "points must be a CUDA float64 tensor [n, dim]")
+    if (not isinstance(planes, torch.Tensor) or planes.dim() != 2 or planes.dtype != torch.float64
+            or not planes.is_cuda or planes.shape[1] != points.shape[1] + 1):
+        raise CgError(CG_EINVAL, "planes must be a CUDA float64 tensor [ell, dim + 1]")
+    return points.contiguous(), planes.contiguous()
+
+
+def signatures(points: torch.Tensor, planes: torch.Tensor, *, stream=None) -> torch.Tensor:
+    """cg_signatures (f1): packed cell signatures int64 [n, ceil(ell/64)] of
+    points f64 [n, dim] against half-spaces planes f64 [ell, dim + 1]."""
+    points, planes = _check_points(points, planes)
+    n, dim = points.shape
+    ell = planes.shape[0]
+    words = torch.empty((n, (ell + 63) // 64), dtype=torch.int64, device=points.device)
+    stream = stream or torch.cuda.current_stream(points.device)
+    with torch.cuda.device(points.device):
+        _check(lib().cg_signatures(ctypes.c_void_p(points.data_ptr()), n, dim,
+                                   ctypes.c_void_p(planes.data_ptr()), ell,
+                                   ctypes.c_void_p(words.data_ptr()),
+                                   ctypes.c_void_p(stream.cuda_stream)))
+    return words
+
+
+def build_points(points: torch.Tensor, planes: torch.Tensor, *, stream=None, dict_kind="global",
+                 lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False,
+                 sort_kind="auto") -> BuildResult:
+    """cg_build_points (f1): the cell graph of the sampled points' signatures,
+    computed and packed on the device (no n x ell byte matrix)."""
+    points, planes = _check_points(points, planes)
+    n, dim = points.shape
+    ell = planes.shape[0]
+    stream = stream or torch.cuda.current_stream(points.device)
+    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats,
+                      sort_kind)
+    c, e = cg_cells(), cg_edges()
+    with torch.cuda.device(points.device):
+        _check(lib().cg_build_points(ctypes.c_void_p(points.data_ptr()), n, dim,
+                                     ctypes.c_void_p(planes.data_ptr()), ell, ctypes.byref(o),
+                                     ctypes.byref(c), ctypes.byref(e)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    res = BuildResult(_wrap_cells(c, points.device), _wrap_edges(e, points.device))
+    if want_stats:
+        res.stats = _stats_dict(st)
+    if want_index and ih.value:
+        res.index = Index(ih.value, points.device)
     return res
 
 

@@ -728,8 +728,16 @@ static int validate_common(int64_t n, int32_t ell, const void* p, cg_cells* cell
   return CG_OK;
 }
 
+// f1 input: sampled points + half-space constraints (signatures on device)
+struct PointsIn {
+  const double* points = nullptr;
+  int dim = 0;
+  const double* planes = nullptr;
+};
+
 static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, int32_t ell,
-                       const cg_opts* o_in, cg_cells* cells, cg_edges* edges) {
+                       const cg_opts* o_in, cg_cells* cells, cg_edges* edges,
+                       const PointsIn* pin = nullptr) {
   if (cells) std::memset(cells, 0, sizeof(*cells));
   if (edges) std::memset(edges, 0, sizeof(*edges));
   cg_opts o;
@@ -740,8 +748,15 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
   const auto h0 = std::chrono::steady_clock::now();
   double setup_us = 0;
   try {
-    validate_common(n, ell, vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words),
-                    cells, edges);
+    const void* in0 = vecs ? static_cast<const void*>(vecs)
+                           : (words ? static_cast<const void*>(words)
+                                    : static_cast<const void*>(pin ? pin->points : nullptr));
+    validate_common(n, ell, in0, cells, edges);
+    if (pin) {
+      if (pin->dim < 1 || pin->dim > signatures_max_dim())
+        throw CgError{CG_EINVAL, "dim must be in [1, 16]"};
+      if (!pin->planes) throw CgError{CG_EINVAL, "planes is NULL"};
+    }
     if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
         o.dict_kind != CG_DICT_GLOBAL)
       throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
@@ -753,7 +768,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     };
     check_arch();
     lap("arch");
-    check_device_ptr(vecs ? static_cast<const void*>(vecs) : static_cast<const void*>(words), "input");
+    check_device_ptr(in0, "input");
+    if (pin) check_device_ptr(pin->planes, "planes");
     lap("ptr");
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
@@ -790,13 +806,17 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     } else if (vecs) {
       if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
       launch_pack(vecs, n, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo);
+    } else if (pin) {
+      if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
+      launch_signatures(pin->points, n, pin->dim, pin->planes, ell, keys.p, flags.p, s,
+                        msd ? top_hist.p : nullptr, dlo);
     } else {
       CG_CUDA(cudaMemcpyAsync(keys.p, words, size_t(n) * W * 8, cudaMemcpyDeviceToDevice, s));
       launch_check_pad(keys.p, n, ell, flags.p, s);
     }
     tm.mark();  // 1: pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(),
-                    (vecs && msd && !scatter) ? top_hist.p : nullptr,
+                    ((vecs || pin) && msd && !scatter) ? top_hist.p : nullptr,
                     scatter ? boff.p : nullptr, B);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
@@ -846,6 +866,42 @@ int cg_build_ex(const uint8_t* vecs, int64_t n, int32_t ell, const cg_opts* o, c
 int cg_build_packed_ex(const uint64_t* words, int64_t n, int32_t ell, const cg_opts* o,
                        cg_cells* cells, cg_edges* edges) {
   return build_entry(nullptr, words, n, ell, o, cells, edges);
+}
+
+int cg_build_points(const double* points, int64_t n, int32_t dim, const double* planes,
+                    int32_t ell, const cg_opts* o, cg_cells* cells, cg_edges* edges) {
+  PointsIn pin;
+  pin.points = points;
+  pin.dim = dim;
+  pin.planes = planes;
+  return build_entry(nullptr, nullptr, n, ell, o, cells, edges, &pin);
+}
+
+int cg_signatures(const double* points, int64_t n, int32_t dim, const double* planes,
+                  int32_t ell, uint64_t* words, cg_stream_t stream) {
+  try {
+    if (!points || !planes || !words) throw CgError{CG_EINVAL, "NULL argument"};
+    if (n < 1) throw CgError{CG_EINVAL, "n must be >= 1"};
+    if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    if (dim < 1 || dim > signatures_max_dim()) throw CgError{CG_EINVAL, "dim must be in [1, 16]"};
+    check_arch();
+    check_device_ptr(points, "points");
+    check_device_ptr(planes, "planes");
+    check_device_ptr(words, "words");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    WsScope ws;
+    DevBuf<uint32_t> flag(1, s);
+    CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
+    launch_signatures(points, n, dim, planes, ell, words, flag.p, s);
+    uint32_t* h = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+    CG_CUDA(cudaMemcpyAsync(h, flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (h[0]) throw CgError{CG_EINPUT, "non-finite constraint value (NaN/inf in points or planes)"};
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  }
+  return CG_OK;
 }
 
 int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* o_in,

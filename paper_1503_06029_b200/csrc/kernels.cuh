@@ -14,6 +14,15 @@ void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32
 // packed input: copy + check pad bits (err |= 1 if a pad bit is set)
 void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s);
 
+// ---------------------------------------------------------------- f1 signatures
+// points f64[n][dim], planes f64[ell][dim+1] (a_0..a_{dim-1}, b) -> packed
+// keys u64[n][W]: bit k = [fma chain b + sum a_t p_t >= 0] (sign.cu);
+// *err |= 1 on a non-finite value; optional top-digit histogram as k_pack.
+int signatures_max_dim();
+void launch_signatures(const double* pts, int64_t n, int dim, const double* planes, int ell,
+                       uint64_t* keys, uint32_t* err, cudaStream_t s, uint32_t* hist = nullptr,
+                       int dlo = 8);
+
 // ---------------------------------------------------------------- radix engine (a2, a4, a7)
 struct SortStats {
   int passes = 0;

@@ -243,6 +243,82 @@ def arrangement3d_uniform(seed: int, k: int = 64, n: int = 1 << 20):
 
 
 # --------------------------------------------------------------------------
+# f1 inputs: FP64 points + half-space planes (the signatures are computed by
+# the code under test, not here)
+# --------------------------------------------------------------------------
+def fig1_points():
+    """Three lines and the four points A, B, C, D of the paper's Figure 1
+    (P:60-90): planes f64[3, 3] rows (a_x, a_y, b) for a.p + b >= 0, points
+    f64[4, 2]; their signatures are the printed table A=111, B=110, C=100,
+    D=101.  The coordinates are a construction with that table (the
+    figure's geometry is not in the text)."""
+    planes = np.array([[1.0, 0.0, 0.0],     # c_0: x >= 0
+                       [0.0, 1.0, 0.0],     # c_1: y >= 0
+                       [-1.0, -1.0, 2.0]])  # c_2: x + y <= 2
+    points = np.array([[0.5, 0.5], [2.0, 1.0], [3.0, -0.5], [0.5, -0.5]])
+    return points, planes
+
+
+def arrangement_points(seed: int, k: int, dim: int, margin: float = 1e-9):
+    """k random hyperplanes in general position in R^dim (dim 2 or 3), unit
+    normals, offsets U(-0.5, 0.5), and 2^dim FP64 points around every vertex
+    (intersection of dim planes): vertex + delta * M^-1 s for every sign
+    pattern s, M the vertex's plane normals, so the points take all 2^dim
+    sign combinations of those planes while every other plane keeps its
+    sign at the vertex; every cell touches a vertex, so every cell is hit.
+    delta is a quarter of the distance to the nearest other plane, and the
+    arrangement is redrawn until every |a.p + b| >= margin (far above FP64
+    rounding), so any evaluation order yields the same signs.  Returns
+    (points f64[2^dim * C(k, dim), dim], planes f64[k, dim + 1]), shuffled."""
+    rng = np.random.default_rng(seed)
+    combos = np.array(list(itertools.combinations(range(k), dim)), dtype=np.int64)
+    signs = np.array(list(itertools.product((-1.0, 1.0), repeat=dim)))
+    for _ in range(200):
+        A = rng.standard_normal((k, dim))
+        A /= np.linalg.norm(A, axis=1, keepdims=True)
+        b = rng.uniform(-0.5, 0.5, size=k)
+        M = A[combos]                                   # [V, dim, dim]
+        if np.min(np.abs(np.linalg.det(M))) < 1e-6:
+            continue
+        V = np.linalg.solve(M, -b[combos][..., None])[..., 0]  # vertices [V, dim]
+        Dir = np.linalg.solve(M[:, None], signs[None, :, :, None])[..., 0]  # [V, 2^dim, dim]
+        val = V @ A.T + b[None, :]                       # [V, k]
+        own = np.zeros_like(val, dtype=bool)
+        own[np.arange(len(combos))[:, None], combos] = True
+        other = np.where(own, np.inf, np.abs(val))
+        slope = np.abs(np.einsum("vsd,kd->vsk", Dir, A)).max(axis=1)  # [V, k]
+        slope = np.where(own, 0.0, slope)
+        delta = 0.25 * np.min(other / np.maximum(slope, 1e-300), axis=1)  # [V]
+        pts = (V[:, None, :] + delta[:, None, None] * Dir).reshape(-1, dim)
+        vals = pts @ A.T + b[None, :]
+        if np.min(np.abs(vals)) < margin:
+            continue
+        planes = np.concatenate([A, b[:, None]], axis=1)
+        return np.ascontiguousarray(pts[rng.permutation(len(pts))]), planes
+    raise RuntimeError(f"no arrangement of {k} planes in R^{dim} with margin {margin}")
+
+
+def arrangement_cells_edges(k: int, dim: int):
+    """Closed forms for a simple arrangement of k hyperplanes in R^dim
+    (dim 2: 1 + k + C(k,2) cells, k^2 edges; dim 3: sum_{i<=3} C(k,i) cells,
+    k * sum_{i<=2} C(k-1,i) edges -- every facet on a plane is a cell of the
+    induced (dim-1)-arrangement)."""
+    cells = sum(math.comb(k, i) for i in range(dim + 1))
+    edges = k * sum(math.comb(k - 1, i) for i in range(dim))
+    return cells, edges
+
+
+def points_uniform(seed: int, k: int, n: int, dim: int = 3):
+    """C3-style FP64 input for f1 at any size: k planes (N(0,I) unit normals,
+    U(-1/2,1/2) offsets) and n points uniform in [-1,1]^dim."""
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((k, dim))
+    A /= np.linalg.norm(A, axis=1, keepdims=True)
+    b = rng.uniform(-0.5, 0.5, size=k)
+    return rng.uniform(-1.0, 1.0, size=(n, dim)), np.concatenate([A, b[:, None]], axis=1)
+
+
+# --------------------------------------------------------------------------
 # small structured / random inputs for tests
 # --------------------------------------------------------------------------
 def hypercube(ell: int) -> np.ndarray:
