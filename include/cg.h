@@ -139,8 +139,9 @@ int cg_build_packed_ex(const uint64_t* words, int64_t n, int32_t ell, const cg_o
  * The value is evaluated in one fixed IEEE-754 order, v = b_k;
  * v = fma(a_kt, p_t, v) for t = 0 .. dim-1 (round to nearest, DESIGN G21),
  * so results are bit-reproducible on any IEEE machine.  Inputs are borrowed.
- * Errors: CG_EINVAL (NULL/host pointers, n < 1, ell or dim out of range),
- * CG_EINPUT (a value is NaN or infinite). */
+ * Every coordinate and coefficient must be finite with |x| <= 2^60 (then no
+ * value can overflow).  Errors: CG_EINVAL (NULL/host pointers, n < 1, ell or
+ * dim out of range), CG_EINPUT (an input NaN, infinite or above 2^60). */
 
 /* Signatures only: words = u64[n][ceil(ell/64)] (device, caller-allocated),
  * the packed format of cg_cells.  Blocks until done (the error flag). */

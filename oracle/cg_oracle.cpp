@@ -359,12 +359,19 @@ int oracle_query(const uint64_t* cells, int64_t nc, int32_t ell, const uint64_t*
 // f1: signatures of n points (row-major f64[n][dim]) against ell half-spaces
 // (f64[ell][dim+1], row k = a_k0 .. a_k(dim-1), b_k) as bytes u8[n][ell]
 // (the oracle's vector input form).  Returns 0, or -1 (bad sizes or
-// NULL), -2 (a non-finite constraint value).
+// NULL), -2 (an input not finite or above 2^60 in magnitude, or a
+// non-finite value).
 int oracle_signatures(const double* points, int64_t n, int32_t dim, const double* planes,
                       int32_t ell, uint8_t* out) {
   if (!points || !planes || !out || n < 1 || dim < 1 || dim > 16 || ell < 1 || ell > kMaxEll)
     return kEINVAL;
   int rc = kOK;
+  // inputs must be finite with magnitude <= 2^60 (the C ABI's contract)
+  const double kMaxMag = std::ldexp(1.0, 60);
+  for (int64_t i = 0; i < n * dim; ++i)
+    if (!(std::fabs(points[i]) <= kMaxMag)) rc = kEINPUT;
+  for (int64_t i = 0; i < int64_t(ell) * (dim + 1); ++i)
+    if (!(std::fabs(planes[i]) <= kMaxMag)) rc = kEINPUT;
   for (int64_t r = 0; r < n; ++r) {
     const double* p = points + r * dim;
     for (int k = 0; k < ell; ++k) {

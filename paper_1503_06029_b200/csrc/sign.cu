@@ -7,14 +7,15 @@
 // DESIGN G12), points are f64[n][dim], planes f64[ell][dim + 1] =
 // (a_i0 .. a_i(dim-1), b_i).  The value is evaluated in ONE fixed IEEE-754
 // order, v = b; v = fma(a_t, p_t, v) for t = 0 .. dim-1 (DESIGN G21), so the
-// CPU oracle (std::fma, same order) reproduces every bit exactly.  A
-// non-finite value raises *err (CG_EINPUT).
+// CPU oracle (std::fma, same order) reproduces every bit exactly.  Inputs
+// must be finite with magnitude <= 2^60 (then no value can overflow); any
+// other input raises *err (CG_EINPUT).
 //
 // The output is the packed key layout of pack.cu (bit k at word k/64,
 // position 63 - k%64), so the sort consumes it directly and the n*ell-byte
-// signature matrix never exists (8.6 GB at C5).  One thread per output word:
-// it loads its point once (coalesced: consecutive threads, consecutive
-// points) and evaluates its <= 64 planes from shared memory.  Like k_pack it
+// signature matrix never exists (8.6 GB at C5).  One thread per point: it
+// loads its point once (coalesced) and evaluates the planes word by word from
+// shared memory (warp-uniform plane index: broadcast loads).  Like k_pack it
 // can count the MSD sort's top digits of word 0 on the way.
 #include "kernels.cuh"
 
@@ -23,6 +24,9 @@ namespace {
 
 constexpr int kSignThreads = 256;
 constexpr int kMaxDim = 16;
+// |coordinate|, |coefficient| <= 2^60: the fma chain of <= 16 terms then
+// stays below 2^125 in magnitude, far from overflow, so every value is finite
+constexpr double kMaxMag = 1152921504606846976.0;  // 2^60
 
 template <int DIM>  // DIM > 0: compile-time dimension; 0: runtime dim
 __global__ void __launch_bounds__(kSignThreads)
@@ -35,48 +39,93 @@ __global__ void __launch_bounds__(kSignThreads)
   const int dim = DIM > 0 ? DIM : dim_rt;
   const int pl = dim + 1;
   const double* P = planes;
-  if (planes_in_smem) {
-    for (int i = threadIdx.x; i < ell * pl; i += blockDim.x) spl[i] = planes[i];
-    P = spl;
+  bool bad = false;
+  // inputs bounded by kMaxMag keep every fma chain finite (checked once per
+  // value instead of per result)
+  for (int i = threadIdx.x; i < ell * pl; i += blockDim.x) {
+    const double c = planes[i];
+    bad |= !(fabs(c) <= kMaxMag);
+    if (planes_in_smem) spl[i] = c;
   }
+  if (planes_in_smem) P = spl;
   const int nd = hist ? 8 - dlo : 0;
   if (hist)
     for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   uint32_t last[3] = {0, 0, 0}, cnt[3] = {0, 0, 0};
-  bool bad = false;
-  const int64_t total = n * W;
-  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
-       g += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = g / W;
-    const int w = int(g - r * W);
-    double p[DIM > 0 ? DIM : kMaxDim];
+  // thread per group of R consecutive points: all lanes of a warp evaluate
+  // the same plane at the same time (shared-memory broadcast loads), and each
+  // plane's coefficients are loaded once for R points (register blocking)
+  constexpr int R = 4;
+  const int64_t ngroups = (n + R - 1) / R;
+  for (int64_t gq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; gq < ngroups;
+       gq += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r0 = gq * R;
+    double p[R][DIM > 0 ? DIM : kMaxDim];
 #pragma unroll
-    for (int t = 0; t < (DIM > 0 ? DIM : kMaxDim); ++t)
-      if (t < dim) p[t] = __ldg(pts + r * dim + t);
-    const int k0 = 64 * w, len = min(64, ell - k0);
-    uint64_t word = 0;
-    for (int j = 0; j < len; ++j) {
-      const double* a = P + (k0 + j) * pl;
-      double v = a[dim];  // b_k
+    for (int q = 0; q < R; ++q) {
+      const int64_t r = r0 + q < n ? r0 + q : n - 1;
 #pragma unroll
       for (int t = 0; t < (DIM > 0 ? DIM : kMaxDim); ++t)
-        if (t < dim) v = __fma_rn(a[t], p[t], v);
-      bad |= !isfinite(v);
-      word |= uint64_t(v >= 0.0) << (63 - j);
+        if (t < dim) p[q][t] = __ldg(pts + r * dim + t);
     }
-    keys[g] = word;
-    if (nd && w == 0) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        if (d < nd) {
-          const uint32_t bin = uint32_t(word >> (8 * (dlo + d))) & 255u;
-          if (bin != last[d]) {
-            if (cnt[d]) atomicAdd(&sh[d][last[d]], cnt[d]);
-            last[d] = bin;
-            cnt[d] = 0;
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int t = 0; t < (DIM > 0 ? DIM : kMaxDim); ++t)
+        if (t < dim) bad |= !(fabs(p[q][t]) <= kMaxMag);
+    for (int w = 0; w < W; ++w) {
+      const int k0 = 64 * w, len = min(64, ell - k0);
+      // bits shifted in MSB-first: plane k0 + j ends at position 63 - j
+      uint32_t hi[R], lo[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) hi[q] = lo[q] = 0u;
+#pragma unroll 4
+      for (int j = 0; j < len; ++j) {
+        const double* a = P + (k0 + j) * pl;
+        double v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = a[dim];  // b_k
+#pragma unroll
+        for (int t = 0; t < (DIM > 0 ? DIM : kMaxDim); ++t) {
+          if (t < dim) {
+            const double at = a[t];
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[q] = __fma_rn(at, p[q][t], v[q]);
           }
-          ++cnt[d];
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const uint32_t bit = v[q] >= 0.0 ? 1u : 0u;
+          if (j < 32) hi[q] = 2u * hi[q] + bit;
+          else lo[q] = 2u * lo[q] + bit;
+        }
+      }
+      uint64_t word[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        // left-align a short last word (len < 64)
+        const uint64_t wv = len > 32 ? (uint64_t(hi[q]) << (len - 32)) | lo[q] : uint64_t(hi[q]);
+        word[q] = wv << (64 - len);
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (r0 + q < n) {
+          keys[(r0 + q) * W + w] = word[q];
+          if (nd && w == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              if (d < nd) {
+                const uint32_t bin = uint32_t(word[q] >> (8 * (dlo + d))) & 255u;
+                if (bin != last[d]) {
+                  if (cnt[d]) atomicAdd(&sh[d][last[d]], cnt[d]);
+                  last[d] = bin;
+                  cnt[d] = 0;
+                }
+                ++cnt[d];
+              }
+            }
+          }
         }
       }
     }
@@ -101,8 +150,7 @@ int signatures_max_dim() { return kMaxDim; }
 void launch_signatures(const double* pts, int64_t n, int dim, const double* planes, int ell,
                        uint64_t* keys, uint32_t* err, cudaStream_t s, uint32_t* hist, int dlo) {
   const int W = (ell + 63) / 64;
-  const int64_t total = n * W;
-  int64_t blocks = std::min<int64_t>((total + kSignThreads - 1) / kSignThreads,
+  int64_t blocks = std::min<int64_t>((n + 4 * kSignThreads - 1) / (4 * kSignThreads),
                                      int64_t(num_sms()) * 8);
   if (blocks < 1) blocks = 1;
   if (hist && (dlo < 5 || dlo > 7)) hist = nullptr;

@@ -119,6 +119,9 @@ def test_points_errors(cg):
         cg.build_points(_dev(P), _dev(np.full((5, 4), np.inf)))
     assert ei.value.code == CG_EINPUT
     with pytest.raises(CgError) as ei:
+        cg.signatures(_dev(np.full((4, 3), 2.0 ** 61)), _dev(A))
+    assert ei.value.code == CG_EINPUT
+    with pytest.raises(CgError) as ei:
         cg.build_points(_dev(np.zeros((4, 17))), _dev(np.ones((5, 18))))
     assert ei.value.code == CG_EINVAL
     with pytest.raises(CgError):

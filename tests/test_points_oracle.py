@@ -62,6 +62,10 @@ def test_nonfinite_is_einput():
     assert rc == oracle.EINPUT
     rc, _ = oracle.signatures(np.array([[1.0, 0.0]]), np.array([[np.inf, 0.0, 0.0]]))
     assert rc == oracle.EINPUT
+    rc, _ = oracle.signatures(np.array([[2.0 ** 61, 0.0]]), np.array([[1.0, 0.0, 0.0]]))
+    assert rc == oracle.EINPUT
+    rc, _ = oracle.signatures(np.array([[2.0 ** 60, 0.0]]), np.array([[1.0, 0.0, 0.0]]))
+    assert rc == 0
 
 
 def test_fma_order_is_the_definition():
