@@ -253,6 +253,8 @@ def run_ours(args):
             "alg_bytes_def": "compulsory bytes, DESIGN.md section 6 (bench.alg_bytes)"}
     total_alg = sum(ab.values())
     whole = total_alg / (ms * 1e-3) / 1e9
+    # ---- row f1: on-device signatures of FP64 points (not part of the step)
+    f1 = run_f1(torch, cg, dev, lg) if args.f1 else None
     # ---- e2e through the host-buffer C-ABI entry
     e2e = run_e2e(torch, cg, x, args, dev)
     # ---- CPU oracle baseline on a bounded sample
@@ -280,6 +282,7 @@ def run_ours(args):
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "f1_signatures": f1,
     }
     print(json.dumps(out))
 
@@ -416,6 +419,40 @@ def run_dist_e2e(torch, tdist, cgdist, x, ell, ops, stream, dev, args, rank, wor
             "steps": args.e2e_steps, "api": "dist.build_distributed (pinned host shards)"}
 
 
+def run_f1(torch, cg, dev, lg):
+    """Row f1 measured alone: cg_signatures on n = 2^lg uniform FP64 points in
+    R^3 against ell = 128 C3-style planes (device-resident inputs).  The
+    kernel is FP64-FMA bound: peak = 148 SMs x 64 FP64 FMA/clk x 2 flop x
+    the SM clock."""
+    import synth
+
+    n, ell, dim = 1 << lg, 128, 3
+    _, A = synth.points_uniform(5, ell, 1, dim)
+    pts = torch.empty((n, dim), dtype=torch.float64, device=dev)
+    pts.uniform_(-1.0, 1.0, generator=torch.Generator(device=dev).manual_seed(5))
+    planes = torch.from_numpy(A).to(dev)
+    w = cg.signatures(pts, planes)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        w = cg.signatures(pts, planes)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    del w, pts
+    flops = 2.0 * n * ell * dim
+    peak = 148 * 64 * 2 * 1.965e9 / 1e12
+    tf = flops / (ms * 1e-3) / 1e12
+    return {"n": n, "ell": ell, "dim": dim, "ms": round(ms, 3),
+            "points_per_s": round(n / (ms * 1e-3), 1),
+            "roofline": {"bound": "alu", "unit": "TFLOP/s (fp64 fma)", "achieved": round(tf, 2),
+                         "peak": round(peak, 2), "frac": round(tf / peak, 4),
+                         "peak_source": "148 SM x 64 fp64 FMA/clk x 2 x 1.965 GHz (unit counts)"},
+            "hbm_bytes": n * dim * 8 + n * 16}
+
+
 def run_e2e(torch, cg, x, args, dev):
     """Same metric through cg_build_host: pinned host input, H2D + build +
     D2H of the cell table and edge list inside the timed region."""
@@ -512,6 +549,8 @@ def main():
     ap.add_argument("--scale-log2", type=int, default=26, help="C5 n = 2^k (26 = BASELINE CFG5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-f1", dest="f1", action="store_false",
+                    help="skip the row-f1 signature measurement")
     ap.add_argument("--cpu-sample-log2", type=int, default=22)
     ap.add_argument("--ref-sample-log2", type=int, default=20)
     args = ap.parse_args()

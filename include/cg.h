@@ -153,6 +153,31 @@ int cg_signatures(const double* points, int64_t n, int32_t dim, const double* pl
 int cg_build_points(const double* points, int64_t n, int32_t dim, const double* planes,
                     int32_t ell, const cg_opts* o, cg_cells* cells, cg_edges* edges);
 
+/* ---- f4: path queries on G_X ----------------------
+ * The graph is built so that one can "find a path in such a graph" (P:20,
+ * P:57); GPU graph traversal is the paper's stated next step. */
+
+/* CSR of the undirected cell graph from the canonical edge list of
+ * cg_build (edges = u32[n_edges][2], (i, j) with i < j, ascending; device).
+ * Outputs (device, caller-allocated): row_ptr = u64[n_cells + 1], col =
+ * u32[2 * n_edges]; the neighbours of v are col[row_ptr[v] .. row_ptr[v+1])
+ * in ascending order.  Blocks until done.  Errors: CG_EINVAL (NULL/host
+ * pointers, n_cells < 1, n_edges < 0), CG_ETOOBIG (n_cells >= 2^32).  The
+ * edge list must be canonical with indices < n_cells (unchecked). */
+int cg_csr(const uint32_t* edges, int64_t n_edges, int64_t n_cells, uint64_t* row_ptr,
+           uint32_t* col, cg_stream_t stream);
+
+/* Breadth-first search from `source` over a CSR of cg_csr: dist = i32[n_cells]
+ * (device) receives the number of edges on a shortest path (-1: not
+ * reachable); parent (optional, i32[n_cells]) the canonical BFS tree: the
+ * smallest neighbour one step closer to the source (-1 for the source and
+ * unreachable cells), so a path to any cell is read back by following it.
+ * *eccentricity (optional, host) = the largest finite distance.  Blocks
+ * (one host synchronisation per level).  Errors: CG_EINVAL (NULL/host
+ * pointers, source out of range), CG_ETOOBIG. */
+int cg_bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t n_cells, int64_t source,
+           int32_t* dist, int32_t* parent, int32_t* eccentricity, cg_stream_t stream);
+
 /* End-to-end entry with HOST buffers.  h_vecs = uint8[n][ell] in host memory
  * (pinned for full PCIe speed, pageable accepted).  The library copies it to
  * the device (chunked, overlapped with the pack kernel), builds, and copies

@@ -15,6 +15,7 @@ build_packed(words_u64[n, W], ell)
 brute(bytes_u8[n, ell])          ORACLE-B: sort/unique + all-pairs distance
 query(cells_u64[nc, W], ell, q_u64[nq, W])  self / neighbour indices
 signatures(points_f64[n, dim], planes_f64[ell, dim+1])  f1: bytes u8[n, ell]
+csr(edges_u32[m, 2], nv) / bfs(row_ptr, col, src)      f4: adjacency, distances, parents
 All return ``(rc, cells u64[nc, W], edges u32[m, 2])`` (query: ``(rc, self, nbr)``).
 """
 from __future__ import annotations
@@ -60,6 +61,10 @@ def _load():
         lib.oracle_brute.argtypes = [P, i64, i32, i32, pp, pi64, pp, pi64]
         lib.oracle_query.argtypes = [P, i64, i32, P, i64, P, P]
         lib.oracle_signatures.argtypes = [P, i64, i32, P, i32, P]
+        lib.oracle_csr.argtypes = [P, i64, i64, P, P]
+        lib.oracle_csr.restype = ctypes.c_int
+        lib.oracle_bfs.argtypes = [P, P, i64, i64, P, P]
+        lib.oracle_bfs.restype = ctypes.c_int
         lib.oracle_signatures.restype = ctypes.c_int
         lib.oracle_free.argtypes = [P]
         for f in (lib.oracle_build, lib.oracle_build_packed, lib.oracle_brute, lib.oracle_query):
@@ -191,3 +196,29 @@ def signatures(points: np.ndarray, planes: np.ndarray):
     out = np.zeros((n, ell), dtype=np.uint8)
     rc = lib.oracle_signatures(P.ctypes.data, n, dim, A.ctypes.data, ell, out.ctypes.data)
     return rc, out
+
+
+def csr(edges: np.ndarray, nv: int):
+    """f4 adjacency of G_X: ``(rc, row_ptr u64[nv+1], col u32[2m])``."""
+    lib = _load()
+    E = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+    m = E.shape[0]
+    row_ptr = np.zeros(nv + 1, dtype=np.uint64)
+    col = np.zeros(max(1, 2 * m), dtype=np.uint32)
+    rc = lib.oracle_csr(E.ctypes.data, m, nv, row_ptr.ctypes.data, col.ctypes.data)
+    return rc, row_ptr, col[: 2 * m]
+
+
+def bfs(row_ptr: np.ndarray, col: np.ndarray, src: int):
+    """f4 BFS: ``(rc, dist i32[nv], parent i32[nv])``."""
+    lib = _load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+    cl = np.ascontiguousarray(col, dtype=np.uint32)
+    if cl.size == 0:
+        cl = np.zeros(1, dtype=np.uint32)
+    nv = rp.shape[0] - 1
+    dist = np.zeros(nv, dtype=np.int32)
+    parent = np.zeros(nv, dtype=np.int32)
+    rc = lib.oracle_bfs(rp.ctypes.data, cl.ctypes.data, nv, int(src), dist.ctypes.data,
+                        parent.ctypes.data)
+    return rc, dist, parent

@@ -22,6 +22,10 @@
  *   ORACLE-B  oracle_brute : unpacked byte vectors, std::sort + std::unique,
  *             then all-pairs Hamming distance (the naive method).
  *   plus      oracle_query : self/neighbour lookup of query vectors.
+ *   and       oracle_csr / oracle_bfs : adjacency lists of G_X and breadth-
+ *             first distances from a source (the f4 row: "find a path in
+ *             such a graph"); parent = the smallest neighbour
+ *             one step closer to the source (DESIGN G22).
  *   and       oracle_signatures : the cell signature of sampled points (the
  *             f1 row): bit k of point P is 1 iff P satisfies constraint c_k
  *             (P:92), c_k being the half-space a_k . p + b_k >= 0 (a tie is
@@ -44,6 +48,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <new>
 #include <set>
 #include <thread>
@@ -383,6 +388,59 @@ int oracle_signatures(const double* points, int64_t n, int32_t dim, const double
     }
   }
   return rc;
+}
+
+// f4: adjacency of the undirected graph with vertices 0..nv-1 and edge list
+// u32[m][2] -> row_ptr u64[nv+1], col u32[2m] (each list ascending).
+int oracle_csr(const uint32_t* edges, int64_t m, int64_t nv, uint64_t* row_ptr, uint32_t* col) {
+  if (nv < 1 || m < 0 || !row_ptr || (m > 0 && (!edges || !col))) return kEINVAL;
+  std::vector<std::vector<uint32_t>> adj(static_cast<size_t>(nv));
+  for (int64_t e = 0; e < m; ++e) {
+    const uint32_t a = edges[2 * e], b = edges[2 * e + 1];
+    if (a >= nv || b >= nv) return kEINVAL;
+    adj[a].push_back(b);
+    adj[b].push_back(a);
+  }
+  uint64_t at = 0;
+  for (int64_t v = 0; v < nv; ++v) {
+    std::sort(adj[v].begin(), adj[v].end());
+    row_ptr[v] = at;
+    for (uint32_t w : adj[v]) col[at++] = w;
+  }
+  row_ptr[nv] = at;
+  return kOK;
+}
+
+// f4: BFS distances from src over the CSR (queue order is irrelevant to the
+// distances); parent[v] = smallest neighbour u with dist[u] = dist[v] - 1.
+int oracle_bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t nv, int64_t src,
+               int32_t* dist, int32_t* parent) {
+  if (nv < 1 || src < 0 || src >= nv || !row_ptr || !dist || !parent) return kEINVAL;
+  for (int64_t v = 0; v < nv; ++v) dist[v] = -1;
+  std::deque<uint32_t> q;
+  dist[src] = 0;
+  q.push_back(uint32_t(src));
+  while (!q.empty()) {
+    const uint32_t v = q.front();
+    q.pop_front();
+    for (uint64_t k = row_ptr[v]; k < row_ptr[v + 1]; ++k) {
+      const uint32_t w = col[k];
+      if (dist[w] < 0) {
+        dist[w] = dist[v] + 1;
+        q.push_back(w);
+      }
+    }
+  }
+  for (int64_t v = 0; v < nv; ++v) {
+    parent[v] = -1;
+    if (dist[v] > 0)
+      for (uint64_t k = row_ptr[v]; k < row_ptr[v + 1]; ++k)
+        if (dist[col[k]] == dist[v] - 1) {
+          parent[v] = int32_t(col[k]);
+          break;
+        }
+  }
+  return kOK;
 }
 
 void oracle_free(void* p) { std::free(p); }

@@ -107,6 +107,10 @@ def lib():
     L.cg_version.restype = ctypes.c_int
     L.cg_kernel_launches.argtypes = []
     L.cg_kernel_launches.restype = ctypes.c_int64
+    L.cg_csr.argtypes = [P, i64, i64, P, P, P]
+    L.cg_csr.restype = ctypes.c_int
+    L.cg_bfs.argtypes = [P, P, i64, i64, P, P, ctypes.POINTER(i32), P]
+    L.cg_bfs.restype = ctypes.c_int
     L.cg_signatures.argtypes = [P, i64, i32, P, i32, P, P]
     L.cg_signatures.restype = ctypes.c_int
     L.cg_build_points.argtypes = [P, i64, i32, P, i32, ctypes.POINTER(cg_opts),
@@ -163,7 +167,7 @@ def _install_torch_allocator(L):
 EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg_build_host",
             "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
-            "cg_kernel_launches", "cg_signatures", "cg_build_points",
+            "cg_kernel_launches", "cg_signatures", "cg_build_points", "cg_csr", "cg_bfs",
             "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
 
 
@@ -508,3 +512,39 @@ def dist_finalize(gathered: torch.Tensor, counts, *, stream=None,
 def kernel_launches() -> int:
     """Kernels the library has launched in this process (cg_kernel_launches)."""
     return int(lib().cg_kernel_launches())
+
+
+def csr(edges: torch.Tensor, n_cells: int, *, stream=None):
+    """cg_csr (f4): canonical edge list int32 [m, 2] (device) -> (row_ptr int64
+    [n_cells + 1], col int32 [2m]) with sorted adjacency lists."""
+    if edges.dim() != 2 or edges.shape[1] != 2 or edges.dtype != torch.int32 or not edges.is_cuda:
+        raise CgError(CG_EINVAL, "edges must be a CUDA int32 tensor [m, 2]")
+    edges = edges.contiguous()
+    m = edges.shape[0]
+    dev = edges.device
+    row_ptr = torch.empty(n_cells + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(1, 2 * m), dtype=torch.int32, device=dev)
+    stream = stream or torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        _check(lib().cg_csr(ctypes.c_void_p(edges.data_ptr()), m, n_cells,
+                            ctypes.c_void_p(row_ptr.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                            ctypes.c_void_p(stream.cuda_stream)))
+    return row_ptr, col[: 2 * m]
+
+
+def bfs(row_ptr: torch.Tensor, col: torch.Tensor, source: int, *, want_parent=True,
+        stream=None):
+    """cg_bfs (f4): (dist int32 [n], parent int32 [n] or None, eccentricity)."""
+    n = row_ptr.shape[0] - 1
+    dev = row_ptr.device
+    dist = torch.empty(n, dtype=torch.int32, device=dev)
+    parent = torch.empty(n, dtype=torch.int32, device=dev) if want_parent else None
+    ecc = ctypes.c_int32()
+    stream = stream or torch.cuda.current_stream(dev)
+    col = col if col.numel() else torch.zeros(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().cg_bfs(ctypes.c_void_p(row_ptr.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                            n, int(source), ctypes.c_void_p(dist.data_ptr()),
+                            ctypes.c_void_p(parent.data_ptr() if parent is not None else 0),
+                            ctypes.byref(ecc), ctypes.c_void_p(stream.cuda_stream)))
+    return dist, parent, ecc.value

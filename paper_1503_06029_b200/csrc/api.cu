@@ -877,6 +877,52 @@ int cg_build_points(const double* points, int64_t n, int32_t dim, const double* 
   return build_entry(nullptr, nullptr, n, ell, o, cells, edges, &pin);
 }
 
+int cg_csr(const uint32_t* edges, int64_t n_edges, int64_t n_cells, uint64_t* row_ptr,
+           uint32_t* col, cg_stream_t stream) {
+  try {
+    if (!row_ptr || (n_edges > 0 && (!edges || !col))) throw CgError{CG_EINVAL, "NULL argument"};
+    if (n_cells < 1 || n_edges < 0) throw CgError{CG_EINVAL, "n_cells >= 1, n_edges >= 0"};
+    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    check_arch();
+    if (n_edges > 0) {
+      check_device_ptr(edges, "edges");
+      check_device_ptr(col, "col");
+    }
+    check_device_ptr(row_ptr, "row_ptr");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    WsScope ws;
+    build_csr(edges, n_edges, n_cells, row_ptr, col, s);
+    CG_CUDA(cudaStreamSynchronize(s));
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  }
+  return CG_OK;
+}
+
+int cg_bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t n_cells, int64_t source,
+           int32_t* dist, int32_t* parent, int32_t* eccentricity, cg_stream_t stream) {
+  try {
+    if (!row_ptr || !col || !dist) throw CgError{CG_EINVAL, "NULL argument"};
+    if (n_cells < 1 || source < 0 || source >= n_cells)
+      throw CgError{CG_EINVAL, "source must be in [0, n_cells)"};
+    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    check_arch();
+    check_device_ptr(row_ptr, "row_ptr");
+    check_device_ptr(dist, "dist");
+    if (parent) check_device_ptr(parent, "parent");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    WsScope ws;
+    const int ecc = bfs(row_ptr, col, n_cells, source, dist, parent, s);
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (eccentricity) *eccentricity = ecc;
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  }
+  return CG_OK;
+}
+
 int cg_signatures(const double* points, int64_t n, int32_t dim, const double* planes,
                   int32_t ell, uint64_t* words, cg_stream_t stream) {
   try {

@@ -23,6 +23,17 @@ void launch_signatures(const double* pts, int64_t n, int dim, const double* plan
                        uint64_t* keys, uint32_t* err, cudaStream_t s, uint32_t* hist = nullptr,
                        int dlo = 8);
 
+// ---------------------------------------------------------------- f4 CSR + BFS (graph.cu)
+// canonical edge list (u32 (i, j), i < j, ascending) -> CSR with sorted
+// adjacency: row_ptr u64[nv + 1], col u32[2m]
+void build_csr(const uint32_t* edges, int64_t m, int64_t nv, uint64_t* row_ptr, uint32_t* col,
+               cudaStream_t s);
+// level-synchronous BFS from src: dist i32[nv] (-1 unreachable), optional
+// canonical parent i32[nv] (smallest neighbour one level closer, -1 for the
+// source / unreachable).  Returns the source's eccentricity.  Host-synchronising.
+int bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t nv, int64_t src, int32_t* dist,
+        int32_t* parent, cudaStream_t s);
+
 // ---------------------------------------------------------------- radix engine (a2, a4, a7)
 struct SortStats {
   int passes = 0;
