@@ -253,8 +253,10 @@ def run_ours(args):
             "alg_bytes_def": "compulsory bytes, DESIGN.md section 6 (bench.alg_bytes)"}
     total_alg = sum(ab.values())
     whole = total_alg / (ms * 1e-3) / 1e9
-    # ---- row f1: on-device signatures of FP64 points (not part of the step)
+    # ---- rows f1 / f4, measured alone (not part of the step)
     f1 = run_f1(torch, cg, dev, lg) if args.f1 else None
+    f4 = run_f4(torch, cg, dev) if args.f1 else None
+    f3 = run_f3(torch, cg, dev) if args.f1 else None
     # ---- e2e through the host-buffer C-ABI entry
     e2e = run_e2e(torch, cg, x, args, dev)
     # ---- CPU oracle baseline on a bounded sample
@@ -283,6 +285,8 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "f1_signatures": f1,
+        "f4_csr_bfs": f4,
+        "f3_allpairs": f3,
     }
     print(json.dumps(out))
 
@@ -451,6 +455,63 @@ def run_f1(torch, cg, dev, lg):
                          "peak": round(peak, 2), "frac": round(tf / peak, 4),
                          "peak_source": "148 SM x 64 fp64 FMA/clk x 2 x 1.965 GHz (unit counts)"},
             "hbm_bytes": n * dim * 8 + n * 16}
+
+
+def run_f4(torch, cg, dev, ell=22):
+    """Row f4 measured alone: CSR construction and a BFS over the cell graph of
+    the hypercube H_ell (all 2^ell cells: 4.2M cells, 46M edges at ell = 22),
+    built by cg_build (not timed); TEPS = 2m / BFS time."""
+    import synth
+
+    x = torch.from_numpy(synth.hypercube(ell)).to(dev)
+    res = cg.build(x)
+    n, m = res.cells.shape[0], res.edges.shape[0]
+    del x
+    rp, col = cg.csr(res.edges, n)
+    dist, parent, ecc = cg.bfs(rp, col, 0)
+    torch.cuda.synchronize(dev)
+    reps = 3
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    for _ in range(reps):
+        rp, col = cg.csr(res.edges, n)
+    e1.record()
+    for _ in range(reps):
+        dist, parent, ecc = cg.bfs(rp, col, 0)
+    e2.record()
+    torch.cuda.synchronize(dev)
+    csr_ms, bfs_ms = e0.elapsed_time(e1) / reps, e1.elapsed_time(e2) / reps
+    return {"graph": f"hypercube H_{ell}", "n_cells": n, "n_edges": m, "csr_ms": round(csr_ms, 3),
+            "bfs_ms": round(bfs_ms, 3), "bfs_levels": ecc + 1,
+            "teps": round(2 * m / (bfs_ms * 1e-3), 1),
+            "note": "BFS includes the canonical-parent pass and one host sync per level"}
+
+
+def run_f3(torch, cg, dev):
+    """Row f3 measured alone: cg_allpairs on the C5 recipe's first 2^17 cells
+    (ell = 128): the naive method (every pair) and Alg. 1-2 with h = 5 anchors
+    (the paper's best h on its GPU); pair-checks/s."""
+    import synth
+
+    d = synth.config("C5", scale_log2=17)
+    x = synth.unpack_words_torch(torch.from_numpy(d["words"].view(np.int64)).to(dev), d["ell"])
+    res = cg.build(x)
+    n = res.cells.shape[0]
+    out = {"workload": "C5 recipe at n = 2^17 (ell = 128)", "n_cells": n,
+           "pairs": n * (n - 1) // 2}
+    for h in (0, 5):
+        e, cmp = cg.allpairs(res.cells, d["ell"], h)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        e, cmp = cg.allpairs(res.cells, d["ell"], h)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        out[f"h{h}"] = {"ms": round(ms, 2), "pairs_compared": cmp,
+                        "pairs_per_s": round(out["pairs"] / (ms * 1e-3), 1),
+                        "edges_match_build": bool(torch.equal(e, res.edges))}
+    return out
 
 
 def run_e2e(torch, cg, x, args, dev):

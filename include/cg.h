@@ -153,6 +153,21 @@ int cg_signatures(const double* points, int64_t n, int32_t dim, const double* pl
 int cg_build_points(const double* points, int64_t n, int32_t dim, const double* planes,
                     int32_t ell, const cg_opts* o, cg_cells* cells, cg_edges* edges);
 
+/* ---- f3: the all-pairs methods ----------------------
+ * Distance-1 pairs of a cell table by comparing pairs: the naive method
+ * with `anchors` = 0, Alg. 1-2 with `anchors` = h in
+ * [1, 8]: d(x_a, x_j) precomputed for the first h cells, a pair skipped when
+ * |d(x_a, x_i) - d(x_a, x_j)| > 1 for some anchor (the triangle inequality,
+ * P:46; the sound form of the guard, DESIGN G15).  cells = u64[n_cells][W]
+ * (device, distinct rows, e.g. cg_build's table); *edges receives the
+ * canonical list (i < j, ascending; free with cg_edges_free) -- equal to
+ * cg_build's edge list for a canonical table, hence an independent in-GPU
+ * cross-check.  *pairs_compared (optional) = pairs that passed the anchor
+ * test.  O(n^2) work: meant for n up to ~10^6.  Blocks.  Errors: CG_EINVAL,
+ * CG_ETOOBIG, CG_ENOMEM. */
+int cg_allpairs(const uint64_t* cells, int64_t n_cells, int32_t ell, int32_t anchors,
+                cg_edges* edges, int64_t* pairs_compared, cg_stream_t stream);
+
 /* ---- f4: path queries on G_X ----------------------
  * The graph is built so that one can "find a path in such a graph" (P:20,
  * P:57); GPU graph traversal is the paper's stated next step. */

@@ -7,9 +7,10 @@ hand-written sm_100a CUDA behind the C ABI of include/cg.h.
     res = build(vecs_uint8_cuda)      # res.cells int64 [nc, W], res.edges int32 [m, 2]
     res = build_points(points_f64_cuda, planes_f64_cuda)   # signatures on the device (f1)
 """
-from .cg import (BuildResult, CgError, Index, bfs, build, build_host, build_packed,  # noqa: F401
-                 build_points, csr, lib, signatures, version)
+from .cg import (BuildResult, CgError, Index, allpairs, bfs, build, build_host,  # noqa: F401
+                 build_packed, build_points, csr, lib, signatures, version)
 
 __all__ = ["build", "build_packed", "build_host", "build_points", "signatures", "csr", "bfs",
+           "allpairs",
            "BuildResult",
            "Index", "CgError", "lib", "version"]

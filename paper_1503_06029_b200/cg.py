@@ -107,6 +107,8 @@ def lib():
     L.cg_version.restype = ctypes.c_int
     L.cg_kernel_launches.argtypes = []
     L.cg_kernel_launches.restype = ctypes.c_int64
+    L.cg_allpairs.argtypes = [P, i64, i32, i32, ctypes.POINTER(cg_edges), ctypes.POINTER(i64), P]
+    L.cg_allpairs.restype = ctypes.c_int
     L.cg_csr.argtypes = [P, i64, i64, P, P, P]
     L.cg_csr.restype = ctypes.c_int
     L.cg_bfs.argtypes = [P, P, i64, i64, P, P, ctypes.POINTER(i32), P]
@@ -168,6 +170,7 @@ EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg
             "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
             "cg_kernel_launches", "cg_signatures", "cg_build_points", "cg_csr", "cg_bfs",
+            "cg_allpairs",
             "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
 
 
@@ -548,3 +551,21 @@ def bfs(row_ptr: torch.Tensor, col: torch.Tensor, source: int, *, want_parent=Tr
                             ctypes.c_void_p(parent.data_ptr() if parent is not None else 0),
                             ctypes.byref(ecc), ctypes.c_void_p(stream.cuda_stream)))
     return dist, parent, ecc.value
+
+
+def allpairs(cells: torch.Tensor, ell: int, anchors: int = 0, *, stream=None):
+    """cg_allpairs (f3): distance-1 pairs of a cell table int64 [n, W] (device)
+    by pair comparison (naive, or Alg. 1-2 with `anchors` anchors).  Returns
+    (edges int32 [m, 2] canonical, pairs_compared)."""
+    if cells.dim() != 2 or cells.dtype != torch.int64 or not cells.is_cuda:
+        raise CgError(CG_EINVAL, "cells must be a CUDA int64 tensor [n, W]")
+    cells = cells.contiguous()
+    n = cells.shape[0]
+    e = cg_edges()
+    cmp = ctypes.c_int64()
+    stream = stream or torch.cuda.current_stream(cells.device)
+    with torch.cuda.device(cells.device):
+        _check(lib().cg_allpairs(ctypes.c_void_p(cells.data_ptr()), n, ell, anchors,
+                                 ctypes.byref(e), ctypes.byref(cmp),
+                                 ctypes.c_void_p(stream.cuda_stream)))
+    return _wrap_edges(e, cells.device), cmp.value

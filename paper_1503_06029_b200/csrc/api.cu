@@ -877,6 +877,51 @@ int cg_build_points(const double* points, int64_t n, int32_t dim, const double* 
   return build_entry(nullptr, nullptr, n, ell, o, cells, edges, &pin);
 }
 
+int cg_allpairs(const uint64_t* cells, int64_t n_cells, int32_t ell, int32_t anchors,
+                cg_edges* edges, int64_t* pairs_compared, cg_stream_t stream) {
+  if (edges) std::memset(edges, 0, sizeof(*edges));
+  uint64_t* eout = nullptr;
+  try {
+    if (!cells || !edges) throw CgError{CG_EINVAL, "NULL argument"};
+    if (n_cells < 1) throw CgError{CG_EINVAL, "n_cells must be >= 1"};
+    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    if (anchors < 0 || anchors > allpairs_max_anchors() || anchors > n_cells)
+      throw CgError{CG_EINVAL, "anchors must be in [0, min(8, n_cells)]"};
+    check_arch();
+    check_device_ptr(cells, "cells");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int W = (ell + 63) / 64;
+    WsScope ws;
+    uint64_t cap = std::max<uint64_t>(uint64_t(n_cells) * 2, 1 << 16);
+    DevBuf<uint64_t> hits(cap, s);
+    uint64_t cmp = 0;
+    uint64_t m = launch_allpairs(cells, n_cells, W, anchors, hits.p, cap, &cmp, s);
+    if (m > cap) {
+      cap = m;
+      hits.alloc(cap, s);
+      m = launch_allpairs(cells, n_cells, W, anchors, hits.p, cap, &cmp, s);
+    }
+    DevBuf<uint64_t> alt(std::max<uint64_t>(m, 1), s);
+    uint64_t* so = hits.p;
+    if (m > 1)
+      radix_sort<uint64_t>(hits.p, alt.p, nullptr, nullptr, nullptr, false, int64_t(m), 64, &so,
+                           nullptr, s, nullptr);
+    eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
+    if (m) launch_rotate_edges(so, int64_t(m), eout, s);
+    CG_CUDA(cudaStreamSynchronize(s));
+    edges->ij = reinterpret_cast<uint32_t*>(eout);
+    edges->n_edges = int64_t(m);
+    if (pairs_compared) *pairs_compared = int64_t(cmp);
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (eout) dev_free(eout, nullptr);
+    if (edges) std::memset(edges, 0, sizeof(*edges));
+    return e.code;
+  }
+  return CG_OK;
+}
+
 int cg_csr(const uint32_t* edges, int64_t n_edges, int64_t n_cells, uint64_t* row_ptr,
            uint32_t* col, cg_stream_t stream) {
   try {

@@ -34,6 +34,13 @@ void build_csr(const uint32_t* edges, int64_t m, int64_t nv, uint64_t* row_ptr, 
 int bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t nv, int64_t src, int32_t* dist,
         int32_t* parent, cudaStream_t s);
 
+// ---------------------------------------------------------------- f3 all-pairs (allpairs.cu)
+// distance-1 pairs of a cell table by the naive / anchor method (Alg. 1-2):
+// unsorted (i << 32 | j) into out[0..cap); returns the total (rerun if > cap)
+int allpairs_max_anchors();
+uint64_t launch_allpairs(const uint64_t* cells, int64_t n, int W, int h, uint64_t* out,
+                         uint64_t cap, uint64_t* n_compared, cudaStream_t s);
+
 // ---------------------------------------------------------------- radix engine (a2, a4, a7)
 struct SortStats {
   int passes = 0;
