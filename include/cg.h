@@ -153,6 +153,21 @@ int cg_signatures(const double* points, int64_t n, int32_t dim, const double* pl
 int cg_build_points(const double* points, int64_t n, int32_t dim, const double* planes,
                     int32_t ell, const cg_opts* o, cg_cells* cells, cg_edges* edges);
 
+/* ---- f2: incremental insertion ----------------------
+ * The generator "generates (and possibly accumulates)" samples: extend
+ * the cell graph of an accumulated input (its canonical table cells =
+ * u64[n_cells][W] and edge list edges = u32[n_edges][2], device, e.g. the
+ * outputs of cg_build) by new samples vecs = uint8[n_new][ell] (device, 0/1
+ * bytes).  *cells_out / *edges_out receive the cell graph of the union of
+ * both multisets -- byte-identical to cg_build on the concatenated input --
+ * computed from the batch alone plus flip lookups into the existing table
+ * (free with cg_cells_free / cg_edges_free).  Blocks.  Errors: as cg_build
+ * (the batch), CG_EINVAL (NULL/host pointers, sizes), CG_ETOOBIG.  The
+ * existing table and edges must be canonical (unchecked). */
+int cg_insert(const uint64_t* cells, int64_t n_cells, const uint32_t* edges, int64_t n_edges,
+              int32_t ell, const uint8_t* vecs, int64_t n_new, const cg_opts* o,
+              cg_cells* cells_out, cg_edges* edges_out);
+
 /* ---- f3: the all-pairs methods ----------------------
  * Distance-1 pairs of a cell table by comparing pairs: the naive method
  * with `anchors` = 0, Alg. 1-2 with `anchors` = h in

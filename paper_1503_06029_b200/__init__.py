@@ -8,9 +8,9 @@ hand-written sm_100a CUDA behind the C ABI of include/cg.h.
     res = build_points(points_f64_cuda, planes_f64_cuda)   # signatures on the device (f1)
 """
 from .cg import (BuildResult, CgError, Index, allpairs, bfs, build, build_host,  # noqa: F401
-                 build_packed, build_points, csr, lib, signatures, version)
+                 build_packed, build_points, csr, insert, lib, signatures, version)
 
 __all__ = ["build", "build_packed", "build_host", "build_points", "signatures", "csr", "bfs",
-           "allpairs",
+           "allpairs", "insert",
            "BuildResult",
            "Index", "CgError", "lib", "version"]

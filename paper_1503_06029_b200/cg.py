@@ -107,6 +107,9 @@ def lib():
     L.cg_version.restype = ctypes.c_int
     L.cg_kernel_launches.argtypes = []
     L.cg_kernel_launches.restype = ctypes.c_int64
+    L.cg_insert.argtypes = [P, i64, P, i64, i32, P, i64, ctypes.POINTER(cg_opts),
+                            ctypes.POINTER(cg_cells), ctypes.POINTER(cg_edges)]
+    L.cg_insert.restype = ctypes.c_int
     L.cg_allpairs.argtypes = [P, i64, i32, i32, ctypes.POINTER(cg_edges), ctypes.POINTER(i64), P]
     L.cg_allpairs.restype = ctypes.c_int
     L.cg_csr.argtypes = [P, i64, i64, P, P, P]
@@ -170,7 +173,7 @@ EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg
             "cg_host_free", "cg_query", "cg_index_info", "cg_set_allocator", "cg_cells_free",
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
             "cg_kernel_launches", "cg_signatures", "cg_build_points", "cg_csr", "cg_bfs",
-            "cg_allpairs",
+            "cg_allpairs", "cg_insert",
             "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
 
 
@@ -569,3 +572,27 @@ def allpairs(cells: torch.Tensor, ell: int, anchors: int = 0, *, stream=None):
                                  ctypes.byref(e), ctypes.byref(cmp),
                                  ctypes.c_void_p(stream.cuda_stream)))
     return _wrap_edges(e, cells.device), cmp.value
+
+
+def insert(cells: torch.Tensor, edges: torch.Tensor, vecs: torch.Tensor, *, stream=None):
+    """cg_insert (f2): the cell graph of (accumulated input) + (new samples
+    vecs uint8 [n_new, ell]), from an existing canonical table int64 [n, W]
+    and edge list int32 [m, 2] (device).  Returns (cells, edges)."""
+    if cells.dim() != 2 or cells.dtype != torch.int64 or not cells.is_cuda:
+        raise CgError(CG_EINVAL, "cells must be a CUDA int64 tensor [n, W]")
+    if vecs.dim() != 2 or vecs.dtype != torch.uint8 or not vecs.is_cuda:
+        raise CgError(CG_EINVAL, "vecs must be a CUDA uint8 tensor [n_new, ell]")
+    cells, vecs = cells.contiguous(), vecs.contiguous()
+    m = edges.shape[0]
+    eptr = edges.contiguous().data_ptr() if m else 0
+    n_new, ell = vecs.shape
+    stream = stream or torch.cuda.current_stream(cells.device)
+    o, _, _ = _opts(stream, "global", True, -1, False, False)
+    c, e = cg_cells(), cg_edges()
+    with torch.cuda.device(cells.device):
+        _check(lib().cg_insert(ctypes.c_void_p(cells.data_ptr()), cells.shape[0],
+                               ctypes.c_void_p(eptr), m, ell,
+                               ctypes.c_void_p(vecs.data_ptr()), n_new, ctypes.byref(o),
+                               ctypes.byref(c), ctypes.byref(e)))
+    c.ell, c.words_per_cell = ell, (ell + 63) // 64
+    return _wrap_cells(c, cells.device), _wrap_edges(e, cells.device)

@@ -877,6 +877,76 @@ int cg_build_points(const double* points, int64_t n, int32_t dim, const double* 
   return build_entry(nullptr, nullptr, n, ell, o, cells, edges, &pin);
 }
 
+int cg_insert(const uint64_t* cells, int64_t n_cells, const uint32_t* edges, int64_t n_edges,
+              int32_t ell, const uint8_t* vecs, int64_t n_new, const cg_opts* o_in,
+              cg_cells* cells_out, cg_edges* edges_out) {
+  if (cells_out) std::memset(cells_out, 0, sizeof(*cells_out));
+  if (edges_out) std::memset(edges_out, 0, sizeof(*edges_out));
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  cg_cells bc;
+  cg_edges be;
+  std::memset(&bc, 0, sizeof(bc));
+  std::memset(&be, 0, sizeof(be));
+  uint64_t* cout = nullptr;
+  uint64_t* eout = nullptr;
+  try {
+    if (!cells || !vecs || !cells_out || !edges_out || (n_edges > 0 && !edges))
+      throw CgError{CG_EINVAL, "NULL argument"};
+    if (n_cells < 1 || n_edges < 0 || n_new < 1) throw CgError{CG_EINVAL, "n_cells >= 1, n_new >= 1"};
+    if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    check_arch();
+    check_device_ptr(cells, "cells");
+    // 1. the batch alone: sorted unique cells + its internal edges
+    cg_opts ob;
+    cg_opts_init(&ob);
+    ob.stream = o.stream;
+    const int rc = build_entry(vecs, nullptr, n_new, ell, &ob, &bc, &be);
+    if (rc != CG_OK) throw CgError{rc, std::string("batch build: ") + cg_last_error()};
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    WsScope ws;
+    // 2. an index over the existing table; self + flip lookups of the batch
+    int b = 0;
+    while (b < 28 && (uint64_t(n_cells) >> (b + 1)) >= 1) ++b;
+    const int fextra = std::min(5, 32 - b);
+    DevBuf<uint32_t> T((size_t(1) << b) + 1, s);
+    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s);
+    CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
+    build_global_index(cells, n_cells, W, b, fextra, T.p, F.p, s);
+    GlobalDict g{cells, nullptr, T.p, F.p, b, fextra, W, ell, n_cells};
+    const int64_t nb = bc.n_cells;
+    DevBuf<int32_t> self_idx(size_t(nb), s), nbr(size_t(nb) * ell, s);
+    launch_query_global(g, bc.words, nb, self_idx.p, nbr.p, s);
+    // 3-4. merge the tables, remap + extend the edges
+    int64_t nc = 0, m = 0;
+    insert_merge(cells, n_cells, edges, n_edges, bc.words, nb, be.ij, be.n_edges, self_idx.p,
+                 nbr.p, ell, &cout, &nc, &eout, &m, s);
+    CG_CUDA(cudaStreamSynchronize(s));
+    cells_out->words = cout;
+    cells_out->n_cells = nc;
+    cells_out->ell = ell;
+    cells_out->words_per_cell = W;
+    edges_out->ij = reinterpret_cast<uint32_t*>(eout);
+    edges_out->n_edges = m;
+    cout = eout = nullptr;
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    if (cout) dev_free(cout, nullptr);
+    if (eout) dev_free(eout, nullptr);
+    if (cells_out) std::memset(cells_out, 0, sizeof(*cells_out));
+    if (edges_out) std::memset(edges_out, 0, sizeof(*edges_out));
+    cg_cells_free(&bc);
+    cg_edges_free(&be);
+    return e.code;
+  }
+  cg_cells_free(&bc);
+  cg_edges_free(&be);
+  return CG_OK;
+}
+
 int cg_allpairs(const uint64_t* cells, int64_t n_cells, int32_t ell, int32_t anchors,
                 cg_edges* edges, int64_t* pairs_compared, cg_stream_t stream) {
   if (edges) std::memset(edges, 0, sizeof(*edges));
