@@ -257,6 +257,7 @@ def run_ours(args):
     f1 = run_f1(torch, cg, dev, lg) if args.f1 else None
     f4 = run_f4(torch, cg, dev) if args.f1 else None
     f3 = run_f3(torch, cg, dev) if args.f1 else None
+    f2 = run_f2(torch, cg, x, dev) if args.f1 else None
     # ---- e2e through the host-buffer C-ABI entry
     e2e = run_e2e(torch, cg, x, args, dev)
     # ---- CPU oracle baseline on a bounded sample
@@ -287,6 +288,7 @@ def run_ours(args):
         "f1_signatures": f1,
         "f4_csr_bfs": f4,
         "f3_allpairs": f3,
+        "f2_insert": f2,
     }
     print(json.dumps(out))
 
@@ -485,6 +487,30 @@ def run_f4(torch, cg, dev, ell=22):
             "bfs_ms": round(bfs_ms, 3), "bfs_levels": ecc + 1,
             "teps": round(2 * m / (bfs_ms * 1e-3), 1),
             "note": "BFS includes the canonical-parent pass and one host sync per level"}
+
+
+def run_f2(torch, cg, x, dev, batch_log2=20):
+    """Row f2 measured alone: the C5 graph of the first n - 2^20 rows (built,
+    not timed) extended by the last 2^20 rows with cg_insert; compared with
+    the full rebuild of the step."""
+    n = x.shape[0]
+    nb = 1 << batch_log2
+    old = cg.build(x[: n - nb])
+    new = x[n - nb:].contiguous()
+    cells, edges = cg.insert(old.cells, old.edges, new)
+    torch.cuda.synchronize(dev)
+    del cells, edges
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        cells, edges = cg.insert(old.cells, old.edges, new)
+        del cells, edges
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    return {"table_cells": int(old.cells.shape[0]), "batch_rows": nb, "ms": round(ms, 3),
+            "batch_rows_per_s": round(nb / (ms * 1e-3), 1)}
 
 
 def run_f3(torch, cg, dev):

@@ -917,13 +917,10 @@ int cg_insert(const uint64_t* cells, int64_t n_cells, const uint32_t* edges, int
     CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
     build_global_index(cells, n_cells, W, b, fextra, T.p, F.p, s);
     GlobalDict g{cells, nullptr, T.p, F.p, b, fextra, W, ell, n_cells};
-    const int64_t nb = bc.n_cells;
-    DevBuf<int32_t> self_idx(size_t(nb), s), nbr(size_t(nb) * ell, s);
-    launch_query_global(g, bc.words, nb, self_idx.p, nbr.p, s);
     // 3-4. merge the tables, remap + extend the edges
     int64_t nc = 0, m = 0;
-    insert_merge(cells, n_cells, edges, n_edges, bc.words, nb, be.ij, be.n_edges, self_idx.p,
-                 nbr.p, ell, &cout, &nc, &eout, &m, s);
+    insert_merge(cells, n_cells, edges, n_edges, bc.words, bc.n_cells, be.ij, be.n_edges, g, ell,
+                 &cout, &nc, &eout, &m, s);
     CG_CUDA(cudaStreamSynchronize(s));
     cells_out->words = cout;
     cells_out->n_cells = nc;

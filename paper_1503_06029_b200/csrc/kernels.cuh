@@ -42,14 +42,14 @@ uint64_t launch_allpairs(const uint64_t* cells, int64_t n, int W, int h, uint64_
                          uint64_t cap, uint64_t* n_compared, cudaStream_t s);
 
 // ---------------------------------------------------------------- f2 insertion (insert.cu)
-// V (nv sorted unique rows, canonical edges ev[mv]) + batch B (nb sorted
-// unique rows, its canonical edges eb[mb]) with self_idx[nb] (index of b in
-// V or -1) and nbr[nb][ell] (index in V of b ^ e_k or -1) -> the merged
+// V (nv sorted unique rows, canonical edges ev[mv], index g over it) +
+// batch B (nb sorted unique rows, its canonical edges eb[mb]) -> the merged
 // table and its canonical edge list (allocated with dev_alloc, u32 pairs).
+struct GlobalDict;
 void insert_merge(const uint64_t* cv_rows, int64_t nv, const uint32_t* ev, int64_t mv,
                   const uint64_t* cb_rows, int64_t nb, const uint32_t* eb, int64_t mb,
-                  const int32_t* self_idx, const int32_t* nbr, int ell, uint64_t** cells_out,
-                  int64_t* nc_out, uint64_t** edges_out, int64_t* m_out, cudaStream_t s);
+                  const GlobalDict& g, int ell, uint64_t** cells_out, int64_t* nc_out,
+                  uint64_t** edges_out, int64_t* m_out, cudaStream_t s);
 
 // ---------------------------------------------------------------- radix engine (a2, a4, a7)
 struct SortStats {

@@ -581,8 +581,12 @@ __global__ void __launch_bounds__(256)
     };
     const uint64_t t0 = tw(0);
     const int64_t x = b ? int64_t(t0 >> (64 - b)) : 0;
-    uint32_t lo = g.T[x];
-    uint32_t len = g.T[x + 1] - lo;
+    // prefix filter first: most flipped targets are absent
+    const int fb = b + g.fextra;
+    const uint64_t y = fb ? (t0 >> (64 - fb)) : 0ull;
+    const bool maybe = (g.F[y >> 5] >> (y & 31)) & 1u;
+    uint32_t lo = maybe ? g.T[x] : 0u;
+    uint32_t len = maybe ? g.T[x + 1] - lo : 0u;
     while (len > 0) {  // lower bound of t in the bucket
       const uint32_t half = len >> 1;
       const uint64_t* R = g.keys + int64_t(lo + half) * W;
@@ -599,7 +603,7 @@ __global__ void __launch_bounds__(256)
       }
     }
     int32_t found = -1;
-    if (lo < g.T[x + 1]) {
+    if (maybe && lo < g.T[x + 1]) {
       const uint64_t* R = g.keys + int64_t(lo) * W;
       bool eq = true;
       for (int w = 0; w < W && eq; ++w) eq = R[w] == tw(w);
