@@ -17,12 +17,13 @@
 //     popc(R ^ V_i) = 1.
 //   far (k < b): filter bit of the target's (b+E)-prefix, then the bucket
 //     T[x]..T[x+1] of the survivors is compared (warp-flattened rounds).
-// Output (a7): a CTA owns a contiguous tile of 256 cells, each warp 32 of
-// them; a warp's hits go to its shared-memory buffer and the warp sorts them
-// by (i, j) with a warp-synchronous bitonic network.  The tile reserves one
-// block of a scratch list with a single atomicAdd and records (count,
-// position); a scan of the counts + k_tile_copy then place the blocks in tile
-// order, so the concatenation IS the canonical edge list (no global sort).
+// Output (a7): a warp owns a contiguous tile of 32 cells (per-warp ticket;
+// the warps of a CTA never wait for each other); its hits go to its
+// shared-memory buffer and the warp orders them by (i, j).  The tile
+// reserves one block of a scratch list with a single atomicAdd and records
+// (count, position); a scan of the counts + k_tile_copy then place the
+// blocks in tile order, so the concatenation IS the canonical edge list (no
+// global sort).
 // Tiles whose hits overflow a warp buffer (dense graphs) are re-run together
 // in spill mode; their hits are sorted and dropped into their ranges.
 #include "kernels.cuh"
@@ -30,8 +31,13 @@
 namespace cgk {
 namespace {
 
-constexpr int kTileCells = 256;     // cells per tile = threads per CTA
-constexpr int kTileEdgeCap = 4096;  // shared-memory edge buffer per tile
+// Work unit ("tile"): 32 consecutive canonical cells = one warp, taken by a
+// per-warp atomic ticket; the 8 warps of a CTA never synchronise with each
+// other (no barrier stalls behind the slowest warp of a CTA).
+constexpr int kTileCells = 32;      // cells per tile = lanes per warp
+constexpr int kProbeWarps = 8;      // warps per CTA (independent)
+constexpr int kWarpEdgeCap = 512;   // shared-memory edge buffer per warp
+constexpr int kTileEdgeCap = kWarpEdgeCap;
 
 template <int WC>
 struct GRow {
@@ -55,18 +61,14 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 }
 
 template <int WC>
-__global__ void __launch_bounds__(kTileCells)
+__global__ void __launch_bounds__(32 * kProbeWarps)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                    unsigned long long* total, unsigned long long* issued,
                    uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
                    uint4* __restrict__ ovf, uint32_t* ovf_n,
                    const uint8_t* __restrict__ tile_sel) {
-  constexpr int kWarpEdgeCap = kTileEdgeCap / (kTileCells / 32);
-  __shared__ uint64_t ebuf[kTileCells / 32][kWarpEdgeCap];
-  __shared__ uint32_t s_wcnt[kTileCells / 32];
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_base;
+  __shared__ uint64_t ebuf[kProbeWarps][kWarpEdgeCap];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t lt = lanemask_lt();
   const int W = WC > 0 ? WC : g.W;
@@ -76,16 +78,13 @@ __global__ void __launch_bounds__(kTileCells)
   uint64_t* wbuf = ebuf[tid >> 5];
 
   while (true) {
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int64_t tile = s_tile;
+    uint32_t tk = 0;
+    if (lane == 0) tk = atomicAdd(ticket, 1u);
+    const int64_t tile = __shfl_sync(kFull, tk, 0);
     if (tile >= ntiles) break;
-    if (tile_sel && !tile_sel[tile]) {  // spill re-run: only the overflow tiles
-      __syncthreads();
-      continue;
-    }
+    if (tile_sel && !tile_sel[tile]) continue;  // spill re-run: only the overflow tiles
     uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
-    const int64_t i = i_lo + tile * kTileCells + tid;
+    const int64_t i = i_lo + tile * kTileCells + lane;
     const bool valid = i < i_hi;
     // ---- the cell
     const uint64_t* Vp = g.keys + (valid ? i : 0) * W;
@@ -373,17 +372,13 @@ __global__ void __launch_bounds__(kTileCells)
       }
       emit(hit, e);
     }
-    if (spill) {  // spill mode: no ordered output
-      __syncthreads();
-      continue;
-    }
-    // ---- tile output.  Each warp orders its own list: short lists (<= 64,
-    // the common case) by rank counting straight into the output, longer ones
-    // by a warp-synchronous bitonic network in the shared buffer.  The tile's
-    // block of the scratch list is reserved with one atomicAdd and every warp
-    // writes its list at its prefix inside the block.  tile_cnt/tile_pos let
-    // a scan + copy place the blocks in canonical order afterwards (a
-    // look-back would make each tile wait for its predecessor).
+    if (spill) continue;  // spill mode: no ordered output
+    // ---- tile output.  The warp orders its own list: short lists (<= 32,
+    // the common case) by rank counting on 32-bit keys, <= 64 on 64-bit keys,
+    // longer ones by a warp-synchronous bitonic network in the buffer; one
+    // atomicAdd reserves the tile's block of the scratch list.  tile_cnt /
+    // tile_pos let a scan + copy place the blocks in canonical order
+    // afterwards (a look-back would make each tile wait for its predecessor).
     const uint32_t wn = min(wfill, uint32_t(kWarpEdgeCap));
     __syncwarp();
     if (wn > 64) {
@@ -408,33 +403,23 @@ __global__ void __launch_bounds__(kTileCells)
         }
       }
     }
-    if (lane == 0) s_wcnt[tid >> 5] = wfill;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t cnt = 0;
-      bool over = false;
-      for (int w = 0; w < kTileCells / 32; ++w) {
-        const uint32_t c = s_wcnt[w];
-        s_wcnt[w] = cnt;
-        cnt += c;
-        over |= c > uint32_t(kWarpEdgeCap);
-      }
-      status[tile] = cnt;  // tile_cnt
-      if (over) {
-        // rare: hits beyond a warp buffer were dropped; the host re-runs this
-        // tile in spill mode and writes its range directly
+    uint32_t bs = 0;
+    if (lane == 0) {
+      status[tile] = wfill;  // tile_cnt
+      if (wfill > uint32_t(kWarpEdgeCap)) {
+        // rare: hits beyond the warp buffer were dropped; the host re-runs
+        // this tile in spill mode and writes its range directly
         const uint32_t k = atomicAdd(ovf_n, 1u);
-        ovf[k] = make_uint4(uint32_t(tile), 0u, cnt, 0u);
-        s_base = 0xffffffffu;
-      } else {
-        s_base = uint32_t(atomicAdd(total, (unsigned long long)cnt));
+        ovf[k] = make_uint4(uint32_t(tile), 0u, wfill, 0u);
+        bs = 0xffffffffu;
+      } else if (wfill) {
+        bs = uint32_t(atomicAdd(total, (unsigned long long)wfill));
       }
-      status[ntiles + tile] = s_base;  // tile_pos in the scratch list
+      status[ntiles + tile] = bs;  // tile_pos in the scratch list
     }
-    __syncthreads();
-    const uint32_t base = s_base;
+    const uint32_t base = __shfl_sync(kFull, bs, 0);
     if (base != 0xffffffffu && wn > 0) {
-      const uint64_t wpos = uint64_t(base) + s_wcnt[tid >> 5];
+      const uint64_t wpos = uint64_t(base);
       if (wn <= 32 && g.n_cells <= (int64_t(1) << 27)) {
         // one hit per lane: rank on a 32-bit key (source lane << 27 | j),
         // the keys exchanged by shuffles
@@ -463,7 +448,7 @@ __global__ void __launch_bounds__(kTileCells)
           if (wpos + q < cap) out[wpos + q] = wbuf[q];  // sorted (i << 32 | j) keys
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) my_issued += __shfl_xor_sync(kFull, my_issued, o);
@@ -486,11 +471,11 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
                          unsigned long long* spill_n, cudaStream_t s, const uint8_t* tile_sel) {
   const int64_t ntiles = (i_hi - i_lo + kTileCells - 1) / kTileCells;
   if (ntiles <= 0) return;
-  const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms()) * 8));
+  const int grid = int(std::min<int64_t>((ntiles + kProbeWarps - 1) / kProbeWarps, int64_t(num_sms()) * 8));
   switch (g.W) {
-    case 1: k_probe_global<1><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    case 2: k_probe_global<2><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    default: k_probe_global<0><<<grid, kTileCells, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 1: k_probe_global<1><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 2: k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    default: k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
   }
   CG_LAUNCH_CHECK();
 }
@@ -531,21 +516,42 @@ void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const u
   CG_LAUNCH_CHECK();
 }
 
-// one warp per tile: its sorted block of (i << 32 | j) keys from the scratch
-// list to the tile's canonical offset, as (i, j) u32 pairs
-__global__ void k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t* __restrict__ off,
-                            const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cntv,
-                            int64_t ntiles, uint64_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t t = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nw) {
-    const uint32_t c = cntv[t];
-    if (pos[t] == 0xffffffffu) continue;  // overflow tile: written by the spill path
-    const uint64_t* src = scratch + pos[t];
-    uint64_t* dst = out + off[t];
-    for (uint32_t q = lane; q < c; q += 32) {
-      const uint64_t k = src[q];
-      dst[q] = (k >> 32) | (k << 32);
+// Tile blocks -> canonical positions.  A CTA takes 256 consecutive tiles:
+// their destination ranges are contiguous (off = exclusive scan of the
+// counts), so the CTA flattens them -- thread per destination element, its
+// tile found by a binary search over the tiles' prefix in shared memory --
+// and writes one contiguous run as (i, j) u32 pairs.  Overflow tiles
+// (pos = 0xffffffff) are written by the spill path and skipped here.
+constexpr int kCopyTiles = 256;
+
+__global__ void __launch_bounds__(256)
+    k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t* __restrict__ off,
+                const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cntv, int64_t ntiles,
+                uint64_t* __restrict__ out) {
+  __shared__ uint32_t s_pre[kCopyTiles + 1], s_pos[kCopyTiles];
+  for (int64_t t0 = int64_t(blockIdx.x) * kCopyTiles; t0 < ntiles;
+       t0 += int64_t(gridDim.x) * kCopyTiles) {
+    const int nt = int(ntiles - t0 < kCopyTiles ? ntiles - t0 : int64_t(kCopyTiles));
+    __syncthreads();
+    const uint32_t base = off[t0];
+    for (int q = threadIdx.x; q < nt; q += blockDim.x) {
+      s_pre[q] = off[t0 + q] - base;
+      s_pos[q] = pos[t0 + q];
+    }
+    if (threadIdx.x == 0) s_pre[nt] = off[t0 + nt - 1] - base + cntv[t0 + nt - 1];
+    __syncthreads();
+    const uint32_t E = s_pre[nt];
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+      int lo = 0, hi = nt - 1;  // last tile with s_pre <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pre[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint32_t p = s_pos[lo];
+      if (p == 0xffffffffu) continue;
+      const uint64_t k = scratch[p + (e - s_pre[lo])];
+      out[uint64_t(base) + e] = (k >> 32) | (k << 32);
     }
   }
 }
@@ -553,7 +559,7 @@ __global__ void k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t
 void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s) {
   if (ntiles <= 0) return;
-  const int64_t blocks = std::min<int64_t>((ntiles * 32 + 255) / 256, int64_t(num_sms()) * 16);
+  const int64_t blocks = std::min<int64_t>((ntiles + kCopyTiles - 1) / kCopyTiles, int64_t(num_sms()) * 8);
   k_tile_copy<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(scratch, off, pos, cnt, ntiles, out);
   CG_LAUNCH_CHECK();
 }
