@@ -152,7 +152,10 @@ def _torch_alloc(size, stream, ctx):
 
 def _torch_free(ptr, stream, ctx):
     if ptr:
-        torch._C._cuda_cudaCachingAllocator_raw_delete(int(ptr))
+        try:
+            torch._C._cuda_cudaCachingAllocator_raw_delete(int(ptr))
+        except Exception:  # interpreter shutdown: torch is already torn down
+            pass
 
 
 _ALLOC_CB = _ALLOC_T(_torch_alloc)

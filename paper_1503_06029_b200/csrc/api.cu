@@ -1315,21 +1315,31 @@ int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, 
     tm.start(o.stats != nullptr, s);
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-    // concatenate the runs (each sorted and unique; duplicates across runs
-    // are removed by the global sort + dedupe below)
-    DevBuf<uint64_t> keys(size_t(total) * W, s);
-    int64_t at = 0;
-    for (int g = 0; g < G; ++g) {
-      if (counts[g])
-        CG_CUDA(cudaMemcpyAsync(keys.p + at * W, runs + int64_t(g) * stride * W,
-                                size_t(counts[g]) * W * 8, cudaMemcpyDeviceToDevice, s));
-      at += counts[g];
+    // the runs are sorted: on the MSD path they are gathered straight into
+    // the global top-B-bit buckets (no global radix passes; the bucket pass
+    // sorts each bucket's run segments and removes cross-run duplicates);
+    // otherwise concatenated and sorted in full
+    const bool msd = W <= 2 && o.sort_kind != 1;
+    DevBuf<uint64_t> keys(size_t(total) * W, s, msd ? Mem::Persist : Mem::Scratch);
+    const int B = msd_prefix_bits(total);
+    DevBuf<uint32_t> boff(msd ? (size_t(1) << B) + 1 : 1, s);
+    if (msd) {
+      gather_runs_by_prefix(runs, counts, G, stride, W, B, keys.p, boff.p, s);
+    } else {
+      int64_t at = 0;
+      for (int g = 0; g < G; ++g) {
+        if (counts[g])
+          CG_CUDA(cudaMemcpyAsync(keys.p + at * W, runs + int64_t(g) * stride * W,
+                                  size_t(counts[g]) * W * 8, cudaMemcpyDeviceToDevice, s));
+        at += counts[g];
+      }
     }
     tm.mark();
     Shard sh;
     sh.rank = rank;
     sh.world = G;
-    build_from_keys(keys, total, ell, o, flags.p, tm, o.stats, &b, sh);
+    build_from_keys(keys, total, ell, o, flags.p, tm, o.stats, &b, sh, nullptr,
+                    msd ? boff.p : nullptr, B);
     fill_stats(tm, total, o.stats);
     store_counters(o.stats);
   } catch (const CgError& e) {

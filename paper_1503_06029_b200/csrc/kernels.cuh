@@ -78,6 +78,12 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
 // bucket-ordered and the caller must finish with a full sort.
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
                    cudaStream_t s, SortStats* st, const uint32_t* top_hist = nullptr);
+// G sorted runs (rows u64[G][stride][W], stride in rows, W <= 2, counts on the host) ->
+// their rows grouped by the top B bits into out (u64[total][W]; each bucket
+// holds its runs' segments one after the other) and off[2^B + 1] = bucket
+// starts -- the input of sort_unique_msd(..., pre_off = off, pre_B = B).
+void gather_runs_by_prefix(const uint64_t* runs, const int64_t* counts, int G, int64_t stride,
+                           int W, int B, uint64_t* out, uint32_t* off, cudaStream_t s);
 // prefix bits B (8, 16 or 24) the MSD path uses for n keys; digit dlo = (64-B)/8
 int msd_prefix_bits(int64_t n);
 // MSD sort with dedupe fused into the bucket pass: the sorted unique cells

@@ -1219,6 +1219,89 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
   return false;
 }
 
+// ---------------------------------------------------------------- merge of sorted runs
+// (the distributed merge): G sorted runs are already
+// ordered inside every top-B-bit bucket, so instead of re-sorting their
+// concatenation the rows are gathered straight into the global buckets --
+// per-run bucket bounds, global bucket offsets, one copy -- and the bucket
+// pass (with its dedupe) does the rest.
+namespace {
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+__global__ void k_run_bucket_base(const uint32_t* __restrict__ offs, int G, int64_t nbk,
+                                  uint32_t* __restrict__ size) {
+  for (int64_t bk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; bk < nbk;
+       bk += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t t = 0;
+    for (int g = 0; g < G; ++g) t += offs[g * (nbk + 1) + bk + 1] - offs[g * (nbk + 1) + bk];
+    size[bk] = t;
+  }
+}
+
+// base[g][bk] = start of run g's segment of bucket bk in the gathered array
+__global__ void k_run_segment_base(const uint32_t* __restrict__ offs, const uint32_t* __restrict__ off,
+                                   int G, int64_t nbk, uint32_t* __restrict__ base) {
+  for (int64_t bk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; bk < nbk;
+       bk += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t t = off[bk];
+    for (int g = 0; g < G; ++g) {
+      base[g * nbk + bk] = t;
+      t += offs[g * (nbk + 1) + bk + 1] - offs[g * (nbk + 1) + bk];
+    }
+  }
+}
+
+template <class K>
+__global__ void k_run_gather(const K* __restrict__ run, int64_t n, int B,
+                             const uint32_t* __restrict__ roff, const uint32_t* __restrict__ base,
+                             K* __restrict__ out) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const K k = run[e];
+    const int64_t bk = int64_t(KT<K>::top(k) >> (64 - B));
+    out[base[bk] + (e - roff[bk])] = k;
+  }
+}
+
+template <class K>
+void gather_runs_impl(const K* runs, const int64_t* counts, int G, int64_t stride, int B, K* out,
+                      uint32_t* off, cudaStream_t s) {
+  const int64_t nbk = int64_t(1) << B;
+  DevBuf<uint32_t> offs(size_t(G) * (nbk + 1), s), base(size_t(G) * nbk, s);
+  CG_CUDA(cudaMemsetAsync(offs.p, 0, offs.n * 4, s));
+  for (int g = 0; g < G; ++g) {
+    if (counts[g] <= 0) continue;
+    k_bucket_bounds<K><<<grid_for(counts[g], 256, 16), 256, 0, s>>>(runs + g * stride, counts[g], B,
+                                                                   offs.p + g * (nbk + 1));
+    CG_LAUNCH_CHECK();
+  }
+  k_run_bucket_base<<<grid_for(nbk, 256, 16), 256, 0, s>>>(offs.p, G, nbk, off);
+  CG_LAUNCH_CHECK();
+  launch_scan_u32(off, nbk, s);  // exclusive: bucket starts
+  int64_t total = 0;
+  for (int g = 0; g < G; ++g) total += counts[g];
+  k_set_u32<<<1, 1, 0, s>>>(off + nbk, uint32_t(total));
+  CG_LAUNCH_CHECK();
+  k_run_segment_base<<<grid_for(nbk, 256, 16), 256, 0, s>>>(offs.p, off, G, nbk, base.p);
+  CG_LAUNCH_CHECK();
+  for (int g = 0; g < G; ++g) {
+    if (counts[g] <= 0) continue;
+    k_run_gather<K><<<grid_for(counts[g], 256, 16), 256, 0, s>>>(
+        runs + g * stride, counts[g], B, offs.p + g * (nbk + 1), base.p + g * nbk, out);
+    CG_LAUNCH_CHECK();
+  }
+}
+}  // namespace
+
+void gather_runs_by_prefix(const uint64_t* runs, const int64_t* counts, int G, int64_t stride,
+                           int W, int B, uint64_t* out, uint32_t* off, cudaStream_t s) {
+  if (W == 1)
+    gather_runs_impl<uint64_t>(runs, counts, G, stride, B, out, off, s);
+  else
+    gather_runs_impl<ulonglong2>(reinterpret_cast<const ulonglong2*>(runs), counts, G, stride, B,
+                                 reinterpret_cast<ulonglong2*>(out), off, s);
+}
+
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
                    cudaStream_t s, SortStats* st, const uint32_t* top_hist) {
   if (W == 1) {
