@@ -346,7 +346,8 @@ struct Shard {
 static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
                             uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out,
                             const Shard& sh = Shard(), const uint32_t* top_hist = nullptr,
-                            const uint32_t* pre_off = nullptr, int pre_B = 0) {
+                            const uint32_t* pre_off = nullptr, int pre_B = 0,
+                            const uint32_t* tile_hist = nullptr) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
@@ -365,7 +366,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     uint64_t* ko = nullptr;
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
-    done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off, pre_B)
+    done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off, pre_B,
+                                   tile_hist)
                  : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     sorted = ko;
     if (done && fused) {
@@ -789,6 +791,9 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     const int B = msd_prefix_bits(n);
     const int dlo = (64 - B) / 8;
     DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
+    // the pack kernel's per-tile counts of the first sort pass's digit (that
+    // pass then needs no look-back)
+    DevBuf<uint32_t> tile_hist(msd ? size_t((n + msd_tile_rows(W) - 1) / msd_tile_rows(W)) * 256 : 1, s);
     // scatter pack (CG_SCATTER=1): rows go straight into their top-B-bit
     // bucket via per-bucket atomic cursors, so the sort needs no global radix
     // pass.  Measured at C5: sort 4.25 -> 2.33 ms but pack 1.53 -> 6.5 ms
@@ -805,7 +810,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
       launch_pack_scatter(vecs, n, ell, B, boff.p, bcur.p, keys.p, flags.p, s);
     } else if (vecs) {
       if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
-      launch_pack(vecs, n, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo);
+      launch_pack(vecs, n, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo,
+                  msd ? tile_hist.p : nullptr, msd_tile_rows(W));
     } else if (pin) {
       if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
       launch_signatures(pin->points, n, pin->dim, pin->planes, ell, keys.p, flags.p, s,
@@ -817,7 +823,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     tm.mark();  // 1: pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(),
                     ((vecs || pin) && msd && !scatter) ? top_hist.p : nullptr,
-                    scatter ? boff.p : nullptr, B);
+                    scatter ? boff.p : nullptr, B,
+                    (vecs && msd && !scatter) ? tile_hist.p : nullptr);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
   } catch (const CgError& e) {

@@ -9,8 +9,11 @@ namespace cgk {
 // uint8[n][ell] (0/1 bytes) -> u64[n][W] MSB-first; *err |= 1 on a byte > 1.
 // hist (optional, zeroed, u32[(8 - dlo) * 256]): counts of the 8-bit digits
 // dlo..7 of word 0, for the MSD sort (dlo in 5..7).
+// tile_hist (optional, with hist): u32[ceil(n / tile_rows)][256] counts of
+// digit dlo per tile of tile_rows rows (the first one-sweep pass's tiles).
 void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
-                 cudaStream_t s, uint32_t* hist = nullptr, int dlo = 8);
+                 cudaStream_t s, uint32_t* hist = nullptr, int dlo = 8,
+                 uint32_t* tile_hist = nullptr, int tile_rows = 0);
 // packed input: copy + check pad bits (err |= 1 if a pad bit is set)
 void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s);
 
@@ -92,9 +95,14 @@ int msd_prefix_bits(int64_t n);
 // sort + dedupe instead).
 // pre_off (device, 2^pre_B + 1 entries): keys already grouped by their top
 // pre_B bits (launch_pack_scatter) -> no global radix pass.
+// tile_hist (optional): per-tile counts of the first pass's digit from the
+// pack kernel, tiles of msd_tile_rows(W) rows: the first pass skips its
+// look-back.
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
-                     const uint32_t* pre_off = nullptr, int pre_B = 0);
+                     const uint32_t* pre_off = nullptr, int pre_B = 0,
+                     const uint32_t* tile_hist = nullptr);
+int msd_tile_rows(int W);
 // MSD scatter pack (W <= 2, ell % 16 == 0, 16-byte aligned rows): histogram of
 // the top B bits from the first 16 bytes of each row, then pack straight into
 // the prefix buckets (start = exclusive scan of the histogram, cursor zeroed).

@@ -28,12 +28,18 @@ constexpr uint64_t kHi7 = 0xfefefefefefefefeull;
 // (the top bits the MSD sort partitions on), run-length accumulated per
 // thread so constant digits do not serialise shared-memory atomics; this
 // saves the sort's separate histogram read of the keys.
+//
+// With tile_hist (the MSD sort's first one-sweep pass then needs no
+// look-back): the CTA walks whole tiles of tile_rows rows (the sort's tiles)
+// and also writes each tile's count of digit dlo, tile_hist[t][256].
 template <int VEC>
 __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, int64_t n,
                                               int ell, int W, uint64_t* __restrict__ keys,
                                               uint32_t* __restrict__ err,
-                                              uint32_t* __restrict__ hist, int dlo) {
+                                              uint32_t* __restrict__ hist, int dlo,
+                                              uint32_t* __restrict__ tile_hist, int tile_rows) {
   __shared__ uint32_t sh[3][256];
+  __shared__ uint32_t st[256];
   const int nd = hist ? 8 - dlo : 0;
   if (hist) {
     for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
@@ -42,8 +48,18 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
   uint32_t last[3] = {0, 0, 0}, cnt[3] = {0, 0, 0};
   const int64_t total = n * W;
   uint64_t bad = 0;
-  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
-       g += int64_t(gridDim.x) * blockDim.x) {
+  const int64_t ntiles = tile_hist ? (n + tile_rows - 1) / tile_rows : 1;
+  const int64_t twords = tile_hist ? int64_t(tile_rows) * W : total;
+  // without tile_hist: one "tile" = all words, grid-strided over all CTAs
+  for (int64_t t = tile_hist ? blockIdx.x : 0; t < ntiles; t += tile_hist ? gridDim.x : 1) {
+  if (tile_hist) {
+    st[threadIdx.x] = 0u;
+    __syncthreads();
+  }
+  const int64_t g0 = t * twords, gend = min(total, g0 + twords);
+  const int64_t gstep = tile_hist ? int64_t(blockDim.x) : int64_t(gridDim.x) * blockDim.x;
+  for (int64_t g = g0 + (tile_hist ? 0 : int64_t(blockIdx.x) * blockDim.x) + threadIdx.x; g < gend;
+       g += gstep) {
     const int64_t r = g / W;
     const int w = int(g - r * W);
     const int len = min(64, ell - 64 * w);
@@ -87,6 +103,7 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
       }
     }
     keys[g] = word;
+    if (tile_hist && w == 0) atomicAdd(&st[uint32_t(word >> (8 * dlo)) & 255u], 1u);
     if (nd && w == 0) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -101,6 +118,12 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
         }
       }
     }
+  }
+  if (tile_hist) {
+    __syncthreads();
+    tile_hist[t * 256 + threadIdx.x] = st[threadIdx.x];
+    __syncthreads();
+  }
   }
   if (bad) atomicOr(err, 1u);
   if (hist) {
@@ -186,21 +209,22 @@ __global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W
 }  // namespace
 
 void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
-                 cudaStream_t s, uint32_t* hist, int dlo) {
+                 cudaStream_t s, uint32_t* hist, int dlo, uint32_t* tile_hist, int tile_rows) {
   const int W = (ell + 63) / 64;
   const int64_t total = n * W;
   const int threads = 256;
-  int64_t blocks = (total + threads - 1) / threads;
+  int64_t blocks = tile_hist ? (n + tile_rows - 1) / tile_rows : (total + threads - 1) / threads;
   blocks = std::min<int64_t>(blocks, int64_t(num_sms()) * 8);
   if (blocks < 1) blocks = 1;
   if (hist && (dlo < 5 || dlo > 7)) hist = nullptr;  // at most 3 top digits
+  if (!hist) tile_hist = nullptr;
   const uintptr_t a = reinterpret_cast<uintptr_t>(vecs);
   if (ell % 16 == 0 && a % 16 == 0) {
-    k_pack<16><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
+    k_pack<16><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
   } else if (ell % 8 == 0 && a % 8 == 0) {
-    k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
+    k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
   } else {
-    k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo);
+    k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
   }
   CG_LAUNCH_CHECK();
 }

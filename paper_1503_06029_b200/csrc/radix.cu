@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(kSortThreads, 3)
     k_onesweep(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                uint32_t* __restrict__ vout, int64_t n, int shift,
                const uint32_t* __restrict__ bucket_base, uint64_t* status,
-               uint32_t* tile_counter, uint32_t epoch) {
+               uint32_t* tile_counter, uint32_t epoch,
+               const uint32_t* __restrict__ tile_pre) {
   constexpr int IPT = TileCfg<K, V>::IPT;
   constexpr int TILE = TileCfg<K, V>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -170,7 +171,10 @@ __global__ void __launch_bounds__(kSortThreads, 3)
     wcnt[ww][tid] = total;
     total += c;
   }
-  const uint32_t excl_tiles = lookback(status, tile, kRadix, tid, total, epoch);
+  // earlier tiles' count of digit tid: precomputed (the pack kernel counted
+  // this pass's digit per tile) or by decoupled look-back
+  const uint32_t excl_tiles = tile_pre ? tile_pre[tile * kRadix + tid]
+                                       : lookback(status, tile, kRadix, tid, total, epoch);
   uint32_t tile_n_u;
   const uint32_t dex = block_excl_scan(total, s_scan, &tile_n_u);
   s_dexcl[tid] = dex;
@@ -970,12 +974,41 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
   CG_LAUNCH_CHECK();
 }
 
+// tile_cnt[t][256] (per-tile digit counts) -> tile_pre[t][256] = exclusive
+// prefix over tiles, per digit: chunk sums, a scan of the chunk sums, fill.
+constexpr int kPreChunk = 64;
+__global__ void k_tile_chunk_sum(const uint32_t* __restrict__ cnt, int64_t nt,
+                                 uint32_t* __restrict__ csum) {
+  const int64_t c = blockIdx.x, d = threadIdx.x;
+  uint32_t t = 0;
+  for (int64_t q = c * kPreChunk; q < min(nt, (c + 1) * kPreChunk); ++q) t += cnt[q * kRadix + d];
+  csum[c * kRadix + d] = t;
+}
+__global__ void k_tile_chunk_scan(uint32_t* __restrict__ csum, int64_t nc) {
+  const int d = threadIdx.x;
+  uint32_t run = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    const uint32_t v = csum[c * kRadix + d];
+    csum[c * kRadix + d] = run;
+    run += v;
+  }
+}
+__global__ void k_tile_fill(const uint32_t* __restrict__ cnt, int64_t nt,
+                            const uint32_t* __restrict__ cpre, uint32_t* __restrict__ pre) {
+  const int64_t c = blockIdx.x, d = threadIdx.x;
+  uint32_t run = cpre[c * kRadix + d];
+  for (int64_t q = c * kPreChunk; q < min(nt, (c + 1) * kPreChunk); ++q) {
+    pre[q * kRadix + d] = run;
+    run += cnt[q * kRadix + d];
+  }
+}
+
 // Generic pass driver over digits [dlo, dhi) of the top word.
 template <class K>
 void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
                   uint32_t* vals_alt, bool want_vals, int64_t n, int dlo, int dhi, K** keys_out,
                   uint32_t** vals_out, cudaStream_t s, SortStats* st,
-                  const uint32_t* dev_hist = nullptr) {
+                  const uint32_t* dev_hist = nullptr, const uint32_t* tile_hist = nullptr) {
   *keys_out = keys;
   if (vals_out) *vals_out = nullptr;
   auto identity_or_input = [&]() {
@@ -1043,6 +1076,19 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
   DevBuf<uint32_t> counters(size_t(P), s);
   CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint64_t), s));
   CG_CUDA(cudaMemsetAsync(counters.p, 0, counters.n * sizeof(uint32_t), s));
+  // the first pass needs no look-back when the pack kernel counted its digit
+  // per tile (same tiles: keys-only passes of the pack output)
+  DevBuf<uint32_t> tpre(tile_hist && !V && digits[0] == dlo ? size_t(tiles) * kRadix : 0, s);
+  if (tpre.n) {
+    const int64_t nch = (tiles + kPreChunk - 1) / kPreChunk;
+    DevBuf<uint32_t> csum(size_t(nch) * kRadix, s);
+    k_tile_chunk_sum<<<unsigned(nch), kRadix, 0, s>>>(tile_hist, tiles, csum.p);
+    CG_LAUNCH_CHECK();
+    k_tile_chunk_scan<<<1, kRadix, 0, s>>>(csum.p, nch);
+    CG_LAUNCH_CHECK();
+    k_tile_fill<<<unsigned(nch), kRadix, 0, s>>>(tile_hist, tiles, csum.p, tpre.p);
+    CG_LAUNCH_CHECK();
+  }
   K* ck = keys;
   K* ak = keys_alt;
   const uint32_t* cv = vals_in;
@@ -1053,11 +1099,11 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
     if (V) {
       k_onesweep<K, true><<<unsigned(tiles), kSortThreads, TileCfg<K, true>::SMEM, s>>>(
           ck, ak, cv, av, n, shift, dbases.p + p * kRadix, status.p, counters.p + p,
-          uint32_t(p + 1));
+          uint32_t(p + 1), nullptr);
     } else {
       k_onesweep<K, false><<<unsigned(tiles), kSortThreads, TileCfg<K, false>::SMEM, s>>>(
           ck, ak, nullptr, nullptr, n, shift, dbases.p + p * kRadix, status.p, counters.p + p,
-          uint32_t(p + 1));
+          uint32_t(p + 1), (p == 0 && tpre.n) ? tpre.p : nullptr);
     }
     CG_LAUNCH_CHECK();
     std::swap(ck, ak);
@@ -1156,14 +1202,14 @@ __global__ void k_compact_buckets(const K* __restrict__ src, const uint32_t* __r
 template <class K>
 bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaStream_t s,
                       SortStats* st, const uint32_t* top_hist, const uint32_t* pre_off = nullptr,
-                      int pre_B = 0) {
+                      int pre_B = 0, const uint32_t* tile_hist = nullptr) {
   // pre_off: keys are already grouped by their top pre_B bits (scatter pack),
   // pre_off[b] = first row of bucket b -- no global pass needed
   const int B = pre_off ? pre_B : msd_prefix_bits(n);
   K* ko = keys;
   if (!pre_off)
     radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
-                    s, st, top_hist);
+                    s, st, top_hist, tile_hist);
   const int64_t nb = int64_t(1) << B;
   DevBuf<uint32_t> offb(pre_off ? 1 : size_t(nb) + 1, s);
   const uint32_t* offp = pre_off ? pre_off : offb.p;
@@ -1198,13 +1244,17 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
 }
 }  // namespace
 
+int msd_tile_rows(int W) {
+  return W == 1 ? TileCfg<uint64_t, false>::TILE : TileCfg<ulonglong2, false>::TILE;
+}
+
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
-                     const uint32_t* pre_off, int pre_B) {
+                     const uint32_t* pre_off, int pre_B, const uint32_t* tile_hist) {
   if (W == 1) {
     uint64_t* o = nullptr;
     const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist, pre_off,
-                                               pre_B);
+                                               pre_B, tile_hist);
     *cells = o;
     return ok;
   }
@@ -1212,7 +1262,7 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
     ulonglong2* o = nullptr;
     const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
                                                  reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
-                                                 st, top_hist, pre_off, pre_B);
+                                                 st, top_hist, pre_off, pre_B, tile_hist);
     *cells = reinterpret_cast<uint64_t*>(o);
     return ok;
   }
