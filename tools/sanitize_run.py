@@ -23,4 +23,17 @@ for x in cases:
             r.index.query(q)
         torch.cuda.synchronize()
         del r
-print("sanitize run ok")
+print("sanitize build paths ok")
+
+# rows f1-f4 on small inputs
+P, A = synth.arrangement_points(3, 8, 2)
+res = cg.build_points(torch.from_numpy(P).cuda(), torch.from_numpy(A).cuda())
+w = cg.signatures(torch.from_numpy(P).cuda(), torch.from_numpy(A).cuda())
+rp, col = cg.csr(res.edges, res.cells.shape[0])
+cg.bfs(rp, col, 0)
+c1 = synth.config("C1")["bytes"]
+r1 = cg.build(torch.from_numpy(c1[:600]).cuda())
+cg.insert(r1.cells, r1.edges, torch.from_numpy(c1[600:]).cuda())
+cg.allpairs(r1.cells, 32, 3)
+torch.cuda.synchronize()
+print("sanitize f-rows ok")
