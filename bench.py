@@ -258,6 +258,7 @@ def run_ours(args):
     f4 = run_f4(torch, cg, dev) if args.f1 else None
     f3 = run_f3(torch, cg, dev) if args.f1 else None
     f2 = run_f2(torch, cg, x, dev) if args.f1 else None
+    qb = run_query(torch, cg, x, dev) if args.f1 else None
     # ---- e2e through the host-buffer C-ABI entry
     e2e = run_e2e(torch, cg, x, args, dev)
     # ---- CPU oracle baseline on a bounded sample
@@ -289,6 +290,7 @@ def run_ours(args):
         "f4_csr_bfs": f4,
         "f3_allpairs": f3,
         "f2_insert": f2,
+        "b_query": qb,
     }
     print(json.dumps(out))
 
@@ -487,6 +489,33 @@ def run_f4(torch, cg, dev, ell=22):
             "bfs_ms": round(bfs_ms, 3), "bfs_levels": ecc + 1,
             "teps": round(2 * m / (bfs_ms * 1e-3), 1),
             "note": "BFS includes the canonical-parent pass and one host sync per level"}
+
+
+def run_query(torch, cg, x, dev, nq_log2=20):
+    """Row b measured alone: cg_query (self + ell single-bit-flip lookups per
+    query) of 2^20 random cells of the C5 table against its index
+    (asynchronous, device-resident queries)."""
+    res = cg.build(x, want_index=True)
+    n = res.cells.shape[0]
+    g = torch.Generator(device=dev).manual_seed(9)
+    q = res.cells[torch.randint(0, n, (1 << nq_log2,), device=dev, generator=g)].contiguous()
+    self_idx, nbr = res.index.query(q)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        self_idx, nbr = res.index.query(q)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    nq = q.shape[0]
+    ell = res.index.ell
+    return {"table_cells": n, "queries": nq, "ms": round(ms, 3),
+            "queries_per_s": round(nq / (ms * 1e-3), 1),
+            "lookups_per_s": round(nq * (ell + 1) / (ms * 1e-3), 1),
+            "found_self": int((self_idx >= 0).sum().item()),
+            "found_neighbours": int((nbr >= 0).sum().item())}
 
 
 def run_f2(torch, cg, x, dev, batch_log2=20):
