@@ -381,22 +381,32 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       std::swap(keys.scratch, alt.scratch);
     }
   }
+  int64_t ns = n;  // rows the full sort below orders
   if (!done) {
+    if (msd && n >= (int64_t(1) << 18) && !std::getenv("CG_NO_HASH_DEDUPE")) {
+      // a bucket overflowed: skewed data, typically few distinct cells and
+      // heavy duplication -- drop the copies by hashing first, then
+      // sort only the distinct rows
+      ns = hash_unique_rows(keys.p, n, W, alt.p, s);
+      std::swap(keys.p, alt.p);
+      std::swap(keys.arena, alt.arena);
+      std::swap(keys.scratch, alt.scratch);
+    }
     if (W == 1) {
       uint64_t* ko = nullptr;
-      radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, n, 64, &ko, nullptr,
+      radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, ns, 64, &ko, nullptr,
                            s, &sst);
       sorted = ko;
     } else {
-      sort_rows_multiword(keys.p, n, W, alt.p, s, &sst);
+      sort_rows_multiword(keys.p, ns, W, alt.p, s, &sst);
       sorted = alt.p;
     }
   }
   tm.mark();  // 2: sort
   if (nc < 0) {
     // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
-    cellbuf.alloc(size_t(n) * W, s, Mem::Persist);
-    launch_dedupe(sorted, n, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+    cellbuf.alloc(size_t(ns) * W, s, Mem::Persist);
+    launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
   } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the
     // layered dictionary (the global-dictionary probe derives lcp itself)

@@ -128,7 +128,78 @@ __global__ void k_cell_meta(const uint64_t* __restrict__ cells, int64_t nc, int 
   }
 }
 
+// ---- hash dedupe for skewed inputs (the MSD buckets overflowed: few
+// distinct rows, heavy duplication): every row is inserted into an
+// open-addressed table of row indices (load <= 1/2); the first row of each
+// distinct value to claim a slot is kept, later equal rows are dropped.  The
+// kept rows are then compacted (flags + scan) and only they are sorted.
+__device__ __forceinline__ uint64_t row_hash64(const uint64_t* r, int W) {
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  for (int w = 0; w < W; ++w) {
+    h ^= r[w] + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+  }
+  return h;
+}
+
+__global__ void k_hash_unique(const uint64_t* __restrict__ rows, int64_t n, int W,
+                              uint32_t* __restrict__ table, uint64_t mask,
+                              uint32_t* __restrict__ flag) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t* r = rows + i * W;
+    uint64_t h = row_hash64(r, W) & mask;
+    uint32_t keep = 0;
+    while (true) {
+      uint32_t v = table[h];
+      if (v == 0xffffffffu) {
+        v = atomicCAS(&table[h], 0xffffffffu, uint32_t(i));
+        if (v == 0xffffffffu) {
+          keep = 1;
+          break;
+        }
+      }
+      const uint64_t* o = rows + int64_t(v) * W;
+      bool eq = true;
+      for (int w = 0; w < W && eq; ++w) eq = o[w] == r[w];
+      if (eq) break;  // a copy of a row already kept
+      h = (h + 1) & mask;
+    }
+    flag[i] = keep;
+  }
+}
+
+__global__ void k_hash_compact(const uint64_t* __restrict__ rows, int64_t n, int W,
+                               const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                               uint64_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (flag[i])
+      for (int w = 0; w < W; ++w) out[int64_t(pos[i]) * W + w] = rows[i * W + w];
+}
+
 }  // namespace
+
+int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, cudaStream_t s) {
+  uint64_t cap = 1;
+  while (cap < 2 * uint64_t(n)) cap <<= 1;
+  DevBuf<uint32_t> table(cap, s), flag(size_t(n), s), pos(size_t(n), s);
+  CG_CUDA(cudaMemsetAsync(table.p, 0xff, cap * 4, s));
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 16);
+  k_hash_unique<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(rows, n, W, table.p, cap - 1,
+                                                                       flag.p);
+  CG_LAUNCH_CHECK();
+  CG_CUDA(cudaMemcpyAsync(pos.p, flag.p, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+  launch_scan_u32(pos.p, n, s);
+  uint32_t* h = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(h, pos.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(h + 1, flag.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  k_hash_compact<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(rows, n, W, flag.p, pos.p, out);
+  CG_LAUNCH_CHECK();
+  CG_CUDA(cudaStreamSynchronize(s));
+  return int64_t(h[0]) + h[1];
+}
 
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
                       cudaStream_t s) {

@@ -116,6 +116,10 @@ void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, 
                       cudaStream_t s);
 
 // ---------------------------------------------------------------- a3 dedupe + compaction
+// Distinct rows of rows u64[n][W] (first occurrences, input order) into out
+// (u64[n][W] capacity) by an open-addressed hash set; returns their count.
+// Used when skew overflows the MSD buckets.  Host-synchronising.
+int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, cudaStream_t s);
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],
 // lcp[n_c] (leading equal bits with the next cell; 0xffff for the last),
 // *n_cells (device u32).
