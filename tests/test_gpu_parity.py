@@ -325,3 +325,16 @@ def test_loaded_library_is_in_tree(cg):
 
     maps = open("/proc/self/maps").read()
     assert os.path.realpath(cgm.LIB_PATH) in maps or cgm.LIB_PATH in maps
+
+
+@pytest.mark.parametrize("ell,n", [(64, 1 << 19), (128, 1 << 19), (200, 300000), (1024, 1 << 18)])
+def test_heavy_duplication_hash_path(cg, ell, n):
+    """Skewed inputs (few distinct cells) at n >= 2^18 overflow the MSD
+    buckets and go through the hash dedupe + full sort of the distinct rows."""
+    rng = np.random.default_rng(ell + n)
+    base = synth.clustered_bytes(ell, 4000, ell, 6, 2)
+    x = np.ascontiguousarray(base[rng.integers(0, base.shape[0], size=n)])
+    cells, edges, _ = gpu_build(cg, x)
+    rc, oc, oe = oracle.build(x)
+    assert rc == 0
+    assert np.array_equal(cells, oc) and np.array_equal(edges, oe)
