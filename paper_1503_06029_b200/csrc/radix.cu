@@ -639,6 +639,42 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// TMA bulk copies (cp.async.bulk, 1-D) completing on an mbarrier: one thread
+// moves a whole bucket global -> shared; the CTA waits on the barrier phase.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ bool key_eq(const uint64_t& a, const uint64_t& b) { return a == b; }
 __device__ __forceinline__ bool key_eq(const ulonglong2& a, const ulonglong2& b) {
   return a.x == b.x && a.y == b.y;
@@ -684,7 +720,38 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? 3 : 4)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t lt = lanemask_lt();
 
-  auto prefetch = [&](int64_t bk, K* dst) {
+  // 16-byte keys: the next bucket arrives by one TMA bulk copy per bucket
+  // (mbarrier completion); 8-byte keys: per-thread cp.async
+  constexpr bool BULK = PREF && sizeof(K) == 16;
+  __shared__ uint64_t s_bar[2];
+  if (BULK) {
+    if (tid == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  auto prefetch = [&](int64_t bk, K* dst, uint64_t* bar) {
+    if (BULK) {
+      if (tid == 0) {
+        uint32_t S = 0, lo = 0;
+        if (bk < nbuckets) {
+          lo = off[bk];
+          S = off[bk + 1] - lo;
+        }
+        if (S > 0 && S <= uint32_t(CAP)) {
+          // the buffer was last written by the threads (generic proxy): order
+          // those writes before the async-proxy (TMA) writes
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(bar, S * uint32_t(sizeof(K)));
+          bulk_g2s(dst, keys + lo, S * uint32_t(sizeof(K)), bar);
+        } else {
+          mbar_arrive(bar);  // nothing to move: complete the phase
+        }
+      }
+      return;
+    }
     if (PREF && bk < nbuckets) {
       const uint32_t lo = off[bk];
       const int S = int(off[bk + 1] - lo);
@@ -693,12 +760,16 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? 3 : 4)
     }
     cp_async_commit();
   };
-  prefetch(blockIdx.x, buf0);
+  prefetch(blockIdx.x, buf0, &s_bar[0]);
   int it = 0;
   for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x, ++it) {
     K* s = (it & 1) ? buf1 : buf0;
-    prefetch(bk + gridDim.x, (it & 1) ? buf0 : buf1);
-    cp_async_wait1();
+    prefetch(bk + gridDim.x, (it & 1) ? buf0 : buf1, &s_bar[(it + 1) & 1]);
+    if (BULK) {
+      mbar_wait(&s_bar[it & 1], uint32_t(it >> 1) & 1u);  // use it/2 of this buffer
+    } else {
+      cp_async_wait1();
+    }
     __syncthreads();
     const uint32_t lo = off[bk], hi = off[bk + 1];
     const int S = int(hi - lo);
