@@ -67,9 +67,10 @@ def main():
             lines.append(f"- {m}: {v}")
         lines.append("")
     if os.path.exists(launches):
-        lines.append("## launch list (bench.py --steps 2 --warmup 1 under ncu)")
+        lines.append("## launch list of the last build (bench.py --steps 2 --warmup 1 --no-f1 under ncu)")
         lines.append("")
-        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launches.py"), launches, "20"],
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launches.py"), launches,
+                            os.environ.get("LAUNCHES_PER_STEP", "20")],
                            capture_output=True, text=True).stdout
         lines += ["```", p.rstrip(), "```"]
     with open(os.path.join(OUT, f"{tag}_summary.md"), "w") as f:
