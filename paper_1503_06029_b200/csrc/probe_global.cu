@@ -38,6 +38,9 @@ constexpr int kTileCells = 32;      // cells per tile = lanes per warp
 constexpr int kProbeWarps = 8;      // warps per CTA (independent)
 constexpr int kWarpEdgeCap = 512;   // shared-memory edge buffer per warp
 constexpr int kTileEdgeCap = kWarpEdgeCap;
+#ifndef PROBE_MIN_BLOCKS
+#define PROBE_MIN_BLOCKS 6  // 40 registers, 6 CTAs (48 warps) per SM
+#endif
 
 template <int WC>
 struct GRow {
@@ -61,7 +64,7 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 }
 
 template <int WC>
-__global__ void __launch_bounds__(32 * kProbeWarps)
+__global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
                    unsigned long long* total, unsigned long long* issued,
