@@ -1045,6 +1045,14 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
   CG_LAUNCH_CHECK();
 }
 
+// bases[d][b] = exclusive scan of hist[d][0..256) (one block per digit)
+__global__ void k_digit_bases(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases) {
+  __shared__ uint32_t tmp[33];
+  uint32_t total;
+  const uint32_t v = hist[blockIdx.x * kRadix + threadIdx.x];
+  bases[blockIdx.x * kRadix + threadIdx.x] = block_excl_scan(v, tmp, &total);
+}
+
 // tile_cnt[t][256] (per-tile digit counts) -> tile_pre[t][256] = exclusive
 // prefix over tiles, per digit: chunk sums, a scan of the chunk sums, fill.
 constexpr int kPreChunk = 64;
@@ -1105,12 +1113,25 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
     CG_LAUNCH_CHECK();
     hsrc = hist.p;
   }
-  uint32_t* hh = static_cast<uint32_t*>(host_stage(hist.n * sizeof(uint32_t)));
-  CG_CUDA(cudaMemcpyAsync(hh, hsrc, hist.n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  CG_CUDA(cudaStreamSynchronize(s));
   std::vector<int> digits;
   std::vector<uint32_t> bases;
-  for (int d = 0; d < nd; ++d) {
+  DevBuf<uint32_t> dbases;
+  if (dev_hist && !want_vals) {
+    // (MSD partition, histogram counted by the pack kernel) no host round
+    // trip: the digit bases are scanned on the device and every digit gets a
+    // pass -- a constant digit only costs one extra copy-like pass
+    for (int d = 0; d < nd; ++d) digits.push_back(d + dlo);
+    dbases.alloc(size_t(nd) * kRadix, s);
+    k_digit_bases<<<unsigned(nd), kRadix, 0, s>>>(dev_hist, dbases.p);
+    CG_LAUNCH_CHECK();
+  }
+  uint32_t* hh = nullptr;
+  if (digits.empty()) {
+    hh = static_cast<uint32_t*>(host_stage(hist.n * sizeof(uint32_t)));
+    CG_CUDA(cudaMemcpyAsync(hh, hsrc, hist.n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+  }
+  for (int d = 0; hh && d < nd; ++d) {
     const uint32_t* h = hh + d * kRadix;
     bool trivial = false;
     for (int b = 0; b < kRadix; ++b)
@@ -1129,9 +1150,11 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
     return;
   }
   const int P = int(digits.size());
-  DevBuf<uint32_t> dbases(bases.size(), s);
-  CG_CUDA(cudaMemcpyAsync(dbases.p, bases.data(), bases.size() * sizeof(uint32_t),
-                          cudaMemcpyHostToDevice, s));
+  if (hh) {
+    dbases.alloc(bases.size(), s);
+    CG_CUDA(cudaMemcpyAsync(dbases.p, bases.data(), bases.size() * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+  }
   const bool V = want_vals;
   // as many resident tiles per SM as registers allow: prefer shared memory
   if (V) {
