@@ -44,8 +44,11 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_ou
 r = list(csv.reader(out.splitlines()))
 h = r[1]
 rows = r[2:]
-# the template instance whose SASS length matches the report
-fn = min(fns, key=lambda f: abs(len(lines[f]) - len(rows)))
+# the profiled instance: its mangled name from the report, else by SASS length
+mg = subprocess.run(["ncu", "-i", rep, "--print-kernel-base", "mangled", "--page", "details", "--csv"],
+                    capture_output=True, text=True).stdout.splitlines()
+mname = next((c.strip('"') for ln in mg[1:2] for c in ln.split('","') if c.strip('"').startswith("_Z")), None)
+fn = mname if mname in lines else min(fns, key=lambda f: abs(len(lines[f]) - len(rows)))
 ai, si, ii, ti = (h.index("Address"), h.index("Warp Stall Sampling (All Samples)"),
                   h.index("Instructions Executed"), h.index("Source"))
 base = int(rows[0][ai], 16)

@@ -25,7 +25,11 @@ for cub in glob.glob(tmp + "/*.cubin"):
         m = re.search(r"/\*([0-9a-f]{4,})\*/", ln)
         if m and fn and kname in fn:
             lines.setdefault(fn, {})[int(m.group(1), 16)] = loc
-fn = min(lines, key=lambda f: abs(len(lines[f]) - len(rows)))
+# the profiled instance: its mangled name from the report, else by SASS length
+mg = subprocess.run(["ncu", "-i", rep, "--print-kernel-base", "mangled", "--page", "details", "--csv"],
+                    capture_output=True, text=True).stdout.splitlines()
+mname = next((c.strip('"') for ln in mg[1:2] for c in ln.split('","') if c.strip('"').startswith("_Z")), None)
+fn = mname if mname in lines else min(lines, key=lambda f: abs(len(lines[f]) - len(rows)))
 base = int(rows[0][ai], 16)
 agg = {}
 for x in rows:
