@@ -1230,10 +1230,70 @@ template void radix_sort<uint64_t>(uint64_t*, uint64_t*, const uint32_t*, uint32
                                    bool, int64_t, int, uint64_t**, uint32_t**, cudaStream_t,
                                    SortStats*);
 
+namespace {
+// Tie runs of the (word 0, index) order: rows whose word 0 is equal form
+// contiguous runs; the thread at the head of a run (<= kTieRun rows)
+// insertion-sorts the run's indices on the remaining words (stable: equal
+// rows keep index order).  A longer run raises *long_run (then the caller
+// sorts all words instead).
+constexpr int kTieRun = 32;
+__global__ void k_tie_fix(const uint64_t* __restrict__ keys, int W, const uint64_t* __restrict__ w0,
+                          uint32_t* __restrict__ idx, int64_t n, uint32_t* __restrict__ long_run) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = w0[i];
+    if (i > 0 && w0[i - 1] == k) continue;       // not a run head
+    if (i + 1 >= n || w0[i + 1] != k) continue;  // run of one
+    int64_t e = i + 2;
+    while (e < n && w0[e] == k && e - i <= kTieRun) ++e;
+    if (e - i > kTieRun) {
+      atomicOr(long_run, 1u);
+      continue;
+    }
+    for (int64_t a = i + 1; a < e; ++a) {
+      const uint32_t v = idx[a];
+      const uint64_t* rv = keys + int64_t(v) * W;
+      int64_t z = a;
+      while (z > i) {
+        const uint32_t u = idx[z - 1];
+        const uint64_t* ru = keys + int64_t(u) * W;
+        int c = 0;
+        for (int w = 1; w < W && c == 0; ++w) c = ru[w] < rv[w] ? -1 : (ru[w] > rv[w] ? 1 : 0);
+        if (c < 0 || (c == 0 && u < v)) break;
+        idx[z] = u;
+        --z;
+      }
+      idx[z] = v;
+    }
+  }
+}
+}  // namespace
+
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
                          cudaStream_t s, SortStats* st) {
   DevBuf<uint64_t> kw(size_t(n), s), kw_alt(size_t(n), s);
   DevBuf<uint32_t> ia(size_t(n), s), ib(size_t(n), s);
+  {
+    // word 0 decides most orders: sort (word 0, index), then order the runs
+    // of equal word 0 on the remaining words; only if a run is long (heavy
+    // word-0 ties, e.g. arrangement signatures) sort every word (LSD below)
+    k_gather_word<<<grid_for(n, 256), 256, 0, s>>>(keys, W, 0, nullptr, n, kw.p);
+    CG_LAUNCH_CHECK();
+    uint64_t* ko = nullptr;
+    uint32_t* vo = nullptr;
+    radix_sort<uint64_t>(kw.p, kw_alt.p, nullptr, ia.p, ib.p, true, n, 64, &ko, &vo, s, st);
+    DevBuf<uint32_t> flag(1, s);
+    CG_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+    k_tie_fix<<<grid_for(n, 256), 256, 0, s>>>(keys, W, ko, vo, n, flag.p);
+    CG_LAUNCH_CHECK();
+    uint32_t* h = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+    CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (h[0] == 0) {
+      launch_gather_rows(keys, vo, n, W, sorted, s);
+      return;
+    }
+  }
   const uint32_t* idx = nullptr;  // identity before the first word pass
   for (int w = W - 1; w >= 0; --w) {
     k_gather_word<<<grid_for(n, 256), 256, 0, s>>>(keys, W, w, idx, n, kw.p);
