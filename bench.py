@@ -134,9 +134,9 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
     nc, m = st["n_cells"], st["n_edges"]
     dict_b = st.get("dict_bytes", 0)
     # MSD path (W <= 2): 2 top-digit one-sweep passes + the bucket pass, each
-    # reads and writes every key; multi-word LSD (W > 2): per word 8 passes
-    # over (u64 word, u32 index) pairs + gathers
-    sort_key_bytes = 6 * K if W <= 2 else W * (8 * 2 * 12 + 16) + 2 * K
+    # reads and writes every key; W > 2: word-0 gather, 8 passes over
+    # (u64 word 0, u32 index) pairs, one row gather (tie fixes not counted)
+    sort_key_bytes = 6 * K if W <= 2 else 8 + 8 * 2 * 12 + (K + 4) + K
     tiles = (nc + 255) // 256
     return {
         "pack": n * (ell + K),
