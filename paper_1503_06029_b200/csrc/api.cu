@@ -362,16 +362,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   const uint64_t* sorted = nullptr;
   bool done = false;
   int64_t nc = -1;
+  uint32_t in_err = 0;
+  bool in_err_read = false;  // the input-error flag already came back with the sort's counts
   if (msd) {
     uint64_t* ko = nullptr;
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
     done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off, pre_B,
-                                   tile_hist)
+                                   tile_hist, d_flags, &in_err)
                  : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     sorted = ko;
     if (done && fused) {
       nc = ncu;
+      in_err_read = true;
       if (ko == keys.p) cellbuf.adopt(keys.release(), size_t(n) * W, s);
       else cellbuf.adopt(alt.release(), size_t(n) * W, s);
     }
@@ -412,11 +415,14 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     // layered dictionary (the global-dictionary probe derives lcp itself)
     launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
   }
-  uint32_t* hf = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
-  CG_CUDA(cudaMemcpyAsync(hf, d_flags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  CG_CUDA(cudaStreamSynchronize(s));
-  if (hf[0]) throw CgError{CG_EINPUT, "input byte not in {0,1} (or pad bit set in packed input)"};
-  if (nc < 0) nc = hf[1];
+  if (!in_err_read) {
+    uint32_t* hf = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
+    CG_CUDA(cudaMemcpyAsync(hf, d_flags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    in_err = hf[0];
+    if (nc < 0) nc = hf[1];
+  }
+  if (in_err) throw CgError{CG_EINPUT, "input byte not in {0,1} (or pad bit set in packed input)"};
   tm.mark();  // 3: dedupe
   keys.reset();
   alt.reset();

@@ -101,7 +101,8 @@ int msd_prefix_bits(int64_t n);
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
                      const uint32_t* pre_off = nullptr, int pre_B = 0,
-                     const uint32_t* tile_hist = nullptr);
+                     const uint32_t* tile_hist = nullptr, const uint32_t* side_dev = nullptr,
+                     uint32_t* side_host = nullptr);
 int msd_tile_rows(int W);
 // MSD scatter pack (W <= 2, ell % 16 == 0, 16-byte aligned rows): histogram of
 // the top B bits from the first 16 bytes of each row, then pack straight into

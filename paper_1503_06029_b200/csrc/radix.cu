@@ -1356,7 +1356,8 @@ __global__ void k_compact_buckets(const K* __restrict__ src, const uint32_t* __r
 template <class K>
 bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaStream_t s,
                       SortStats* st, const uint32_t* top_hist, const uint32_t* pre_off = nullptr,
-                      int pre_B = 0, const uint32_t* tile_hist = nullptr) {
+                      int pre_B = 0, const uint32_t* tile_hist = nullptr,
+                      const uint32_t* side_dev = nullptr, uint32_t* side_host = nullptr) {
   // pre_off: keys are already grouped by their top pre_B bits (scatter pack),
   // pre_off[b] = first row of bucket b -- no global pass needed
   const int B = pre_off ? pre_B : msd_prefix_bits(n);
@@ -1377,11 +1378,14 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   launch_bucket_sort<K>(ko, offp, n, nb, B, flag.p, ucnt.p, s);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
-  uint32_t* h = static_cast<uint32_t*>(host_stage(3 * sizeof(uint32_t)));
+  uint32_t* h = static_cast<uint32_t*>(host_stage(4 * sizeof(uint32_t)));
   CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaMemcpyAsync(h + 1, uoff.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaMemcpyAsync(h + 2, ucnt.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  // the caller's input-error flag rides on the same round trip
+  if (side_dev) CG_CUDA(cudaMemcpyAsync(h + 3, side_dev, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
+  if (side_dev && side_host) *side_host = h[3];
   *cells = ko;
   if (h[0]) return false;
   const int64_t total = int64_t(h[1]) + int64_t(h[2]);
@@ -1404,11 +1408,12 @@ int msd_tile_rows(int W) {
 
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
-                     const uint32_t* pre_off, int pre_B, const uint32_t* tile_hist) {
+                     const uint32_t* pre_off, int pre_B, const uint32_t* tile_hist,
+                     const uint32_t* side_dev, uint32_t* side_host) {
   if (W == 1) {
     uint64_t* o = nullptr;
     const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist, pre_off,
-                                               pre_B, tile_hist);
+                                               pre_B, tile_hist, side_dev, side_host);
     *cells = o;
     return ok;
   }
@@ -1416,7 +1421,8 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
     ulonglong2* o = nullptr;
     const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
                                                  reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
-                                                 st, top_hist, pre_off, pre_B, tile_hist);
+                                                 st, top_hist, pre_off, pre_B, tile_hist, side_dev,
+                                                 side_host);
     *cells = reinterpret_cast<uint64_t*>(o);
     return ok;
   }
