@@ -82,3 +82,28 @@ def test_no_cpu_fallback_in_product_package():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "import oracle" not in src and "from oracle" not in src, fn
+
+
+def test_kernel_launch_counter_and_new_entries_reject_bad_arguments(L):
+    """cg_kernel_launches is monotone; the f1-f4 entries reject NULL / bad
+    sizes before touching the device."""
+    from paper_1503_06029_b200.cg import CG_EINVAL, cg_cells, cg_edges
+
+    a = L.cg_kernel_launches()
+    assert a >= 0 and L.cg_kernel_launches() == a
+    i64 = ctypes.c_int64
+    assert L.cg_signatures(None, 4, 3, None, 8, None, None) == CG_EINVAL
+    fake = ctypes.c_void_p(0x1000)
+    assert L.cg_signatures(fake, 4, 0, fake, 8, fake, None) == CG_EINVAL   # dim 0
+    assert L.cg_signatures(fake, 4, 17, fake, 8, fake, None) == CG_EINVAL  # dim 17
+    assert L.cg_signatures(fake, 0, 3, fake, 8, fake, None) == CG_EINVAL   # n 0
+    c, e = cg_cells(), cg_edges()
+    assert L.cg_insert(None, 1, None, 0, 8, fake, 1, None, ctypes.byref(c), ctypes.byref(e)) == CG_EINVAL
+    assert L.cg_insert(fake, 0, None, 0, 8, fake, 1, None, ctypes.byref(c), ctypes.byref(e)) == CG_EINVAL
+    assert L.cg_allpairs(None, 4, 64, 0, ctypes.byref(e), None, None) == CG_EINVAL
+    assert L.cg_allpairs(fake, 4, 64, 9, ctypes.byref(e), None, None) == CG_EINVAL  # anchors > 8
+    assert L.cg_csr(fake, 1, 0, fake, fake, None) == CG_EINVAL   # n_cells 0
+    ecc = ctypes.c_int32()
+    assert L.cg_bfs(fake, fake, 4, 4, fake, None, ctypes.byref(ecc), None) == CG_EINVAL  # source
+    assert L.cg_bfs(None, fake, 4, 0, fake, None, ctypes.byref(ecc), None) == CG_EINVAL
+    assert c.words is None and e.ij is None
