@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
   const int W = WC > 0 ? WC : g.W;
   const int b = g.b;
   const int fb = g.b + g.fextra;
-  unsigned long long my_issued = 0;
+  uint32_t my_issued = 0;  // per thread (< 2^32); summed as 64-bit at the end
   uint64_t* wbuf = ebuf[tid >> 5];
 
   while (true) {
@@ -453,9 +453,10 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     }
     __syncwarp();
   }
+  unsigned long long wsum = my_issued;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) my_issued += __shfl_xor_sync(kFull, my_issued, o);
-  if (lane == 0 && my_issued) atomicAdd(issued, my_issued);
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+  if (lane == 0 && wsum) atomicAdd(issued, wsum);
 }
 
 }  // namespace
