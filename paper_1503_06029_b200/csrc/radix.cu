@@ -1063,13 +1063,23 @@ __global__ void k_tile_chunk_sum(const uint32_t* __restrict__ cnt, int64_t nt,
   for (int64_t q = c * kPreChunk; q < min(nt, (c + 1) * kPreChunk); ++q) t += cnt[q * kRadix + d];
   csum[c * kRadix + d] = t;
 }
+// one warp per digit: exclusive scan of its nc chunk sums, 32 at a time
 __global__ void k_tile_chunk_scan(uint32_t* __restrict__ csum, int64_t nc) {
-  const int d = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (d >= kRadix) return;
   uint32_t run = 0;
-  for (int64_t c = 0; c < nc; ++c) {
-    const uint32_t v = csum[c * kRadix + d];
-    csum[c * kRadix + d] = run;
-    run += v;
+  for (int64_t c0 = 0; c0 < nc; c0 += 32) {
+    const int64_t c = c0 + lane;
+    const uint32_t v = c < nc ? csum[c * kRadix + d] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (c < nc) csum[c * kRadix + d] = run + x - v;
+    run += __shfl_sync(kFull, x, 31);
   }
 }
 __global__ void k_tile_fill(const uint32_t* __restrict__ cnt, int64_t nt,
@@ -1178,7 +1188,7 @@ void radix_passes(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals,
     DevBuf<uint32_t> csum(size_t(nch) * kRadix, s);
     k_tile_chunk_sum<<<unsigned(nch), kRadix, 0, s>>>(tile_hist, tiles, csum.p);
     CG_LAUNCH_CHECK();
-    k_tile_chunk_scan<<<1, kRadix, 0, s>>>(csum.p, nch);
+    k_tile_chunk_scan<<<kRadix / 8, 256, 0, s>>>(csum.p, nch);
     CG_LAUNCH_CHECK();
     k_tile_fill<<<unsigned(nch), kRadix, 0, s>>>(tile_hist, tiles, csum.p, tpre.p);
     CG_LAUNCH_CHECK();
