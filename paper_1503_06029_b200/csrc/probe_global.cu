@@ -423,16 +423,25 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     const uint32_t base = __shfl_sync(kFull, bs, 0);
     if (base != 0xffffffffu && wn > 0) {
       const uint64_t wpos = uint64_t(base);
-      if (wn <= 32 && g.n_cells <= (int64_t(1) << 27)) {
-        // one hit per lane: rank on a 32-bit key (source lane << 27 | j),
-        // the keys exchanged by shuffles
-        const uint64_t e0 = lane < int(wn) ? wbuf[lane] : ~0ull;
-        const uint32_t k0 = lane < int(wn)
-            ? ((uint32_t(e0 >> 32) - uint32_t(i - lane)) << 27) | uint32_t(e0)
-            : 0xffffffffu;
-        uint32_t r0 = 0;
-        for (uint32_t p = 0; p < wn; ++p) r0 += __shfl_sync(kFull, k0, p) < k0;
-        if (lane < int(wn) && wpos + r0 < cap) out[wpos + r0] = e0;
+      if (wn <= 32) {
+        // one hit per lane.  Every path above emits a source cell's hits in
+        // ascending j (near rows in order, then flips from the least
+        // significant bit up, near before far), so the rank of a hit is
+        // #(hits of lower source lanes) + #(earlier hits of its own source):
+        // a 5-bit radix rank of the source lane from five ballots
+        const bool h0 = lane < int(wn);
+        const uint64_t e0 = h0 ? wbuf[lane] : 0ull;
+        const uint32_t src = h0 ? uint32_t(e0 >> 32) - uint32_t(i - lane) : 0u;
+        uint32_t same = __ballot_sync(kFull, h0), less = 0;
+#pragma unroll
+        for (int k = 4; k >= 0; --k) {
+          const uint32_t bk = __ballot_sync(kFull, (src >> k) & 1u);
+          const uint32_t sb = 0u - ((src >> k) & 1u);  // all ones iff bit k set
+          less |= same & ~bk & sb;
+          same &= bk ^ ~sb;
+        }
+        const uint32_t r0 = __popc(less) + __popc(same & lt);
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = e0;
       } else if (wn <= 64) {
         // rank = number of smaller keys (the (i, j) keys are distinct);
         // every lane reads the same word per step (broadcast)
