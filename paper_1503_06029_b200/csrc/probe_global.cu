@@ -3,8 +3,8 @@
 // the probe itself (no edge sort).
 //
 // Dictionary (a5): the canonical table V (sorted, unique) with a 2^b prefix
-// index T (T[x] = first cell whose top b bits are >= x; ~4-8 cells per
-// bucket) and a prefix filter F of 2^(b+E) bits.  The popcount layering of
+// index T (T[x] = first cell whose top b bits are >= x; 1-2 cells per
+// bucket at the defaults) and a prefix filter F of 2^(b+E) bits.  The popcount layering of
 // the north star is implicit: a hit R of cell V must satisfy R ⊇ V and
 // popc(R) = popc(V) + 1 (the adjacent layer), which the subset/equality tests
 // enforce; the layered dictionary remains available (CG_DICT_SORTED).
@@ -107,16 +107,29 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       return Vp[w];
     };
     int kmax = -1;
+    // the next row is the neighbouring lane's cell: take it by shuffle
+    // (lane 31 and the end of the range load it)
+    uint64_t nxt[WC > 0 ? WC : 1];
+    if (WC > 0) {
+#pragma unroll
+      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) nxt[w] = __shfl_down_sync(kFull, v[w], 1);
+    }
     if (valid) {
       if (lcp_prune) {
-        // lcp(V_i, V_{i+1}) from the next row (the neighbouring lane's cell,
-        // so an L1 hit); the last cell has no successor and probes nothing
+        // lcp(V_i, V_{i+1}); the last cell has no successor and probes nothing
         if (i + 1 < g.n_cells) {
           const uint64_t* Np = g.keys + (i + 1) * W;
+          const bool shfl = WC > 0 && lane < 31 && i + 1 < i_hi;
           int l = -1;
           const int n = WC > 0 ? WC : W;
           for (int w = 0; w < n && l < 0; ++w) {
-            const uint64_t x = Np[w] ^ V(w);
+            uint64_t nw = 0;
+            if (WC > 0) {
+#pragma unroll
+              for (int u = 0; u < (WC > 0 ? WC : 1); ++u)
+                if (u == w) nw = nxt[u];
+            }
+            const uint64_t x = (shfl ? nw : Np[w]) ^ V(w);
             if (x) l = 64 * w + __clzll(x);
           }
           kmax = (l < 0) ? g.ell - 1 : min(l, g.ell - 1);
@@ -275,7 +288,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
           fw[u] = __ldg(g.F + (fa[u] >> 5));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) surv |= bm[u] & (0u - ((fw[u] >> (fa[u] & 31)) & 1u));
+        for (int u = 0; u < 4; ++u) surv |= bm[u] & (0u - (__funnelshift_r(fw[u], fw[u], fa[u]) & 1u));  // shift mod 32
       }
     }
     // ---- far survivors, flattened over the warp
