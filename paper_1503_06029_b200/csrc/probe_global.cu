@@ -170,18 +170,20 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     // ---- near: rows i+1.. in V's own b-prefix bucket
     const bool near_on = kmax >= b;
     const uint64_t pv = b ? (v0 >> (64 - b)) : 0ull;
-    int64_t bucket_end = i + 1;
+    // row indices fit in 32 bits (T is u32): 32-bit index arithmetic
+    const uint32_t i32 = uint32_t(i);
+    uint32_t bucket_end = i32 + 1;
     if (near_on) bucket_end = g.T[pv + 1];
-    const bool near_scan = near_on && (bucket_end - (i + 1) <= 16);
-    int64_t r = i + 1;
+    const bool near_scan = near_on && (bucket_end - (i32 + 1) <= 16u);
+    uint32_t r = i32 + 1;
     while (__any_sync(kFull, near_scan && r < bucket_end)) {
       bool hit[4] = {false, false, false, false};
       if (near_scan && r < bucket_end) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int64_t rr = r + u;
+          const uint32_t rr = r + u;
           if (rr < bucket_end) {
-            const uint64_t* R = g.keys + rr * W;
+            const uint64_t* R = g.keys + size_t(rr) * W;
             uint64_t miss = 0;
             int diff = 0;
             if (WC == 2) {
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) emit(hit[u], ci | uint64_t(r + u));
+      for (int u = 0; u < 4; ++u) emit(hit[u], ci | uint64_t(r + uint32_t(u)));
       if (near_scan) r += 4;
     }
     // big bucket (skewed data): per candidate binary search in (i, bucket_end)
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       const uint32_t o_surv = __shfl_sync(kFull, surv, owner);
       const uint64_t o_v0 = __shfl_sync(kFull, v0, owner);
       const uint64_t o_v1 = __shfl_sync(kFull, my_v1, owner);
-      const int64_t o_i = __shfl_sync(kFull, i, owner);
+      const uint32_t o_i = __shfl_sync(kFull, i32, owner);
       bool hit = false;
       uint64_t e = 0;
       if (gg < total_sv) {
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         const uint64_t t0 = o_v0 | bm;
         const int64_t x = int64_t(t0 >> (64 - b));
         const uint32_t lo = g.T[x], hi = g.T[x + 1];
-        const uint64_t* OV = g.keys + o_i * W;  // owner's row (W > 2 path)
+        const uint64_t* OV = g.keys + size_t(o_i) * W;  // owner's row (W > 2 path)
         int64_t found = -1;
         if (hi - lo <= 12) {
           for (uint32_t rr = lo; rr < hi && found < 0; rr += 4) {
