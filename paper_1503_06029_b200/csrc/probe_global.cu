@@ -303,34 +303,59 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     }
     const uint32_t total_sv = __shfl_sync(kFull, incl, 31);
     const uint64_t my_v1 = (WC == 2) ? V(1) : 0ull;
+    // (owner lane, bit) of every survivor in flattened order, as a u16 table
+    // at the tail of the warp's edge buffer when it fits beside the hits the
+    // rounds can still append (at most one per survivor); else both are
+    // found per round by a search over the prefix sums
+    const bool use_tab = wfill + total_sv + (total_sv + 3) / 4 <= uint32_t(kWarpEdgeCap);
+    uint16_t* stab = reinterpret_cast<uint16_t*>(wbuf + kWarpEdgeCap) - total_sv;
+    if (use_tab) {
+      uint32_t sv = surv, pos = incl - nsv;
+      while (sv) {
+        const uint32_t k = __ffs(sv) - 1;  // least significant bit first: ascending j
+        sv &= sv - 1;
+        stab[pos++] = uint16_t((uint32_t(lane) << 8) | k);
+      }
+      __syncwarp();
+    }
     for (uint32_t gb = 0; gb < total_sv; gb += 32) {
       const uint32_t gg = gb + lane;
-      int owner = 0;
+      int owner = 31, k = 0;
+      if (use_tab) {
+        if (gg < total_sv) {
+          const uint32_t en = stab[gg];
+          owner = int(en >> 8);
+          k = int(en & 255u);
+        }
+      } else {
+        owner = 0;
 #pragma unroll
-      for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-        const uint32_t ic = __shfl_sync(kFull, incl, owner + s2 - 1);
-        if (ic <= gg) owner += s2;
+        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+          const uint32_t ic = __shfl_sync(kFull, incl, owner + s2 - 1);
+          if (ic <= gg) owner += s2;
+        }
+        owner = min(owner, 31);
+        const uint32_t o_incl = __shfl_sync(kFull, incl, owner);
+        const uint32_t o_cnt = __shfl_sync(kFull, nsv, owner);
+        const uint32_t o_surv = __shfl_sync(kFull, surv, owner);
+        if (gg < total_sv) {
+          int m = int(gg - (o_incl - o_cnt));
+#pragma unroll
+          for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+            const int c = __popc((o_surv >> k) & ((1u << s2) - 1u));
+            if (m >= c) {
+              m -= c;
+              k += s2;
+            }
+          }
+        }
       }
-      owner = min(owner, 31);
-      const uint32_t o_incl = __shfl_sync(kFull, incl, owner);
-      const uint32_t o_cnt = __shfl_sync(kFull, nsv, owner);
-      const uint32_t o_surv = __shfl_sync(kFull, surv, owner);
       const uint64_t o_v0 = __shfl_sync(kFull, v0, owner);
       const uint64_t o_v1 = __shfl_sync(kFull, my_v1, owner);
       const uint32_t o_i = __shfl_sync(kFull, i32, owner);
       bool hit = false;
       uint64_t e = 0;
       if (gg < total_sv) {
-        int m = int(gg - (o_incl - o_cnt));
-        int k = 0;
-#pragma unroll
-        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-          const int c = __popc((o_surv >> k) & ((1u << s2) - 1u));
-          if (m >= c) {
-            m -= c;
-            k += s2;
-          }
-        }
         const uint64_t bm = 1ull << (32 + k);  // top-word bit k = key bit 31 - k
         const uint64_t t0 = o_v0 | bm;
         const int64_t x = int64_t(t0 >> (64 - b));
