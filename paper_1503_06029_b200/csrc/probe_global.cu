@@ -63,7 +63,7 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
   }
 }
 
-template <int WC>
+template <int WC, int FR = 5>  // FR: filter loads in flight per lane and round (3-6 measured)
 __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
@@ -278,19 +278,19 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       const int fsh = 32 - fb;
       uint32_t z = ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar));
       my_issued += __popc(z);
-      // branch-free rounds of 4 filter loads in flight; an exhausted slot
+      // branch-free rounds of FR filter loads in flight; an exhausted slot
       // (bm = 0) re-reads the cell's own filter word and is masked out
       while (z) {
-        uint32_t bm[4], fa[4], fw[4];
+        uint32_t bm[FR], fa[FR], fw[FR];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < FR; ++u) {
           bm[u] = z & (0u - z);
           z ^= bm[u];
           fa[u] = y0 | (bm[u] >> fsh);
           fw[u] = __ldg(g.F + (fa[u] >> 5));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) surv |= bm[u] & (0u - (__funnelshift_r(fw[u], fw[u], fa[u]) & 1u));  // shift mod 32
+        for (int u = 0; u < FR; ++u) surv |= bm[u] & (0u - (__funnelshift_r(fw[u], fw[u], fa[u]) & 1u));  // shift mod 32
       }
     }
     // ---- far survivors, flattened over the warp
