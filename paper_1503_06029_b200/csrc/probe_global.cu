@@ -63,7 +63,9 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
   }
 }
 
-template <int WC, int FR = 5>  // FR: filter loads in flight per lane and round (3-6 measured)
+// FR: filter loads in flight per lane and round; NR / SR: near rows and
+// survivor-bucket rows compared per round (A/B at C5: FR 3-6, NR/SR 1, 2, 4)
+template <int WC, int FR = 5, int NR = 2, int SR = 2>
 __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
@@ -177,10 +179,10 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     const bool near_scan = near_on && (bucket_end - (i32 + 1) <= 16u);
     uint32_t r = i32 + 1;
     while (__any_sync(kFull, near_scan && r < bucket_end)) {
-      bool hit[4] = {false, false, false, false};
+      bool hit[NR] = {};
       if (near_scan && r < bucket_end) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < NR; ++u) {
           const uint32_t rr = r + u;
           if (rr < bucket_end) {
             const uint64_t* R = g.keys + size_t(rr) * W;
@@ -204,8 +206,8 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) emit(hit[u], ci | uint64_t(r + uint32_t(u)));
-      if (near_scan) r += 4;
+      for (int u = 0; u < NR; ++u) emit(hit[u], ci | uint64_t(r + uint32_t(u)));
+      if (near_scan) r += NR;
     }
     // big bucket (skewed data): per candidate binary search in (i, bucket_end)
     {
@@ -363,9 +365,9 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         const uint64_t* OV = g.keys + size_t(o_i) * W;  // owner's row (W > 2 path)
         int64_t found = -1;
         if (hi - lo <= 12) {
-          for (uint32_t rr = lo; rr < hi && found < 0; rr += 4) {
+          for (uint32_t rr = lo; rr < hi && found < 0; rr += SR) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < SR; ++u) {
               const uint32_t ru = rr + u;
               if (ru < hi) {
                 const uint64_t* R = g.keys + int64_t(ru) * W;
