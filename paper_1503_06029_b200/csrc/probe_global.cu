@@ -596,17 +596,32 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) s_pre[nt] = off[t0 + nt - 1] - base + cntv[t0 + nt - 1];
     __syncthreads();
     const uint32_t E = s_pre[nt];
-    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
-      int lo = 0, hi = nt - 1;  // last tile with s_pre <= e
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_pre[mid] <= e) lo = mid;
-        else hi = mid - 1;
+    // 4 edges per thread and step: all four loads in flight before the stores
+    constexpr int U = 4;
+    for (uint32_t e0 = threadIdx.x; e0 < E; e0 += U * blockDim.x) {
+      uint32_t src[U];
+      uint64_t k[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = e0 + u * blockDim.x;
+        src[u] = 0xffffffffu;
+        if (e < E) {
+          int lo = 0, hi = nt - 1;  // last tile with s_pre <= e
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pre[mid] <= e) lo = mid;
+            else hi = mid - 1;
+          }
+          const uint32_t p = s_pos[lo];
+          if (p != 0xffffffffu) src[u] = p + (e - s_pre[lo]);
+        }
       }
-      const uint32_t p = s_pos[lo];
-      if (p == 0xffffffffu) continue;
-      const uint64_t k = scratch[p + (e - s_pre[lo])];
-      out[uint64_t(base) + e] = (k >> 32) | (k << 32);
+#pragma unroll
+      for (int u = 0; u < U; ++u) k[u] = src[u] != 0xffffffffu ? __ldcs(scratch + src[u]) : 0ull;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (src[u] != 0xffffffffu)
+          out[uint64_t(base) + e0 + u * blockDim.x] = (k[u] >> 32) | (k[u] << 32);
     }
   }
 }
