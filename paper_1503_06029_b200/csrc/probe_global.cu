@@ -281,7 +281,26 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       uint32_t z = ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar));
       my_issued += __popc(z);
       // branch-free rounds of FR filter loads in flight; an exhausted slot
-      // (bm = 0) re-reads the cell's own filter word and is masked out
+      // (bm = 0) re-reads the cell's own filter word and is masked out.
+      // With fextra >= 5 a far flip (key bit k < b) lands on prefix bit
+      // fb - 1 - k >= 5: it changes the filter WORD only, the bit within the
+      // word is the cell's own (y0 & 31), so the test is two shifts
+      if (g.fextra >= 5) {
+        const uint32_t wy = y0 >> 5;
+        const int sh5 = fsh + 5;
+        const uint32_t sc = 31u - (y0 & 31u);
+        while (z) {
+          uint32_t bm[FR], fw[FR];
+#pragma unroll
+          for (int u = 0; u < FR; ++u) {
+            bm[u] = z & (0u - z);
+            z ^= bm[u];
+            fw[u] = __ldg(g.F + (wy | (bm[u] >> sh5)));
+          }
+#pragma unroll
+          for (int u = 0; u < FR; ++u) surv |= bm[u] & uint32_t(int32_t(fw[u] << sc) >> 31);
+        }
+      }
       while (z) {
         uint32_t bm[FR], fa[FR], fw[FR];
 #pragma unroll

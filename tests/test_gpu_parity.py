@@ -338,3 +338,15 @@ def test_heavy_duplication_hash_path(cg, ell, n):
     rc, oc, oe = oracle.build(x)
     assert rc == 0
     assert np.array_equal(cells, oc) and np.array_equal(edges, oe)
+
+
+@pytest.mark.parametrize("fextra", ["0", "2", "4", "5", "8"])
+def test_filter_resolution(cg, fextra, monkeypatch):
+    """The prefix filter's extra bits (CG_FILTER_EXTRA) change only which far
+    flips reach a bucket search, never the result; fextra >= 5 takes the
+    probe's word-only filter test, smaller values the general one."""
+    monkeypatch.setenv("CG_FILTER_EXTRA", fextra)
+    d = synth.config("C5", scale_log2=16)
+    x = synth.unpack_words_np(d["words"], d["ell"])
+    assert_parity(cg, x)
+    assert_parity(cg, synth.clustered_bytes(7, 3000, 96, 5, 2))
