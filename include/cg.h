@@ -45,7 +45,7 @@ enum {
   CG_EINPUT = -2,   /* an input byte is not 0 or 1 (G5), or set pad bits in packed input */
   CG_ENOMEM = -3,   /* device (or pinned host) allocation failed */
   CG_ECUDA = -4,    /* a CUDA runtime error (kernel launch, sticky error) */
-  CG_ETOOBIG = -5,  /* n >= 2^32 (cell and edge indices are u32, G11) */
+  CG_ETOOBIG = -5,  /* n >= 2^32 (cell indices are u32, G11); int32 index outputs with >= 2^31 cells */
   CG_EARCH = -6,    /* the current device is not sm_100 (B200) */
   CG_ENOTIMPL = -7  /* option not implemented */
 };
@@ -68,8 +68,12 @@ typedef struct {
   int64_t n_edges;
 } cg_edges;
 
-/* Opaque, immutable dictionary over a cell table (the popcount-layered,
- * prefix-indexed sorted array built by cg_build_ex, see DESIGN.md a4-a5). */
+/* Opaque, immutable dictionary over a cell table, built by cg_build_ex when
+ * cg_opts.index_out is set: with CG_DICT_GLOBAL (default) a copy of the
+ * canonical table plus its 2^b prefix index and prefix filter; with
+ * CG_DICT_SORTED / CG_DICT_BSEARCH the popcount-layered arrays (DESIGN.md
+ * a4-a5).  The dictionary replaces the paper's search tree (P:205-212,
+ * P:276-281). */
 typedef struct cg_index cg_index;
 
 /* Per-stage device times (CUDA events on the build stream, microseconds)
@@ -107,10 +111,17 @@ typedef struct {
                            full LSD fallback), 1 = full LSD only */
   cg_index** index_out; /* if non-NULL, receives the dictionary (release with cg_index_free) */
   cg_stats* stats;      /* if non-NULL, stage times and counters */
+  int32_t filter_extra; /* prefix filter resolution: b + filter_extra prefix bits per filter
+                           slot, in [0, 8]; -1 = default (5 global, 7 layered).  Changes
+                           only how many probes reach a bucket search, never the result */
+  int32_t reserved0;    /* must be 0 */
+  int64_t edge_cap;     /* initial capacity (edges) of the probe's hit buffer; 0 = default
+                           (4 per probed cell).  A larger m re-runs the probe at the exact
+                           size; only speed depends on it */
 } cg_opts;
 
 /* Fill *o with defaults: stream NULL, CG_DICT_GLOBAL, lcp_prune 1,
- * bucket_log2 -1, no index, no stats. */
+ * bucket_log2 -1, no index, no stats, filter_extra -1, edge_cap 0. */
 void cg_opts_init(cg_opts* o);
 
 /* Build the cell graph of vecs = uint8[n][ell] (device, row-major,
@@ -218,12 +229,16 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
                   uint64_t** h_cells, int64_t* n_cells, uint32_t** h_edges, int64_t* n_edges);
 void cg_host_free(void* p);
 
-/* Streaming query against a built index.  q = u64[nq][W] packed cells
- * (device; pad bits ignored, G19).  Writes (device)
+/* Streaming query against a built index: Alg. 4's lookups for
+ * a batch of vectors -- the vector itself and each of its ell single-bit
+ * flips x XOR e_k are searched in the dictionary.
+ * q = u64[nq][W] packed cells (device; pad bits ignored, G19).  Writes
+ * (device, caller-allocated)
  *   self_idx[r]        = canonical index of q_r, or -1 if q_r is not a cell;
  *   nbr_idx[r*ell + k] = canonical index of q_r with bit k negated, or -1.
  * Asynchronous on stream s (no host sync); nq == 0 is a no-op.
- * Errors: CG_EINVAL (NULL index, NULL pointers with nq > 0, nq < 0). */
+ * Errors: CG_EINVAL (NULL index, NULL pointers with nq > 0, nq < 0),
+ * CG_ETOOBIG (the index holds >= 2^31 cells: indices would not fit int32). */
 int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_idx,
              int32_t* nbr_idx, cg_stream_t s);
 

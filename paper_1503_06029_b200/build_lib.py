@@ -38,14 +38,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          defines: tuple = (), out: str | None = None) -> str:
+    """Build lib/libcg.so.  `defines` / `out` build a tuning variant of the
+    same sources (compile-time constants, e.g. ("PROBE_FR=6",)) into another
+    file for A/B timing (tools/ab_*.py); the product library is LIB."""
+    lib = out or LIB
+    if not force and not defines and lib == LIB and not _stale():
         return LIB
-    os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
-    extra = ["-Xptxas", "-v"] if ptxas_v else []
+    objdir = os.path.join(LIBDIR, "obj" if lib == LIB else "obj_" + os.path.basename(lib))
+    os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    extra = (["-Xptxas", "-v"] if ptxas_v else []) + ["-D" + d for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -59,13 +66,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             if err.strip():
                 sys.stderr.write(err)
     objs = [o for o, _ in results]
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -56,7 +56,8 @@ class cg_opts(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("dict_kind", ctypes.c_int32),
                 ("lcp_prune", ctypes.c_int32), ("bucket_log2", ctypes.c_int32),
                 ("sort_kind", ctypes.c_int32), ("index_out", ctypes.c_void_p),
-                ("stats", ctypes.POINTER(cg_stats))]
+                ("stats", ctypes.POINTER(cg_stats)), ("filter_extra", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("edge_cap", ctypes.c_int64)]
 
 
 _lib = None
@@ -271,10 +272,13 @@ class BuildResult:
 SORT_KINDS = {"auto": 0, "lsd": 1}
 
 
-def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats, sort_kind="auto"):
+def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats, sort_kind="auto",
+          filter_extra=-1, edge_cap=0):
     L = lib()
     o = cg_opts()
     L.cg_opts_init(ctypes.byref(o))
+    o.filter_extra = int(filter_extra)
+    o.edge_cap = int(edge_cap)
     o.stream = ctypes.c_void_p(stream.cuda_stream)
     o.dict_kind = DICT_KINDS[dict_kind] if isinstance(dict_kind, str) else int(dict_kind)
     o.lcp_prune = int(bool(lcp_prune))
@@ -296,7 +300,7 @@ def _stats_dict(st: cg_stats) -> dict:
 def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
           dict_kind="global", lcp_prune: bool = True, bucket_log2: int = -1,
           want_index: bool = False, want_stats: bool = False,
-          sort_kind="auto") -> BuildResult:
+          sort_kind="auto", filter_extra: int = -1, edge_cap: int = 0) -> BuildResult:
     """cg_build_ex on a CUDA uint8 tensor [n, ell] of 0/1 bytes."""
     if not isinstance(vecs, torch.Tensor) or vecs.dim() != 2:
         raise CgError(CG_EINVAL, "vecs must be a 2-D tensor [n, ell]")
@@ -308,7 +312,7 @@ def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
     n, ell = vecs.shape
     stream = stream or torch.cuda.current_stream(vecs.device)
     o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats,
-                      sort_kind)
+                      sort_kind, filter_extra, edge_cap)
     c, e = cg_cells(), cg_edges()
     with torch.cuda.device(vecs.device):
         _check(lib().cg_build_ex(ctypes.c_void_p(vecs.data_ptr()), n, ell, ctypes.byref(o),
@@ -323,14 +327,16 @@ def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
 
 
 def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="global",
-                 lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False):
+                 lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False,
+                 sort_kind="auto", filter_extra=-1, edge_cap=0):
     """cg_build_packed_ex on CUDA int64 [n, ceil(ell/64)] MSB-first words."""
     if words.dim() != 2 or words.dtype != torch.int64 or not words.is_cuda:
         raise CgError(CG_EINVAL, "words must be a CUDA int64 tensor [n, W]")
     words = words.contiguous()
     n = words.shape[0]
     stream = stream or torch.cuda.current_stream(words.device)
-    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats)
+    o, ih, st = _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats,
+                      sort_kind, filter_extra, edge_cap)
     c, e = cg_cells(), cg_edges()
     with torch.cuda.device(words.device):
         _check(lib().cg_build_packed_ex(ctypes.c_void_p(words.data_ptr()), n, ell,
@@ -585,10 +591,19 @@ def insert(cells: torch.Tensor, edges: torch.Tensor, vecs: torch.Tensor, *, stre
         raise CgError(CG_EINVAL, "cells must be a CUDA int64 tensor [n, W]")
     if vecs.dim() != 2 or vecs.dtype != torch.uint8 or not vecs.is_cuda:
         raise CgError(CG_EINVAL, "vecs must be a CUDA uint8 tensor [n_new, ell]")
-    cells, vecs = cells.contiguous(), vecs.contiguous()
-    m = edges.shape[0]
-    eptr = edges.contiguous().data_ptr() if m else 0
+    if (not isinstance(edges, torch.Tensor) or edges.dim() != 2 or edges.shape[1] != 2
+            or edges.dtype != torch.int32 or not edges.is_cuda):
+        raise CgError(CG_EINVAL, "edges must be a CUDA int32 tensor [m, 2]")
+    if cells.device != vecs.device or edges.device != cells.device:
+        raise CgError(CG_EINVAL, "cells, edges and vecs must be on the same device")
     n_new, ell = vecs.shape
+    if cells.shape[1] != (ell + 63) // 64:
+        raise CgError(CG_EINVAL, "cells must have ceil(ell/64) words per row")
+    # keep the contiguous copies alive until the call returns (the library
+    # allocates from the same caching allocator on the same stream)
+    cells, vecs, edges = cells.contiguous(), vecs.contiguous(), edges.contiguous()
+    m = edges.shape[0]
+    eptr = edges.data_ptr() if m else 0
     stream = stream or torch.cuda.current_stream(cells.device)
     o, _, _ = _opts(stream, "global", True, -1, False, False)
     c, e = cg_cells(), cg_edges()

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <climits>
+#include <new>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -79,8 +81,6 @@ struct AllocTimer {
   size_t bytes = 0;
   ~AllocTimer() {
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    if (us > 500 && std::getenv("CG_TRACE"))
-      std::fprintf(stderr, "[cg] slow device allocation: %zu bytes, %.0f us\n", bytes, us);
     g_alloc_us += us;
     ++g_nallocs;
   }
@@ -140,8 +140,6 @@ WsScope::WsScope() {
   Arena& a = cur_arena();
   if (a.depth++ > 0) return;
   if (a.want > a.cap) {
-    if (std::getenv("CG_TRACE"))
-      std::fprintf(stderr, "[cg] arena %zu -> %zu bytes\n", a.cap, a.want);
     if (a.base) {
       cudaDeviceSynchronize();
       if (g_dealloc) g_dealloc(a.base, nullptr, g_alloc_ctx);
@@ -325,6 +323,26 @@ static void check_arch() {
   if (major != 10) throw CgError{CG_EARCH, "cg is built for sm_100a (B200); device major = " + std::to_string(major)};
 }
 
+// Maps the exception in flight to a status code and records its detail: no
+// exception (CgError, std::bad_alloc, anything else) crosses the C ABI.
+static int current_error() {
+  try {
+    throw;
+  } catch (const CgError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return CG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return CG_ECUDA;
+  } catch (...) {
+    set_last_error("unknown exception");
+    return CG_ECUDA;
+  }
+}
+
 // ---------------------------------------------------------------- the pipeline
 struct Built {
   uint64_t* cells = nullptr;
@@ -386,7 +404,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   }
   int64_t ns = n;  // rows the full sort below orders
   if (!done) {
-    if (msd && n >= (int64_t(1) << 18) && !std::getenv("CG_NO_HASH_DEDUPE")) {
+    if (msd && n >= (int64_t(1) << 18)) {
       // a bucket overflowed: skewed data, typically few distinct cells and
       // heavy duplication -- drop the copies by hashing first, then
       // sort only the distinct rows
@@ -451,8 +469,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 0;
     int b = 0;
     while (b < 28 && (uint64_t(nc) >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
-    int fextra = 5;
-    if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
+    int fextra = o.filter_extra >= 0 ? o.filter_extra : 5;
     fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
     const Mem gix = o.index_out ? Mem::Persist : Mem::Scratch;  // T/F outlive the build
     DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
@@ -469,11 +486,16 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       i_hi = nc * (sh.rank + 1) / sh.world;
     }
     const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
-    DevBuf<uint32_t> tinfo(2 * size_t(ntiles), s);  // [count | block position]
+    DevBuf<uint32_t> tcnt(size_t(ntiles), s);  // hits per tile
+    DevBuf<uint64_t> tpos(size_t(ntiles), s);  // block position in the scratch list (~0: overflow)
     DevBuf<uint32_t> ticket(2, s);
     DevBuf<unsigned long long> ctr(4, s);
     DevBuf<uint4> ovf(size_t(ntiles), s);
-    uint64_t cap = std::max<uint64_t>(2 * uint64_t(i_hi - i_lo), 1 << 16);
+    // scratch capacity: 4 hits per cell covers planted sets (m/n_c = 0.5) and
+    // arrangement samples (degree ~ 2d, m/n_c <= 3 in R^3) in one probe pass;
+    // a larger m (P:106 allows n_c*ell/2) costs one re-run at the exact size
+    uint64_t cap = std::max<uint64_t>(4 * uint64_t(i_hi - i_lo), 1 << 16);
+    if (o.edge_cap > 0) cap = uint64_t(o.edge_cap);
     DevBuf<uint64_t> hits(cap, s);  // tile blocks of sorted (i << 32 | j)
     unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
     int reruns = 0;
@@ -481,7 +503,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     while (true) {
       CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
       CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
-      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tinfo.p, ticket.p, ctr.p,
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tcnt.p, tpos.p, ticket.p, ctr.p,
                           ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
       CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -495,11 +517,11 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       ++reruns;
     }
     tm.mark();  // 6: probe
-    // ---- canonical placement of the tile blocks: offsets = exclusive scan
-    // of the tile counts (overflow tiles included), then one copy
-    DevBuf<uint32_t> toff(size_t(ntiles), s);
-    CG_CUDA(cudaMemcpyAsync(toff.p, tinfo.p, size_t(ntiles) * 4, cudaMemcpyDeviceToDevice, s));
-    launch_scan_u32(toff.p, ntiles, s);
+    // ---- canonical placement of the tile blocks: 64-bit offsets = exclusive
+    // scan of the tile counts (overflow tiles included; m may exceed 2^32,
+    // P:106), then one copy
+    DevBuf<uint64_t> toff(size_t(ntiles), s);
+    launch_scan_u32_u64(tcnt.p, toff.p, ntiles, s);
     uint64_t mt = m;  // total including overflow tiles
     if (novf) {
       std::vector<uint4> hv(novf);
@@ -508,24 +530,28 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       for (const uint4& t : hv) mt += t.z;
     }
     uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(mt, 1) * 8, s));
-    launch_tile_copy(hits.p, toff.p, tinfo.p + ntiles, tinfo.p, ntiles, eout, s);
+    launch_tile_copy(hits.p, toff.p, tpos.p, tcnt.p, ntiles, eout, s);
     if (novf) {
       // tiles whose hits overflowed a warp buffer (dense graphs): re-run all
       // of them at once in spill mode, sort the spilled hits (tiles cover
       // disjoint source ranges, so the sorted list is the tiles' lists in
       // tile order) and drop each tile's part at its canonical offset
       const uint64_t ms = mt - m;
+      if (ms >= (uint64_t(1) << 32))
+        throw CgError{CG_ETOOBIG, ">= 2^32 edges from dense overflow tiles"};
+      hits.reset();
       DevBuf<uint8_t> sel(size_t(ntiles), s);
-      DevBuf<uint32_t> sstart(size_t(ntiles), s);
+      DevBuf<uint32_t> scnt(size_t(ntiles), s);
+      DevBuf<uint64_t> sstart(size_t(ntiles), s);
       CG_CUDA(cudaMemsetAsync(sel.p, 0, size_t(ntiles), s));
-      CG_CUDA(cudaMemsetAsync(sstart.p, 0, size_t(ntiles) * 4, s));
-      launch_spill_select(ovf.p, uint32_t(novf), sel.p, sstart.p, s);
-      launch_scan_u32(sstart.p, ntiles, s);
+      CG_CUDA(cudaMemsetAsync(scnt.p, 0, size_t(ntiles) * 4, s));
+      launch_spill_select(ovf.p, uint32_t(novf), sel.p, scnt.p, s);
+      launch_scan_u32_u64(scnt.p, sstart.p, ntiles, s);
       DevBuf<uint64_t> sp1(ms, s), sp2(ms, s);
       CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
       CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
-      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tinfo.p, ticket.p, ctr.p + 3,
-                          ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tcnt.p, tpos.p, ticket.p,
+                          ctr.p + 3, ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
       uint64_t* so = sp1.p;
       if (ms > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, int64_t(ms), 64, &so, nullptr, s, nullptr);
       launch_spill_place(so, int64_t(ms), i_lo, toff.p, sstart.p, eout, s);
@@ -592,8 +618,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   std::vector<uint64_t> h_base(2 * (ell + 1));  // [tbase | fbase]
   uint64_t tot = 0, ftot = 0;
   // filter resolution (tuning knob, ncu-driven): b_p + fextra prefix bits
-  int fextra = kFilterExtra;
-  if (const char* fe = std::getenv("CG_FILTER_EXTRA")) fextra = std::max(0, std::min(8, std::atoi(fe)));
+  const int fextra = o.filter_extra >= 0 ? o.filter_extra : kFilterExtra;
   for (int p = 0; p <= ell; ++p) {
     const uint64_t sz = h_off[p + 1] - h_off[p];
     int b = 0;
@@ -658,14 +683,11 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     ++reruns;
   }
   tm.mark();  // 6: probe
-  // ---- a7 canonical order: radix sort of (i << 32 | j); CG_EDGE_PLACE=1
-  // selects placement by source cell (count, scan, place, fix), which
-  // measured slower at C5 (3.6 vs 3.0 ms: scattered counter atomics)
+  // ---- a7 canonical order: radix sort of (i << 32 | j)
+  if (m >= (uint64_t(1) << 32))
+    throw CgError{CG_ETOOBIG, "layered dictionary: >= 2^32 edges (use CG_DICT_GLOBAL)"};
   uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(m, 1) * 8, s));
-  static const bool edge_place = std::getenv("CG_EDGE_PLACE") && std::atoi(std::getenv("CG_EDGE_PLACE")) == 1;
-  if (edge_place) {
-    place_edges(eb.p, int64_t(m), nc, eout, s);
-  } else {
+  {
     uint64_t* eo = eb.p;
     DevBuf<uint64_t> eb_alt(std::max<uint64_t>(m, 1), s);
     if (m > 1) radix_sort<uint64_t>(eb.p, eb_alt.p, nullptr, nullptr, nullptr, false, int64_t(m), 64, &eo, nullptr, s, nullptr);
@@ -737,6 +759,15 @@ static int finish(int rc, const Built& b, cg_cells* cells, cg_edges* edges, cons
   return rc;
 }
 
+static void validate_opts(const cg_opts& o) {
+  if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
+      o.dict_kind != CG_DICT_GLOBAL)
+    throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
+  if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
+  if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};
+  if (o.reserved0 != 0) throw CgError{CG_EINVAL, "reserved0 must be 0"};
+}
+
 static int validate_common(int64_t n, int32_t ell, const void* p, cg_cells* cells, cg_edges* edges) {
   if (!cells || !edges) throw CgError{CG_EINVAL, "cells/edges out-pointers must not be NULL"};
   if (!p) throw CgError{CG_EINVAL, "input pointer is NULL"};
@@ -775,28 +806,16 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
         throw CgError{CG_EINVAL, "dim must be in [1, 16]"};
       if (!pin->planes) throw CgError{CG_EINVAL, "planes is NULL"};
     }
-    if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
-        o.dict_kind != CG_DICT_GLOBAL)
-      throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
-    static const bool trace = std::getenv("CG_TRACE") != nullptr;
-    auto lap = [&](const char* what) {
-      if (trace)
-        std::fprintf(stderr, "[cg] %-12s %9.1f us\n", what,
-                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
-    };
+    validate_opts(o);
     check_arch();
-    lap("arch");
     check_device_ptr(in0, "input");
     if (pin) check_device_ptr(pin->planes, "planes");
-    lap("ptr");
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     const int W = (ell + 63) / 64;
     WsScope ws;
-    lap("arena");
     StageTimer tm;
     tm.start(o.stats != nullptr, s);  // 0
-    lap("events");
     setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
@@ -810,21 +829,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     // the pack kernel's per-tile counts of the first sort pass's digit (that
     // pass then needs no look-back)
     DevBuf<uint32_t> tile_hist(msd ? size_t((n + msd_tile_rows(W) - 1) / msd_tile_rows(W)) * 256 : 1, s);
-    // scatter pack (CG_SCATTER=1): rows go straight into their top-B-bit
-    // bucket via per-bucket atomic cursors, so the sort needs no global radix
-    // pass.  Measured at C5: sort 4.25 -> 2.33 ms but pack 1.53 -> 6.5 ms
-    // (2^26 scattered L2 atomics), so it is off by default.
-    const bool scatter = vecs && msd && B <= 16 && pack_scatter_ok(vecs, ell) &&
-                         std::getenv("CG_SCATTER") != nullptr;
-    DevBuf<uint32_t> boff(scatter ? (size_t(1) << B) + 1 : 1, s);
-    DevBuf<uint32_t> bcur(scatter ? (size_t(1) << B) : 1, s);
-    if (scatter) {
-      CG_CUDA(cudaMemsetAsync(boff.p, 0, boff.n * 4, s));
-      CG_CUDA(cudaMemsetAsync(bcur.p, 0, bcur.n * 4, s));
-      launch_prefix_hist(vecs, n, ell, B, boff.p, s);
-      launch_scan_u32(boff.p, int64_t(boff.n), s);  // boff[2^B] = n
-      launch_pack_scatter(vecs, n, ell, B, boff.p, bcur.p, keys.p, flags.p, s);
-    } else if (vecs) {
+    if (vecs) {
       if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
       launch_pack(vecs, n, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo,
                   msd ? tile_hist.p : nullptr, msd_tile_rows(W));
@@ -838,22 +843,18 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     }
     tm.mark();  // 1: pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(),
-                    ((vecs || pin) && msd && !scatter) ? top_hist.p : nullptr,
-                    scatter ? boff.p : nullptr, B,
-                    (vecs && msd && !scatter) ? tile_hist.p : nullptr);
+                    ((vecs || pin) && msd) ? top_hist.p : nullptr, nullptr, B,
+                    (vecs && msd) ? tile_hist.p : nullptr);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);
     if (b.edges) dev_free(b.edges, nullptr);
     if (b.index) cg_index_free(b.index);
     if (cells) std::memset(cells, 0, sizeof(*cells));
     if (edges) std::memset(edges, 0, sizeof(*edges));
-    return e.code;
-  } catch (const std::exception& e) {
-    set_last_error(e.what());
-    return CG_ECUDA;
+    return rc_;
   }
   if (o.stats) {
     o.stats->us_host_setup = setup_us;
@@ -875,6 +876,7 @@ void cg_opts_init(cg_opts* o) {
   o->dict_kind = CG_DICT_GLOBAL;
   o->lcp_prune = 1;
   o->bucket_log2 = -1;
+  o->filter_extra = -1;
 }
 
 int cg_build(const uint8_t* vecs, int64_t n, int32_t ell, cg_cells* cells, cg_edges* edges) {
@@ -919,9 +921,13 @@ int cg_insert(const uint64_t* cells, int64_t n_cells, const uint32_t* edges, int
       throw CgError{CG_EINVAL, "NULL argument"};
     if (n_cells < 1 || n_edges < 0 || n_new < 1) throw CgError{CG_EINVAL, "n_cells >= 1, n_new >= 1"};
     if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
-    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    // self lookups into the existing table are int32 (-1 = absent)
+    if (n_cells > int64_t(INT32_MAX)) throw CgError{CG_ETOOBIG, "n_cells >= 2^31"};
+    if (n_edges >= (int64_t(1) << 32)) throw CgError{CG_ETOOBIG, "n_edges >= 2^32"};
     check_arch();
     check_device_ptr(cells, "cells");
+    if (n_edges > 0) check_device_ptr(edges, "edges");
+    check_device_ptr(vecs, "vecs");
     // 1. the batch alone: sorted unique cells + its internal edges
     cg_opts ob;
     cg_opts_init(&ob);
@@ -952,15 +958,15 @@ int cg_insert(const uint64_t* cells, int64_t n_cells, const uint32_t* edges, int
     edges_out->ij = reinterpret_cast<uint32_t*>(eout);
     edges_out->n_edges = m;
     cout = eout = nullptr;
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (cout) dev_free(cout, nullptr);
     if (eout) dev_free(eout, nullptr);
     if (cells_out) std::memset(cells_out, 0, sizeof(*cells_out));
     if (edges_out) std::memset(edges_out, 0, sizeof(*edges_out));
     cg_cells_free(&bc);
     cg_edges_free(&be);
-    return e.code;
+    return rc_;
   }
   cg_cells_free(&bc);
   cg_edges_free(&be);
@@ -1003,11 +1009,11 @@ int cg_allpairs(const uint64_t* cells, int64_t n_cells, int32_t ell, int32_t anc
     edges->ij = reinterpret_cast<uint32_t*>(eout);
     edges->n_edges = int64_t(m);
     if (pairs_compared) *pairs_compared = int64_t(cmp);
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (eout) dev_free(eout, nullptr);
     if (edges) std::memset(edges, 0, sizeof(*edges));
-    return e.code;
+    return rc_;
   }
   return CG_OK;
 }
@@ -1028,9 +1034,9 @@ int cg_csr(const uint32_t* edges, int64_t n_edges, int64_t n_cells, uint64_t* ro
     WsScope ws;
     build_csr(edges, n_edges, n_cells, row_ptr, col, s);
     CG_CUDA(cudaStreamSynchronize(s));
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
-    return e.code;
+  } catch (...) {
+    const int rc_ = current_error();
+    return rc_;
   }
   return CG_OK;
 }
@@ -1051,9 +1057,9 @@ int cg_bfs(const uint64_t* row_ptr, const uint32_t* col, int64_t n_cells, int64_
     const int ecc = bfs(row_ptr, col, n_cells, source, dist, parent, s);
     CG_CUDA(cudaStreamSynchronize(s));
     if (eccentricity) *eccentricity = ecc;
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
-    return e.code;
+  } catch (...) {
+    const int rc_ = current_error();
+    return rc_;
   }
   return CG_OK;
 }
@@ -1078,9 +1084,9 @@ int cg_signatures(const double* points, int64_t n, int32_t dim, const double* pl
     CG_CUDA(cudaMemcpyAsync(h, flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     CG_CUDA(cudaStreamSynchronize(s));
     if (h[0]) throw CgError{CG_EINPUT, "non-finite constraint value (NaN/inf in points or planes)"};
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
-    return e.code;
+  } catch (...) {
+    const int rc_ = current_error();
+    return rc_;
   }
   return CG_OK;
 }
@@ -1123,13 +1129,27 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
     const int64_t nchunk_rows = std::min<int64_t>(chunk_rows, n);
     stage[0].alloc(size_t(nchunk_rows * row_bytes), s);
     stage[1].alloc(size_t(nchunk_rows * row_bytes), s);
-    cudaStream_t cs;
-    CG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    cudaEvent_t ev_copied[2], ev_packed[2];
+    // copy stream and events are released on every exit path
+    struct CopyCtx {
+      cudaStream_t cs = nullptr;
+      cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_packed[2] = {nullptr, nullptr};
+      ~CopyCtx() {
+        if (cs) cudaStreamSynchronize(cs);
+        for (int i = 0; i < 2; ++i) {
+          if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
+          if (ev_packed[i]) cudaEventDestroy(ev_packed[i]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+      }
+    } cc;
+    CG_CUDA(cudaStreamCreateWithFlags(&cc.cs, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
-      CG_CUDA(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
-      CG_CUDA(cudaEventCreateWithFlags(&ev_packed[i], cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&cc.ev_copied[i], cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&cc.ev_packed[i], cudaEventDisableTiming));
     }
+    cudaStream_t cs = cc.cs;
+    cudaEvent_t* ev_copied = cc.ev_copied;
+    cudaEvent_t* ev_packed = cc.ev_packed;
     // the stage buffers were allocated on s: make the copy stream wait for that
     CG_CUDA(cudaEventRecord(ev_packed[0], s));
     CG_CUDA(cudaEventRecord(ev_packed[1], s));
@@ -1149,11 +1169,6 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
       ++k;
     }
     CG_CUDA(cudaStreamSynchronize(s));
-    for (int i = 0; i < 2; ++i) {
-      cudaEventDestroy(ev_copied[i]);
-      cudaEventDestroy(ev_packed[i]);
-    }
-    cudaStreamDestroy(cs);
     stage[0].reset();
     stage[1].reset();
     tm.mark();  // 1: H2D + pack
@@ -1177,14 +1192,14 @@ int cg_build_host(const uint8_t* h_vecs, int64_t n, int32_t ell, const cg_opts* 
     if (o.index_out) *o.index_out = b.index;
     else if (b.index) cg_index_free(b.index);
     return CG_OK;
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);
     if (b.edges) dev_free(b.edges, nullptr);
     if (b.index) cg_index_free(b.index);
     host_pool_free(hc);
     host_pool_free(he);
-    return e.code;
+    return rc_;
   }
 }
 
@@ -1197,14 +1212,16 @@ int cg_query(const cg_index* idx, const uint64_t* q, int64_t nq, int32_t* self_i
     if (nq < 0) throw CgError{CG_EINVAL, "nq < 0"};
     if (nq == 0) return CG_OK;
     if (!q || !self_idx || !nbr_idx) throw CgError{CG_EINVAL, "NULL query/output pointer"};
+    const int64_t ncx = idx->global ? idx->gview.n_cells : idx->view.n_cells;
+    if (ncx > int64_t(INT32_MAX)) throw CgError{CG_ETOOBIG, "index has >= 2^31 cells (int32 outputs)"};
     if (idx->global)
       launch_query_global(idx->gview, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
     else
       launch_query(idx->view, q, nq, self_idx, nbr_idx, reinterpret_cast<cudaStream_t>(s));
     return CG_OK;
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
-    return e.code;
+  } catch (...) {
+    const int rc_ = current_error();
+    return rc_;
   }
 }
 
@@ -1295,10 +1312,10 @@ int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_op
     sh.cells_only = true;
     build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh);
     store_counters(o.stats);
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);
-    return e.code;
+    return rc_;
   }
   run->words = b.cells;
   run->n_cells = b.n_cells;
@@ -1365,11 +1382,11 @@ int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, 
                     msd ? boff.p : nullptr, B);
     fill_stats(tm, total, o.stats);
     store_counters(o.stats);
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);
     if (b.edges) dev_free(b.edges, nullptr);
-    return e.code;
+    return rc_;
   }
   table->words = b.cells;
   table->n_cells = b.n_cells;
@@ -1400,35 +1417,39 @@ int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G,
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     WsScope ws;
-    // (i, j) u32 pairs -> (i << 32 | j) keys, canonical sort, back to pairs.
-    // The per-rank lists are disjoint (each edge is emitted by the rank that
-    // owns its smaller endpoint), so no dedupe is needed.
     const uint64_t* src = reinterpret_cast<const uint64_t*>(gathered);
-    DevBuf<uint64_t> cat(size_t(std::max<int64_t>(m, 1)), s), k1(size_t(std::max<int64_t>(m, 1)), s),
-        k2(size_t(std::max<int64_t>(m, 1)), s);
-    int64_t at = 0;
-    for (int g = 0; g < G; ++g) {
-      if (counts[g])
-        CG_CUDA(cudaMemcpyAsync(cat.p + at, src + int64_t(g) * stride, size_t(counts[g]) * 8,
-                                cudaMemcpyDeviceToDevice, s));
-      at += counts[g];
-    }
     eout = static_cast<uint64_t*>(dev_alloc(size_t(std::max<int64_t>(m, 1)) * 8, s));
-    if (m > 0 && o.dict_kind == CG_DICT_GLOBAL) {
+    if (o.dict_kind == CG_DICT_GLOBAL) {
       // global dictionary: rank g probed the g-th contiguous canonical range
-      // and its list is sorted, so the concatenation is the canonical list
-      CG_CUDA(cudaMemcpyAsync(eout, cat.p, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+      // and its list is sorted, so the concatenation IS the canonical list:
+      // each list is copied once, straight to its offset
+      int64_t at = 0;
+      for (int g = 0; g < G; ++g) {
+        if (counts[g])
+          CG_CUDA(cudaMemcpyAsync(eout + at, src + int64_t(g) * stride, size_t(counts[g]) * 8,
+                                  cudaMemcpyDeviceToDevice, s));
+        at += counts[g];
+      }
     } else if (m > 0) {
-      launch_rotate_edges(cat.p, m, k1.p, s);
+      // layer-sharded lists: (i, j) pairs -> (i << 32 | j) keys, canonical
+      // sort, back to pairs.  The lists are disjoint (each edge is emitted by
+      // the rank that owns its smaller endpoint), so no dedupe is needed.
+      if (m >= (int64_t(1) << 32)) throw CgError{CG_ETOOBIG, ">= 2^32 edges (layered finalize)"};
+      DevBuf<uint64_t> k1(size_t(m), s), k2(size_t(m), s);
+      int64_t at = 0;
+      for (int g = 0; g < G; ++g) {
+        if (counts[g]) launch_rotate_edges(src + int64_t(g) * stride, counts[g], k1.p + at, s);
+        at += counts[g];
+      }
       uint64_t* ko = k1.p;
       if (m > 1) radix_sort<uint64_t>(k1.p, k2.p, nullptr, nullptr, nullptr, false, m, 64, &ko, nullptr, s, nullptr);
       launch_rotate_edges(ko, m, eout, s);
     }
     CG_CUDA(cudaStreamSynchronize(s));
-  } catch (const CgError& e) {
-    set_last_error(e.msg);
+  } catch (...) {
+    const int rc_ = current_error();
     if (eout) dev_free(eout, nullptr);
-    return e.code;
+    return rc_;
   }
   edges->ij = reinterpret_cast<uint32_t*>(eout);
   edges->n_edges = m;

@@ -361,6 +361,8 @@ void insert_merge(const uint64_t* cv_rows, int64_t nv, const uint32_t* ev, int64
   CG_CUDA(cudaStreamSynchronize(s));
   const int64_t mn = int64_t(hc[0]) + int64_t(hc[1]);
   const int64_t m = mv + mn;
+  // the merge ranks new edge keys among the old ones in 32 bits
+  if (m >= (int64_t(1) << 32)) throw CgError{CG_ETOOBIG, "merged edge list has >= 2^32 edges"};
   DevBuf<uint64_t> nk_alt(std::max<size_t>(1, size_t(mn)), s);
   uint64_t* ns = nk.p;
   if (mn > 1) radix_sort<uint64_t>(nk.p, nk_alt.p, nullptr, nullptr, nullptr, false, mn, 64, &ns, nullptr, s, nullptr);

@@ -104,14 +104,6 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
                      const uint32_t* tile_hist = nullptr, const uint32_t* side_dev = nullptr,
                      uint32_t* side_host = nullptr);
 int msd_tile_rows(int W);
-// MSD scatter pack (W <= 2, ell % 16 == 0, 16-byte aligned rows): histogram of
-// the top B bits from the first 16 bytes of each row, then pack straight into
-// the prefix buckets (start = exclusive scan of the histogram, cursor zeroed).
-bool pack_scatter_ok(const uint8_t* vecs, int ell);
-void launch_prefix_hist(const uint8_t* vecs, int64_t n, int ell, int B, uint32_t* hist,
-                        cudaStream_t s);
-void launch_pack_scatter(const uint8_t* vecs, int64_t n, int ell, int B, const uint32_t* start,
-                         uint32_t* cursor, uint64_t* keys, uint32_t* err, cudaStream_t s);
 // popcount (optional) and lcp with the next cell, for a canonical table
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
                       cudaStream_t s);
@@ -176,9 +168,6 @@ void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* 
 constexpr int kWeightTile = 4096;
 void launch_probe_weights(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
                           int lcp_prune, uint32_t* tile_w, cudaStream_t s);
-// Canonical (i, j) u32 pairs from unordered (i << 32 | j) hits without a
-// full sort (count per source, scan, place, per-cell fix-up); edges.cu.
-void place_edges(const uint64_t* hits, int64_t m, int64_t nc, uint64_t* out, cudaStream_t s);
 // (i << 32 | j) -> u32 pair (i, j) little-endian.
 void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStream_t s);
 
@@ -198,32 +187,34 @@ struct GlobalDict {
 };
 void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
                         uint32_t* F, cudaStream_t s);
-// Each tile of 256 cells writes its sorted hits (i << 32 | j) as one block of
-// out[0..cap) (reserved by atomicAdd on *total) and records status[t] =
-// count, status[ntiles + t] = block position (status: u32[2 * ntiles]).
-// Tiles whose hits overflow the shared buffer are listed in ovf (tile, -,
-// count) and must be re-run in spill mode (spill != nullptr: unordered
-// append to spill[0..spill_cap), *spill_n).
+// Each tile of 32 cells writes its sorted hits (i << 32 | j) as one block of
+// out[0..cap) (reserved by atomicAdd on *total) and records tcnt[t] = count,
+// tpos[t] = block position (~0 for an overflow tile).  Tiles whose hits
+// overflow the warp buffer are listed in ovf (tile, -, count) and must be
+// re-run in spill mode (spill != nullptr: unordered append to
+// spill[0..spill_cap), *spill_n).
 void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
-                         uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
-                         unsigned long long* total, unsigned long long* issued, uint4* ovf,
-                         uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
+                         uint64_t* out, uint64_t cap, uint32_t* tcnt, uint64_t* tpos,
+                         uint32_t* ticket, unsigned long long* total, unsigned long long* issued,
+                         uint4* ovf, uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
                          unsigned long long* spill_n, cudaStream_t s,
                          const uint8_t* tile_sel = nullptr);
 // overflow tiles (batched spill path): selection mask + per-tile counts
 void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t* scnt,
                          cudaStream_t s);
 // sorted spilled hits -> out[toff[t] + q - sstart[t]] as (i, j) pairs
-void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint32_t* toff,
-                        const uint32_t* sstart, uint64_t* out, cudaStream_t s);
+void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint64_t* toff,
+                        const uint64_t* sstart, uint64_t* out, cudaStream_t s);
 // place every tile block at its canonical offset off[t] as (i, j) pairs
-void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
+void launch_tile_copy(const uint64_t* scratch, const uint64_t* off, const uint64_t* pos,
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s);
 int64_t probe_global_tiles(int64_t n);
 int probe_global_tile_cells();
 int probe_global_tile_edge_cap();
 // exclusive prefix sum of u32 in place (total < 2^32); edges.cu
 void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s);
+// out[i] = sum of in[0..i) in 64 bits (edge offsets: m may exceed 2^32)
+void launch_scan_u32_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- cg_query
 void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,

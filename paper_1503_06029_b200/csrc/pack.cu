@@ -138,65 +138,6 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
   }
 }
 
-// ---------------------------------------------------------------- MSD scatter path
-// (W <= 2, ell % 16 == 0).  A pre-pass reads only the first 16 bytes of each
-// row and histograms the top B <= 16 bits; after a scan of the 2^B counts
-// the pack kernel writes every packed row straight into its prefix bucket
-// (slot = bucket start + atomicAdd(cursor)), so the sort needs no global
-// radix pass: the bucket pass sorts within buckets anyway.
-__global__ void __launch_bounds__(256) k_prefix_hist(const uint8_t* __restrict__ vecs, int64_t n,
-                                                     int ell, int B, uint32_t* __restrict__ hist) {
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-       r += int64_t(gridDim.x) * blockDim.x) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(vecs + r * ell));
-    const uint64_t lo = (uint64_t(v.y) << 32) | v.x;
-    const uint64_t hi = (uint64_t(v.w) << 32) | v.z;
-    const uint32_t top16 = (bits8_msb(lo) << 8) | bits8_msb(hi);
-    atomicAdd(hist + (top16 >> (16 - B)), 1u);
-  }
-}
-
-template <int W>
-__global__ void __launch_bounds__(256)
-    k_pack_scatter(const uint8_t* __restrict__ vecs, int64_t n, int ell, int B,
-                   const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
-                   uint64_t* __restrict__ keys, uint32_t* __restrict__ err) {
-  uint64_t bad = 0;
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-       r += int64_t(gridDim.x) * blockDim.x) {
-    const uint4* p = reinterpret_cast<const uint4*>(vecs + r * ell);
-    uint64_t w[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-      const int len = min(64, ell - 64 * q);
-      uint4 v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (16 * c < len) v[c] = __ldcs(p + 4 * q + c);
-      uint64_t word = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (16 * c < len) {
-          const uint64_t lo = (uint64_t(v[c].y) << 32) | v[c].x;
-          const uint64_t hi = (uint64_t(v[c].w) << 32) | v[c].z;
-          bad |= (lo | hi) & kHi7;
-          word |= uint64_t(bits8_msb(lo)) << (56 - 16 * c);
-          word |= uint64_t(bits8_msb(hi)) << (48 - 16 * c);
-        }
-      }
-      w[q] = word;
-    }
-    const uint32_t bk = uint32_t(w[0] >> (64 - B));
-    const uint32_t slot = start[bk] + atomicAdd(cursor + bk, 1u);
-    if (W == 2) {
-      *reinterpret_cast<ulonglong2*>(keys + 2 * int64_t(slot)) = make_ulonglong2(w[0], w[W - 1]);
-    } else {
-      keys[slot] = w[0];
-    }
-  }
-  if (bad) atomicOr(err, 1u);
-}
-
 __global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W, uint64_t pad,
                             uint32_t* __restrict__ err) {
   uint64_t bad = 0;
@@ -226,26 +167,6 @@ void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32
   } else {
     k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
   }
-  CG_LAUNCH_CHECK();
-}
-
-bool pack_scatter_ok(const uint8_t* vecs, int ell) {
-  return ell % 16 == 0 && ell <= 128 && (reinterpret_cast<uintptr_t>(vecs) % 16) == 0;
-}
-
-void launch_prefix_hist(const uint8_t* vecs, int64_t n, int ell, int B, uint32_t* hist,
-                        cudaStream_t s) {
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8);
-  k_prefix_hist<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(vecs, n, ell, B, hist);
-  CG_LAUNCH_CHECK();
-}
-
-void launch_pack_scatter(const uint8_t* vecs, int64_t n, int ell, int B, const uint32_t* start,
-                         uint32_t* cursor, uint64_t* keys, uint32_t* err, cudaStream_t s) {
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8);
-  const unsigned g = unsigned(std::max<int64_t>(1, blocks));
-  if (ell <= 64) k_pack_scatter<1><<<g, 256, 0, s>>>(vecs, n, ell, B, start, cursor, keys, err);
-  else k_pack_scatter<2><<<g, 256, 0, s>>>(vecs, n, ell, B, start, cursor, keys, err);
   CG_LAUNCH_CHECK();
 }
 

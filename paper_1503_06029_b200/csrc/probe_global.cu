@@ -41,6 +41,9 @@ constexpr int kTileEdgeCap = kWarpEdgeCap;
 #ifndef PROBE_MIN_BLOCKS
 #define PROBE_MIN_BLOCKS 6  // 40 registers, 6 CTAs (48 warps) per SM
 #endif
+#ifndef PROBE_FR
+#define PROBE_FR 5  // filter loads in flight per round
+#endif
 
 template <int WC>
 struct GRow {
@@ -65,10 +68,11 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 
 // FR: filter loads in flight per lane and round; NR / SR: near rows and
 // survivor-bucket rows compared per round (A/B at C5: FR 3-6, NR/SR 1, 2, 4)
-template <int WC, int FR = 5, int NR = 2, int SR = 2>
+template <int WC, int FR = PROBE_FR, int NR = 2, int SR = 2>
 __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
-                   uint64_t* __restrict__ out, uint64_t cap, uint32_t* status, uint32_t* ticket,
+                   uint64_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ tcnt,
+                   uint64_t* __restrict__ tpos, uint32_t* ticket,
                    unsigned long long* total, unsigned long long* issued,
                    uint64_t* __restrict__ spill, uint64_t spill_cap, unsigned long long* spill_n,
                    uint4* __restrict__ ovf, uint32_t* ovf_n,
@@ -90,13 +94,14 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     if (tile_sel && !tile_sel[tile]) continue;  // spill re-run: only the overflow tiles
     uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
     const int64_t i = i_lo + tile * kTileCells + lane;
-    const bool valid = i < i_hi;
+    const bool valid = i < i_hi;           // this lane probes cell i
+    const bool row_ok = i < g.n_cells;     // row i exists (a shuffle source past i_hi)
     // ---- the cell
-    const uint64_t* Vp = g.keys + (valid ? i : 0) * W;
+    const uint64_t* Vp = g.keys + (row_ok ? i : 0) * W;
     uint64_t v[WC > 0 ? WC : 1];
     if (WC > 0) {
 #pragma unroll
-      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) v[w] = valid ? Vp[w] : 0ull;
+      for (int w = 0; w < (WC > 0 ? WC : 1); ++w) v[w] = row_ok ? Vp[w] : 0ull;
     }
     auto V = [&](int w) -> uint64_t {
       if (WC > 0) {
@@ -111,17 +116,22 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     int kmax = -1;
     // the next row is the neighbouring lane's cell: take it by shuffle
     // (lane 31 and the end of the range load it)
+    const bool nx_ok = i + 1 < g.n_cells;  // row i has a successor row
     uint64_t nxt[WC > 0 ? WC : 1];
     if (WC > 0) {
 #pragma unroll
       for (int w = 0; w < (WC > 0 ? WC : 1); ++w) nxt[w] = __shfl_down_sync(kFull, v[w], 1);
+      if (lane == 31 && nx_ok) {
+#pragma unroll
+        for (int w = 0; w < (WC > 0 ? WC : 1); ++w) nxt[w] = Vp[W + w];
+      }
     }
     if (valid) {
       if (lcp_prune) {
         // lcp(V_i, V_{i+1}); the last cell has no successor and probes nothing
-        if (i + 1 < g.n_cells) {
+        if (nx_ok) {
           const uint64_t* Np = g.keys + (i + 1) * W;
-          const bool shfl = WC > 0 && lane < 31 && i + 1 < i_hi;
+          const bool shfl = WC > 0;
           int l = -1;
           const int n = WC > 0 ? WC : W;
           for (int w = 0; w < n && l < 0; ++w) {
@@ -467,23 +477,23 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         }
       }
     }
-    uint32_t bs = 0;
+    // block positions are 64-bit: m may exceed 2^32 (m <= n_c*ell/2)
+    uint64_t bs = 0;
     if (lane == 0) {
-      status[tile] = wfill;  // tile_cnt
+      tcnt[tile] = wfill;
       if (wfill > uint32_t(kWarpEdgeCap)) {
         // rare: hits beyond the warp buffer were dropped; the host re-runs
         // this tile in spill mode and writes its range directly
         const uint32_t k = atomicAdd(ovf_n, 1u);
         ovf[k] = make_uint4(uint32_t(tile), 0u, wfill, 0u);
-        bs = 0xffffffffu;
+        bs = ~0ull;
       } else if (wfill) {
-        bs = uint32_t(atomicAdd(total, (unsigned long long)wfill));
+        bs = atomicAdd(total, (unsigned long long)wfill);
       }
-      status[ntiles + tile] = bs;  // tile_pos in the scratch list
+      tpos[tile] = bs;  // position of the tile's block in the scratch list
     }
-    const uint32_t base = __shfl_sync(kFull, bs, 0);
-    if (base != 0xffffffffu && wn > 0) {
-      const uint64_t wpos = uint64_t(base);
+    const uint64_t wpos = __shfl_sync(kFull, bs, 0);
+    if (wpos != ~0ull && wn > 0) {
       if (wn <= 32) {
         // one hit per lane.  Every path above emits a source cell's hits in
         // ascending j (near rows in order, then flips from the least
@@ -539,7 +549,7 @@ void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fex
 }
 
 void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64_t i_hi,
-                         uint64_t* out, uint64_t cap, uint32_t* status, uint32_t* ticket,
+                         uint64_t* out, uint64_t cap, uint32_t* tcnt, uint64_t* tpos, uint32_t* ticket,
                          unsigned long long* total, unsigned long long* issued, uint4* ovf,
                          uint32_t* ovf_n, uint64_t* spill, uint64_t spill_cap,
                          unsigned long long* spill_n, cudaStream_t s, const uint8_t* tile_sel) {
@@ -547,9 +557,9 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
   if (ntiles <= 0) return;
   const int grid = int(std::min<int64_t>((ntiles + kProbeWarps - 1) / kProbeWarps, int64_t(num_sms()) * 8));
   switch (g.W) {
-    case 1: k_probe_global<1><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    case 2: k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    default: k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, status, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 1: k_probe_global<1><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 2: k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    default: k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
   }
   CG_LAUNCH_CHECK();
 }
@@ -566,7 +576,7 @@ __global__ void k_spill_select(const uint4* __restrict__ ovf, uint32_t novf, uin
 // sorted spilled hits -> their tiles' canonical ranges:
 // dst = toff[t] + (q - sstart[t]) with t the tile of the hit's source cell
 __global__ void k_spill_place(const uint64_t* __restrict__ sorted, int64_t m, int64_t i_lo,
-                              const uint32_t* __restrict__ toff, const uint32_t* __restrict__ sstart,
+                              const uint64_t* __restrict__ toff, const uint64_t* __restrict__ sstart,
                               uint64_t* __restrict__ out) {
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < m;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -582,8 +592,8 @@ void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t
   CG_LAUNCH_CHECK();
 }
 
-void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint32_t* toff,
-                        const uint32_t* sstart, uint64_t* out, cudaStream_t s) {
+void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint64_t* toff,
+                        const uint64_t* sstart, uint64_t* out, cudaStream_t s) {
   if (m <= 0) return;
   const int64_t blocks = std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 16);
   k_spill_place<<<unsigned(blocks), 256, 0, s>>>(sorted, m, i_lo, toff, sstart, out);
@@ -592,38 +602,40 @@ void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const u
 
 // Tile blocks -> canonical positions.  A CTA takes 256 consecutive tiles:
 // their destination ranges are contiguous (off = exclusive scan of the
-// counts), so the CTA flattens them -- thread per destination element, its
-// tile found by a binary search over the tiles' prefix in shared memory --
-// and writes one contiguous run as (i, j) u32 pairs.  Overflow tiles
-// (pos = 0xffffffff) are written by the spill path and skipped here.
+// counts, 64-bit), so the CTA flattens them -- thread per destination
+// element, its tile found by a binary search over the tiles' prefix in shared
+// memory -- and writes one contiguous run as (i, j) u32 pairs.  Overflow
+// tiles (pos = ~0) are written by the spill path and skipped here.
 constexpr int kCopyTiles = 256;
 
 __global__ void __launch_bounds__(256)
-    k_tile_copy(const uint64_t* __restrict__ scratch, const uint32_t* __restrict__ off,
-                const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cntv, int64_t ntiles,
+    k_tile_copy(const uint64_t* __restrict__ scratch, const uint64_t* __restrict__ off,
+                const uint64_t* __restrict__ pos, const uint32_t* __restrict__ cntv, int64_t ntiles,
                 uint64_t* __restrict__ out) {
-  __shared__ uint32_t s_pre[kCopyTiles + 1], s_pos[kCopyTiles];
+  __shared__ uint32_t s_pre[kCopyTiles + 1];
+  __shared__ uint64_t s_pos[kCopyTiles];
   for (int64_t t0 = int64_t(blockIdx.x) * kCopyTiles; t0 < ntiles;
        t0 += int64_t(gridDim.x) * kCopyTiles) {
     const int nt = int(ntiles - t0 < kCopyTiles ? ntiles - t0 : int64_t(kCopyTiles));
     __syncthreads();
-    const uint32_t base = off[t0];
+    const uint64_t base = off[t0];
+    // within 256 tiles the relative offsets fit 32 bits (<= 256 * 32 * ell hits)
     for (int q = threadIdx.x; q < nt; q += blockDim.x) {
-      s_pre[q] = off[t0 + q] - base;
+      s_pre[q] = uint32_t(off[t0 + q] - base);
       s_pos[q] = pos[t0 + q];
     }
-    if (threadIdx.x == 0) s_pre[nt] = off[t0 + nt - 1] - base + cntv[t0 + nt - 1];
+    if (threadIdx.x == 0) s_pre[nt] = uint32_t(off[t0 + nt - 1] - base) + cntv[t0 + nt - 1];
     __syncthreads();
     const uint32_t E = s_pre[nt];
     // 4 edges per thread and step: all four loads in flight before the stores
     constexpr int U = 4;
     for (uint32_t e0 = threadIdx.x; e0 < E; e0 += U * blockDim.x) {
-      uint32_t src[U];
+      uint64_t src[U];
       uint64_t k[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t e = e0 + u * blockDim.x;
-        src[u] = 0xffffffffu;
+        src[u] = ~0ull;
         if (e < E) {
           int lo = 0, hi = nt - 1;  // last tile with s_pre <= e
           while (lo < hi) {
@@ -631,21 +643,20 @@ __global__ void __launch_bounds__(256)
             if (s_pre[mid] <= e) lo = mid;
             else hi = mid - 1;
           }
-          const uint32_t p = s_pos[lo];
-          if (p != 0xffffffffu) src[u] = p + (e - s_pre[lo]);
+          const uint64_t p = s_pos[lo];
+          if (p != ~0ull) src[u] = p + (e - s_pre[lo]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) k[u] = src[u] != 0xffffffffu ? __ldcs(scratch + src[u]) : 0ull;
+      for (int u = 0; u < U; ++u) k[u] = src[u] != ~0ull ? __ldcs(scratch + src[u]) : 0ull;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (src[u] != 0xffffffffu)
-          out[uint64_t(base) + e0 + u * blockDim.x] = (k[u] >> 32) | (k[u] << 32);
+        if (src[u] != ~0ull) out[base + e0 + u * blockDim.x] = (k[u] >> 32) | (k[u] << 32);
     }
   }
 }
 
-void launch_tile_copy(const uint64_t* scratch, const uint32_t* off, const uint32_t* pos,
+void launch_tile_copy(const uint64_t* scratch, const uint64_t* off, const uint64_t* pos,
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s) {
   if (ntiles <= 0) return;
   const int64_t blocks = std::min<int64_t>((ntiles + kCopyTiles - 1) / kCopyTiles, int64_t(num_sms()) * 8);

@@ -19,11 +19,15 @@
 //   significant); digits are taken from the most significant word.
 //
 // (2) the cell sort for W <= 2 words (MSD fast path): LSD passes over only
-//   the top B bits move the whole keys into 2^B prefix buckets; a boundary
-//   kernel finds the bucket ranges; each bucket (~2^10 keys for uniform keys)
-//   is then fully sorted in shared memory by a bitonic network on the whole
-//   key.  A bucket larger than the shared-memory capacity makes the caller
-//   fall back to the full LSD sort (skewed data), which is always correct.
+//   the top B bits move the whole keys into 2^B prefix buckets (the first
+//   pass takes its tile offsets from the pack kernel's per-tile digit
+//   counts, so it needs no look-back); the bucket starts are found by one
+//   binary search per bucket; each bucket (~2^10 keys for uniform keys) is
+//   then sorted in shared memory by a rank-in-digit pass (k_bucket_rank: the
+//   first varying bit, an 11-bit digit count, ranks within a digit) with the
+//   dedupe of a3 fused in.  Skewed buckets go to a stable byte-pass kernel
+//   (k_bucket_sort); a bucket larger than its capacity makes the caller fall
+//   back to the full LSD sort (skewed data), which is always correct.
 //
 // (3) the multi-word LSD (W > 2): per word (least significant first) a
 //   stable sort of (word, u32 row index) pairs, then a row gather.
@@ -1026,8 +1030,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
     // rank pass: keys (double-buffered with PREF) + two u16 orders + the
     // long-digit list; 1.5x the mean bucket; larger buckets go to the byte passes
     const int rcap = avg <= 1024 ? 1536 : 2048;
-    static const bool pref = !(std::getenv("CG_RANK_PREF") && std::atoi(std::getenv("CG_RANK_PREF")) == 0);
-    const size_t smem = pref ? size_t(rcap) * (2 * sizeof(K) + 8) : size_t(rcap) * (sizeof(K) + 6);
+    const size_t smem = size_t(rcap) * (2 * sizeof(K) + 8);
     const int per_sm = std::max(1, int((222 << 10) / (smem + 10 * 1024)));
     const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
     auto go = [&](auto kern) {
@@ -1035,13 +1038,8 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
     };
-    if (rcap == 1536) {
-      if (pref) go(k_bucket_rank<K, 6, true>);
-      else go(k_bucket_rank<K, 6, false>);
-    } else {
-      if (pref) go(k_bucket_rank<K, 8, true>);
-      else go(k_bucket_rank<K, 8, false>);
-    }
+    if (rcap == 1536) go(k_bucket_rank<K, 6, true>);
+    else go(k_bucket_rank<K, 8, true>);
     CG_LAUNCH_CHECK();
   }
   const size_t smem = size_t(cap) * (sizeof(K) + 4);

@@ -31,6 +31,9 @@ class CudaOps:
     def local(self, vecs):
         from . import cg
 
+        if vecs.shape[0] == 0:  # an empty shard (uneven split, n < G): an empty run
+            return torch.zeros((0, (vecs.shape[1] + 63) // 64), dtype=torch.int64,
+                               device=vecs.device)
         return cg.dist_local(vecs, stream=self.stream)
 
     def merge_probe(self, runs, counts, rank, ell):

@@ -328,6 +328,48 @@ def hypercube(ell: int) -> np.ndarray:
     return ((v[:, None] >> sh[None, :]) & 1).astype(np.uint8)
 
 
+def grid_words_np(side: int, dims: int, perm_mult: int = 1) -> tuple[np.ndarray, int]:
+    """All cells of a `dims`-dimensional grid with `side` vertices per axis,
+    each axis a path embedded by the thermometer code 1^t 0^(side-1-t)
+    (t = 0..side-1), concatenated axis 0 first: ell = dims*(side-1) <= 64,
+    one packed word per cell (bit k = word bit 63-k).  Row r holds the grid
+    point whose mixed-radix number (axis 0 most significant) is
+    (r * perm_mult) mod side^dims (perm_mult coprime to side: a permutation).
+    Generated data only; what the cell graph of it is, is the tests' business."""
+    ell = dims * (side - 1)
+    assert ell <= 64
+    n = side ** dims
+    r = (np.arange(n, dtype=np.uint64) * np.uint64(perm_mult)) % np.uint64(n)
+    w = np.zeros(n, np.uint64)
+    for c in range(dims - 1, -1, -1):
+        t = r % np.uint64(side)
+        r //= np.uint64(side)
+        # thermometer code of t on bits c*(side-1) .. c*(side-1)+side-2
+        code = ((np.uint64(1) << t) - np.uint64(1)) << (np.uint64(side - 1) - t)
+        w |= code << np.uint64(64 - (c + 1) * (side - 1))
+    return w.reshape(n, 1), ell
+
+
+def grid_words_torch(side: int, dims: int, device, perm_mult: int = 1):
+    """grid_words_np on the device (torch int64 [n, 1] holding the u64 bit
+    patterns); for the full-size m >= 2^32 test."""
+    import torch
+
+    ell = dims * (side - 1)
+    assert ell <= 64
+    n = side ** dims
+    r = (torch.arange(n, dtype=torch.int64, device=device) * perm_mult) % n
+    w = torch.zeros(n, dtype=torch.int64, device=device)
+    one = torch.ones((), dtype=torch.int64, device=device)
+    for c in range(dims - 1, -1, -1):
+        t = r % side
+        r = r // side
+        code = ((one << t) - 1) << (side - 1 - t)
+        w |= code << (64 - (c + 1) * (side - 1))
+    del r
+    return w.view(n, 1), ell
+
+
 def random_bytes(seed: int, n: int, ell: int, dup_frac: float = 0.0, p_one: float = 0.5):
     rng = np.random.default_rng(seed)
     nu = max(1, int(round(n * (1.0 - dup_frac))))

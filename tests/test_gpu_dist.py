@@ -64,6 +64,11 @@ def test_logical_ranks_match_single_build(cg, G, dict_kind):
     want_c = res.cells.cpu().numpy().view(np.uint64)
     want_e = res.edges.cpu().numpy().view(np.uint32)
     c, e, ecounts = logical_ranks(cg, x, G, dict_kind)
+    # the oracle decides (P14 G-invariance on top: equal to the 1-GPU build)
+    rc, oc, oe = oracle.build(x)
+    assert rc == 0
+    np.testing.assert_array_equal(c, oc)
+    np.testing.assert_array_equal(e, oe)
     np.testing.assert_array_equal(c, want_c)
     np.testing.assert_array_equal(e, want_e)
     if G > 1:

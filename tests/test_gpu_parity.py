@@ -206,15 +206,25 @@ def test_multiset_x3_and_permutation(cg):
     np.testing.assert_array_equal(e0, e1)
 
 
-def test_options_agree(cg):
+@pytest.mark.parametrize("kw", [dict(), dict(lcp_prune=False), dict(dict_kind="bsearch"),
+                                dict(dict_kind="sorted"), dict(dict_kind="sorted", lcp_prune=False),
+                                dict(dict_kind="bsearch", lcp_prune=False), dict(bucket_log2=0),
+                                dict(bucket_log2=6), dict(dict_kind="sorted", bucket_log2=0),
+                                dict(edge_cap=1), dict(dict_kind="sorted", edge_cap=1)],
+                         ids=lambda kw: ",".join(f"{k}={v}" for k, v in kw.items()) or "default")
+def test_options_vs_oracle(cg, kw):
+    """Every dictionary / pruning / bucket / capacity option gives the oracle's
+    bytes on an arrangement-like clustered input (ell = 150, W = 3) and on a
+    C5-recipe planted input (W = 2)."""
     x = synth.clustered_bytes(8, 30000, 150, n_centers=8, max_flips=3)
-    c0, e0, r0 = gpu_build(cg, x, want_stats=True)
-    for kw in (dict(lcp_prune=False), dict(dict_kind="bsearch"), dict(dict_kind="sorted"),
-               dict(dict_kind="sorted", lcp_prune=False), dict(bucket_log2=0),
-               dict(bucket_log2=6)):
-        c1, e1, r1 = gpu_build(cg, x, want_stats=True, **kw)
-        np.testing.assert_array_equal(c0, c1)
-        np.testing.assert_array_equal(e0, e1)
+    assert_parity(cg, x, **kw)
+    d = synth.config("C5", scale_log2=15)
+    assert_parity(cg, synth.unpack_words_np(d["words"], 128), **kw)
+
+
+def test_lcp_prune_issues_fewer_probes(cg):
+    x = synth.clustered_bytes(8, 30000, 150, n_centers=8, max_flips=3)
+    _, _, r0 = gpu_build(cg, x, want_stats=True)
     _, _, rn = gpu_build(cg, x, want_stats=True, lcp_prune=False)
     assert r0.stats["issued_probes"] <= rn.stats["issued_probes"]
 
@@ -340,13 +350,22 @@ def test_heavy_duplication_hash_path(cg, ell, n):
     assert np.array_equal(cells, oc) and np.array_equal(edges, oe)
 
 
-@pytest.mark.parametrize("fextra", ["0", "2", "4", "5", "8"])
-def test_filter_resolution(cg, fextra, monkeypatch):
-    """The prefix filter's extra bits (CG_FILTER_EXTRA) change only which far
-    flips reach a bucket search, never the result; fextra >= 5 takes the
+@pytest.mark.parametrize("fextra", [0, 2, 4, 5, 8])
+@pytest.mark.parametrize("dict_kind", ["global", "sorted"])
+def test_filter_resolution(cg, fextra, dict_kind):
+    """The prefix filter's extra bits (cg_opts.filter_extra) change only which
+    far flips reach a bucket search, never the result; fextra >= 5 takes the
     probe's word-only filter test, smaller values the general one."""
-    monkeypatch.setenv("CG_FILTER_EXTRA", fextra)
     d = synth.config("C5", scale_log2=16)
     x = synth.unpack_words_np(d["words"], d["ell"])
-    assert_parity(cg, x)
-    assert_parity(cg, synth.clustered_bytes(7, 3000, 96, 5, 2))
+    assert_parity(cg, x, filter_extra=fextra, dict_kind=dict_kind)
+    assert_parity(cg, synth.clustered_bytes(7, 3000, 96, 5, 2), filter_extra=fextra,
+                  dict_kind=dict_kind)
+
+
+def test_bad_options_rejected(cg):
+    x = torch.zeros((10, 8), dtype=torch.uint8, device="cuda")
+    for kw in (dict(filter_extra=9), dict(filter_extra=-2), dict(edge_cap=-1)):
+        with pytest.raises(cg.CgError) as ei:
+            cg.build(x, **kw)
+        assert ei.value.code == -1

@@ -293,3 +293,44 @@ def test_degenerate_sizes():
     assert c.shape == (1, 1) and e.shape[0] == 0
     rc, c, e = oracle.build(np.array([[0], [1], [1], [0]], np.uint8))
     assert c[:, 0].tolist() == [0, 1 << 63] and e.tolist() == [[0, 1]]
+
+
+# ---------------------------------------------------------------- grid graphs (m >= 2^32 recipe)
+def grid_closed_form(side: int, dims: int):
+    """Cell graph of the thermometer-coded grid [side]^dims (synth.grid_words_np):
+    Hamming distance 1 between two codes <=> grid neighbours (one axis moves by
+    one step), and the canonical order is the mixed-radix order with axis 0
+    most significant (00..0 < 10..0 < 110..0 < ... per axis).  So V_i = grid
+    point i, and E = {(i, i + side^p) : digit p of i < side - 1}, ascending;
+    n_c = side^dims, m = dims (side - 1) side^(dims - 1)."""
+    n = side ** dims
+    i = np.arange(n, dtype=np.int64)
+    rows = []
+    for p in range(dims):  # ascending p = ascending j for a fixed i
+        d = (i // side ** p) % side
+        j = np.where(d < side - 1, i + side ** p, -1)
+        rows.append(j)
+    J = np.stack(rows, axis=1)
+    I = np.repeat(i, dims).reshape(n, dims)
+    keep = J >= 0
+    return n, np.stack([I[keep], J[keep]], axis=1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("side,dims,mult", [(3, 6, 7), (4, 4, 5), (5, 3, 2), (2, 9, 5), (3, 18, 1000003)])
+def test_grid_closed_form(side, dims, mult):
+    """Pins the generator of the full-size m >= 2^32 GPU test (3^18 cells,
+    4,649,045,868 edges) on small grids: the oracle's graph of the
+    thermometer-coded grid equals the grid graph in closed form (for 3^18
+    only the counts, from the formula)."""
+    if side ** dims > 10 ** 6:
+        n, m = side ** dims, dims * (side - 1) * side ** (dims - 1)
+        assert (n, m) == (387420489, 4649045868) and m >= 1 << 32
+        return
+    w, ell = synth.grid_words_np(side, dims, mult)
+    rc, c, e = oracle.build_packed(w, ell)
+    assert rc == 0
+    n, want = grid_closed_form(side, dims)
+    assert c.shape[0] == n
+    assert e.shape[0] == dims * (side - 1) * side ** (dims - 1)
+    np.testing.assert_array_equal(e, want)
+    check_invariants(c, e, ell)
