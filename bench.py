@@ -297,8 +297,8 @@ def run_ours(args):
 
 def run_dist(args):
     """N ranks under torchrun (one GPU each): CFG5 split n/N rows per rank,
-    the distributed phases of DESIGN.md section 8 (NCCL all-gather of the
-    sorted runs, contiguous canonical probe ranges, edge all-gather).  Strong
+    the distributed phases of DESIGN.md section 8 (chunked NCCL all-gather of
+    the sorted runs, popcount-layer probe shards, edge all-gather).  Strong
     scaling; device time per step = max over ranks of CUDA-event time."""
     import torch
     import torch.distributed as tdist
@@ -357,14 +357,14 @@ def run_dist(args):
     peak, peak_src = _peaks()
     roof = None
     if st.get("us_probe"):
-        nr = (nc + world - 1) // world
-        ab = alg_bytes(dict(st, n_cells=nr, dict_bytes=st.get("dict_bytes", 0) // world), n, ell)
+        nr = (nc + world - 1) // world  # the rank's probed cells (equal-weight share)
+        ab = alg_bytes(dict(st, n_cells=nr), n, ell)
         a = ab["probe"] / (st["us_probe"] * 1e-6) / 1e9
         roof = {"bound": "hbm", "kernel_stage": "probe", "kernel": "k_probe_global",
                 "achieved": round(a, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(a / peak, 4), "traffic": None,
                 "alg_bytes_per_launch": int(ab["probe"]),
-                "alg_bytes_def": "compulsory bytes of rank 0's probe range (bench.alg_bytes)"}
+                "alg_bytes_def": "compulsory bytes of rank 0's probe share (bench.alg_bytes)"}
     e2e = run_dist_e2e(torch, tdist, cgdist, x, ell, ops, stream, dev, args, rank, world, nc)
     if rank == 0:
         out = {"metric": METRIC, "value": round(nc / (ms * 1e-3), 1), "unit": "cells/s",
@@ -374,8 +374,9 @@ def run_dist(args):
                "config": {"workload": "C5" if lg == 26 else f"C5@2^{lg}", "n": n, "ell": ell,
                           "n_cells": nc, "n_edges": m,
                           "l2": "inputs larger than L2 (8.6 GB / N per rank), no flush",
-                          "parallelism": f"rows/{world} + NCCL all-gather of sorted runs + "
-                          "contiguous canonical probe ranges + NCCL edge all-gather"},
+                          "parallelism": f"rows/{world} + chunked NCCL all-gather of sorted runs "
+                          "(overlapped with the merge) + popcount-layer probe shards + NCCL "
+                          "edge all-gather + G-way merge"},
                "flip_probes_per_s": round(nc * ell / (ms * 1e-3), 1),
                "rank0_stage_us": {k[3:]: round(v, 1) for k, v in st.items()
                                   if k.startswith("us_") and not k.startswith("us_host")},

@@ -92,6 +92,7 @@ typedef struct {
   double us_host_setup;    /* host wall time before the first stage event */
   int64_t dict_bytes;      /* device bytes of the dictionary's index structures (prefix
                               index T + filter F; the cell table itself not counted) */
+  int64_t dict_cells;      /* cells the dictionary holds (n_cells, or a rank's share) */
 } cg_stats;
 
 enum {
@@ -265,25 +266,57 @@ int cg_version(void);            /* (major << 16) | minor */
  * all threads); the difference across a region counts its launches. */
 int64_t cg_kernel_launches(void);
 
-/* ---- distributed phases (one process per GPU; the caller runs the NCCL
- * collectives between them) ----------------- */
+/* ---- distributed phases (row e; one process per GPU, the caller runs the
+ * NCCL collectives between them) --------------------
+ * The paper builds on one GPU; the multi-GPU split follows from the
+ * structure of the problem: a 0->1 flip raises the popcount by one (P:93,
+ * P:103), so the cells of popcount layer p have all their i < j neighbours in
+ * layer p+1, and the flip queries are sharded by popcount layer.
+ *   1. cg_dist_local: each rank's rows -> its sorted unique run, split into
+ *      2^chunk_bits prefix chunks;
+ *   2. per chunk (in prefix order): all-gather of the ranks' pieces, then
+ *      cg_dist_merge_chunk appends their merge to the replicated table (the
+ *      all-gather of chunk c+1 overlaps the merge of chunk c);
+ *   3. cg_dist_probe: the rank probes its share of the (layer, block) order
+ *      with a dictionary over its cells and their target layer only;
+ *   4. all-gather of the edge lists, cg_dist_finalize merges them. */
 
-/* Phase 1: pack + sort + dedupe this rank's rows: a sorted unique run. */
+/* Phase 1: pack + sort + dedupe this rank's rows (vecs = uint8[n_local][ell],
+ * device, n_local >= 1): *run = its sorted unique rows (cg_cells; free with
+ * cg_cells_free).  chunk_off = host int64[2^chunk_bits + 1] receives the row
+ * offsets of the prefix chunks: chunk c = the rows whose top chunk_bits bits
+ * equal c (chunk_bits in [0, 8]).  Errors as cg_build, CG_EINVAL for a bad
+ * chunk_bits / NULL chunk_off. */
 int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_opts* o,
-                  cg_cells* run);
+                  int32_t chunk_bits, cg_cells* run, int64_t* chunk_off);
 
-/* Phase 2: merge G gathered runs (device buffer runs = u64[G][stride][W],
- * run g holding counts[g] (host array) valid rows) into the global canonical
- * table (identical on every rank), then probe this rank's share of the
- * queries: the cells of the (popcount, canonical index) order between the
- * cut points at equal issued-probe weight r/G and (r+1)/G.  Returns the
- * table and this rank's edges (canonical (i, j), ascending). */
-int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, int64_t stride,
-                        int32_t ell, int32_t rank, const cg_opts* o, cg_cells* table,
-                        cg_edges* local_edges);
+/* Phase 2: merge chunk c of every rank's run -- G sorted unique pieces in the
+ * device buffer pieces = u64[G][stride][W], piece g holding counts[g] (host)
+ * rows, all with the same top chunk_bits bits and above every row already in
+ * the table -- and append the sorted unique union at table + (*n_table)*W;
+ * *n_table (host) is advanced.  table = u64[table_cap][W], caller-allocated
+ * (device).  Called once per chunk in prefix order, the result is the
+ * canonical table (G1), identical on every rank.  Errors: CG_EINVAL (NULL,
+ * counts > stride, capacity), CG_ETOOBIG (>= 2^32 rows). */
+int cg_dist_merge_chunk(const uint64_t* pieces, const int64_t* counts, int32_t G, int64_t stride,
+                        int32_t ell, int32_t chunk_bits, const cg_opts* o, uint64_t* table,
+                        int64_t table_cap, int64_t* n_table);
 
-/* Phase 3: merge G gathered edge lists (device buffer u32[G][stride][2],
- * list g holding counts[g] (host) valid pairs) into the canonical list. */
+/* Phase 3: rank `rank` of G probes its share of the flip queries over the
+ * canonical table (device u64[n_cells][W]): the cells of a contiguous range of
+ * the (popcount layer, block of 2^16 canonical cells) order cut at equal probe
+ * weight (1 + candidate bits per cell).  Its dictionary (prefix index +
+ * filter, CG_DICT_GLOBAL) holds only those cells and the layers one above
+ * them (cg_stats.dict_cells / dict_bytes report its size).  *local_edges =
+ * this rank's edges (canonical indices, i < j, ascending; free with
+ * cg_edges_free); the ranks' lists are disjoint and cover E.  G = 1 probes
+ * everything.  Errors: CG_EINVAL (NULL, G not in [1, 64], rank), CG_ETOOBIG. */
+int cg_dist_probe(const uint64_t* table, int64_t n_cells, int32_t ell, int32_t G, int32_t rank,
+                  const cg_opts* o, cg_edges* local_edges);
+
+/* Phase 4: merge G gathered canonical, disjoint edge lists (device buffer
+ * u32[G][stride][2], list g holding counts[g] (host) pairs) into the
+ * canonical edge list (G-way merge, G <= 64). */
 int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G, int64_t stride,
                      const cg_opts* o, cg_edges* edges);
 

@@ -49,7 +49,8 @@ class cg_stats(ctypes.Structure):
                [("sort_passes", ctypes.c_int32), ("probe_reruns", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int64), ("us_host_alloc", ctypes.c_double),
                 ("n_allocs", ctypes.c_int64), ("us_host_total", ctypes.c_double),
-                ("us_host_setup", ctypes.c_double), ("dict_bytes", ctypes.c_int64)]
+                ("us_host_setup", ctypes.c_double), ("dict_bytes", ctypes.c_int64),
+                ("dict_cells", ctypes.c_int64)]
 
 
 class cg_opts(ctypes.Structure):
@@ -122,12 +123,15 @@ def lib():
     L.cg_build_points.argtypes = [P, i64, i32, P, i32, ctypes.POINTER(cg_opts),
                                   ctypes.POINTER(cg_cells), ctypes.POINTER(cg_edges)]
     L.cg_build_points.restype = ctypes.c_int
-    L.cg_dist_local.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells)]
+    L.cg_dist_local.argtypes = [P, i64, i32, ctypes.POINTER(cg_opts), i32,
+                                ctypes.POINTER(cg_cells), ctypes.POINTER(i64)]
     L.cg_dist_local.restype = ctypes.c_int
-    L.cg_dist_merge_probe.argtypes = [P, ctypes.POINTER(i64), i32, i64, i32, i32,
-                                      ctypes.POINTER(cg_opts), ctypes.POINTER(cg_cells),
-                                      ctypes.POINTER(cg_edges)]
-    L.cg_dist_merge_probe.restype = ctypes.c_int
+    L.cg_dist_merge_chunk.argtypes = [P, ctypes.POINTER(i64), i32, i64, i32, i32,
+                                      ctypes.POINTER(cg_opts), P, i64, ctypes.POINTER(i64)]
+    L.cg_dist_merge_chunk.restype = ctypes.c_int
+    L.cg_dist_probe.argtypes = [P, i64, i32, i32, i32, ctypes.POINTER(cg_opts),
+                                ctypes.POINTER(cg_edges)]
+    L.cg_dist_probe.restype = ctypes.c_int
     L.cg_dist_finalize.argtypes = [P, ctypes.POINTER(i64), i32, i64, ctypes.POINTER(cg_opts),
                                    ctypes.POINTER(cg_edges)]
     L.cg_dist_finalize.restype = ctypes.c_int
@@ -178,7 +182,7 @@ EXPORTED = ("cg_opts_init", "cg_build", "cg_build_ex", "cg_build_packed_ex", "cg
             "cg_edges_free", "cg_index_free", "cg_strerror", "cg_last_error", "cg_version",
             "cg_kernel_launches", "cg_signatures", "cg_build_points", "cg_csr", "cg_bfs",
             "cg_allpairs", "cg_insert",
-            "cg_dist_local", "cg_dist_merge_probe", "cg_dist_finalize")
+            "cg_dist_local", "cg_dist_merge_chunk", "cg_dist_probe", "cg_dist_finalize")
 
 
 def _check(rc: int):
@@ -463,60 +467,77 @@ def version() -> int:
 
 
 # ---------------------------------------------------------------- distributed phases
-def dist_local(vecs: torch.Tensor, *, stream=None) -> torch.Tensor:
-    """cg_dist_local: pack + sort + dedupe this rank's rows -> sorted unique
-    run, int64 [c, W] (device)."""
+def dist_local(vecs: torch.Tensor, *, chunk_bits: int = 0, stream=None):
+    """cg_dist_local: pack + sort + dedupe this rank's rows -> (sorted unique
+    run int64 [c, W] (device), chunk_off list of 2^chunk_bits + 1 row offsets
+    of its prefix chunks)."""
     if vecs.dtype != torch.uint8 or vecs.dim() != 2 or not vecs.is_cuda:
         raise CgError(CG_EINVAL, "vecs must be a CUDA uint8 tensor [n, ell]")
     vecs = vecs.contiguous()
     n, ell = vecs.shape
     stream = stream or torch.cuda.current_stream(vecs.device)
-    o, _, _ = _opts(stream, "sorted", True, -1, False, False)
+    o, _, _ = _opts(stream, "global", True, -1, False, False)
     c = cg_cells()
+    off = (ctypes.c_int64 * ((1 << chunk_bits) + 1))()
     with torch.cuda.device(vecs.device):
         _check(lib().cg_dist_local(ctypes.c_void_p(vecs.data_ptr()), n, ell, ctypes.byref(o),
-                                   ctypes.byref(c)))
+                                   int(chunk_bits), ctypes.byref(c), off))
     c.ell, c.words_per_cell = ell, (ell + 63) // 64
-    return _wrap_cells(c, vecs.device)
+    return _wrap_cells(c, vecs.device), [int(x) for x in off]
 
 
-def dist_merge_probe(runs: torch.Tensor, counts, rank: int, ell: int, *, stream=None,
-                     want_stats=False, dict_kind="global"):
-    """cg_dist_merge_probe: runs = int64 [G, stride, W] gathered sorted runs
-    (counts[g] valid rows each).  Returns (table int64 [n_c, W], this rank's
-    edges int32 [m_r, 2], stats).  dict_kind "global": the rank probes a
-    contiguous canonical range; "sorted": its share of the (popcount layer,
-    index) order cut at equal probe weight."""
-    if runs.dtype != torch.int64 or runs.dim() != 3 or not runs.is_cuda:
-        raise CgError(CG_EINVAL, "runs must be a CUDA int64 tensor [G, stride, W]")
-    runs = runs.contiguous()
-    G, stride, W = runs.shape
+def dist_merge_chunk(pieces: torch.Tensor, counts, ell: int, chunk_bits: int,
+                     table: torch.Tensor, n_table: int, *, stream=None) -> int:
+    """cg_dist_merge_chunk: append the sorted unique union of one prefix chunk
+    of every rank's run (pieces int64 [G, stride, W], counts[g] valid rows
+    each) to table (int64 [cap, W], device) after its n_table rows.  Returns
+    the new row count."""
+    if pieces.dtype != torch.int64 or pieces.dim() != 3 or not pieces.is_cuda:
+        raise CgError(CG_EINVAL, "pieces must be a CUDA int64 tensor [G, stride, W]")
+    if table.dtype != torch.int64 or table.dim() != 2 or not table.is_contiguous():
+        raise CgError(CG_EINVAL, "table must be a contiguous int64 tensor [cap, W]")
+    pieces = pieces.contiguous()
+    G, stride, W = pieces.shape
     cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
-    stream = stream or torch.cuda.current_stream(runs.device)
-    o, _, st = _opts(stream, dict_kind, True, -1, False, want_stats)
-    c, e = cg_cells(), cg_edges()
-    with torch.cuda.device(runs.device):
-        _check(lib().cg_dist_merge_probe(ctypes.c_void_p(runs.data_ptr()), cnt, G, stride, ell,
-                                         rank, ctypes.byref(o), ctypes.byref(c),
-                                         ctypes.byref(e)))
-    c.ell, c.words_per_cell = ell, (ell + 63) // 64
-    return (_wrap_cells(c, runs.device), _wrap_edges(e, runs.device),
-            _stats_dict(st) if want_stats else {})
+    nt = ctypes.c_int64(int(n_table))
+    stream = stream or torch.cuda.current_stream(pieces.device)
+    o, _, _ = _opts(stream, "global", True, -1, False, False)
+    with torch.cuda.device(pieces.device):
+        _check(lib().cg_dist_merge_chunk(ctypes.c_void_p(pieces.data_ptr()), cnt, G, stride, ell,
+                                         int(chunk_bits), ctypes.byref(o),
+                                         ctypes.c_void_p(table.data_ptr()), table.shape[0],
+                                         ctypes.byref(nt)))
+    return nt.value
 
 
-def dist_finalize(gathered: torch.Tensor, counts, *, stream=None,
-                  dict_kind="global") -> torch.Tensor:
-    """cg_dist_finalize: gathered = int32 [G, stride, 2] per-rank edge lists
-    (counts[g] valid pairs each) -> canonical edge list int32 [m, 2].
-    dict_kind must match the one the lists were probed with ("global": the
-    lists are canonical ranges -> concatenation; else a sort)."""
+def dist_probe(table: torch.Tensor, ell: int, G: int, rank: int, *, stream=None,
+               want_stats=False, lcp_prune=True):
+    """cg_dist_probe: this rank's share of the flip queries (popcount-layer
+    split) over the canonical table int64 [n_cells, W] (device).  Returns
+    (edges int32 [m_r, 2] canonical, stats)."""
+    if table.dtype != torch.int64 or table.dim() != 2 or not table.is_cuda:
+        raise CgError(CG_EINVAL, "table must be a CUDA int64 tensor [n_cells, W]")
+    table = table.contiguous()
+    stream = stream or torch.cuda.current_stream(table.device)
+    o, _, st = _opts(stream, "global", lcp_prune, -1, False, want_stats)
+    e = cg_edges()
+    with torch.cuda.device(table.device):
+        _check(lib().cg_dist_probe(ctypes.c_void_p(table.data_ptr()), table.shape[0], ell, G, rank,
+                                   ctypes.byref(o), ctypes.byref(e)))
+    return _wrap_edges(e, table.device), (_stats_dict(st) if want_stats else {})
+
+
+def dist_finalize(gathered: torch.Tensor, counts, *, stream=None) -> torch.Tensor:
+    """cg_dist_finalize: gathered = int32 [G, stride, 2] per-rank canonical,
+    disjoint edge lists (counts[g] valid pairs each) -> their G-way merge,
+    the canonical edge list int32 [m, 2]."""
     if gathered.dtype != torch.int32 or gathered.dim() != 3 or not gathered.is_cuda:
         raise CgError(CG_EINVAL, "gathered must be a CUDA int32 tensor [G, stride, 2]")
     gathered = gathered.contiguous()
     G, stride, _ = gathered.shape
     cnt = (ctypes.c_int64 * G)(*[int(c) for c in counts])
     stream = stream or torch.cuda.current_stream(gathered.device)
-    o, _, _ = _opts(stream, dict_kind, True, -1, False, False)
+    o, _, _ = _opts(stream, "global", True, -1, False, False)
     e = cg_edges()
     with torch.cuda.device(gathered.device):
         _check(lib().cg_dist_finalize(ctypes.c_void_p(gathered.data_ptr()), cnt, G, stride,

@@ -352,13 +352,143 @@ struct Built {
   cg_index* index = nullptr;
 };
 
-// Distributed role of a build: cells only (phase 1), or probe only the
-// rank's share of the (popcount, canonical index) order (phase 2).
+// Distributed role of a build: cells only (phase 1 and the chunk merges of
+// the distributed build return the sorted unique rows, no probe).
 struct Shard {
   bool cells_only = false;
-  int rank = 0;
-  int world = 1;
+  int pre_skip = 0;  // pre_off buckets are bits [pre_skip, pre_skip + pre_B) (a prefix chunk)
 };
+
+// a5 + a6 + a7 over one prefix-indexed dictionary: T and F over the rows
+// keys[0..nrows) (the canonical table, or a rank's subsequence U of it with
+// canonical indices idx), probes of the sources (all rows, or the rows
+// src_pos[0..n_src)), and the canonical edge list placed from the probe's
+// sorted tile blocks.  Stage marks 4 (layers: implicit), 5 (dict), 6
+// (probe), 7 (edges).  T/F are handed to *T_out/*F_out when requested.
+struct GlobalOut {
+  uint64_t* edges = nullptr;  // u32 pairs, dev_alloc'd
+  int64_t m = 0;
+  uint64_t issued = 0;
+  int reruns = 0;
+  int64_t dict_bytes = 0;
+  int b = 0, fextra = 0;
+  uint32_t* T = nullptr;  // when keep_index
+  uint32_t* F = nullptr;
+};
+
+static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* src_pos,
+                         const uint32_t* idx, int64_t n_src, int W, int ell, const cg_opts& o,
+                         bool keep_index, StageTimer& tm, GlobalOut* go) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+  const int64_t nc = nrows;
+  {
+    tm.mark();  // 4: layers (implicit in the global dictionary)
+    // ---- a5 one prefix index + filter over the canonical table
+    // defaults measured on C5 (tools/tune_probe.sh): 1-2 cells per bucket and
+    // a b+5-bit filter (probe 4.51 ms vs 5.00 ms at 4-8 cells / b+7 bits)
+    const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 0;
+    int b = 0;
+    while (b < 28 && (uint64_t(nc) >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
+    int fextra = o.filter_extra >= 0 ? o.filter_extra : 5;
+    fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
+    const Mem gix = keep_index ? Mem::Persist : Mem::Scratch;  // T/F outlive the build
+    DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
+    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
+    CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
+    const int64_t dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
+    build_global_index(keys, nc, W, b, fextra, T.p, F.p, s);
+    tm.mark();  // 5: dict
+    GlobalDict g{keys, nullptr, T.p, F.p, b, fextra, W, ell, nc};
+    g.src_pos = src_pos;
+    g.idx = idx;
+    // ---- a6 + a7: probes write the canonical edge list directly
+    const int64_t i_lo = 0, i_hi = n_src;
+    const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
+    DevBuf<uint32_t> tcnt(size_t(ntiles), s);  // hits per tile
+    DevBuf<uint64_t> tpos(size_t(ntiles), s);  // block position in the scratch list (~0: overflow)
+    DevBuf<uint32_t> ticket(2, s);
+    DevBuf<unsigned long long> ctr(4, s);
+    DevBuf<uint4> ovf(size_t(ntiles), s);
+    // scratch capacity: 4 hits per cell covers planted sets (m/n_c = 0.5) and
+    // arrangement samples (degree ~ 2d, m/n_c <= 3 in R^3) in one probe pass;
+    // a larger m (P:106 allows n_c*ell/2) costs one re-run at the exact size
+    uint64_t cap = std::max<uint64_t>(4 * uint64_t(i_hi - i_lo), 1 << 16);
+    if (o.edge_cap > 0) cap = uint64_t(o.edge_cap);
+    DevBuf<uint64_t> hits(cap, s);  // tile blocks of sorted (i << 32 | j)
+    unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
+    int reruns = 0;
+    uint64_t m = 0, issued = 0, novf = 0;
+    while (true) {
+      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
+      CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tcnt.p, tpos.p, ticket.p, ctr.p,
+                          ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
+      CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      m = hc[0];
+      issued = hc[1];
+      novf = uint32_t(hc[2] & 0xffffffffu);
+      if (m <= cap) break;
+      cap = m;
+      hits.alloc(cap, s);
+      ++reruns;
+    }
+    tm.mark();  // 6: probe
+    // ---- canonical placement of the tile blocks: 64-bit offsets = exclusive
+    // scan of the tile counts (overflow tiles included; m may exceed 2^32,
+    // P:106), then one copy
+    DevBuf<uint64_t> toff(size_t(ntiles), s);
+    launch_scan_u32_u64(tcnt.p, toff.p, ntiles, s);
+    uint64_t mt = m;  // total including overflow tiles
+    if (novf) {
+      std::vector<uint4> hv(novf);
+      CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      for (const uint4& t : hv) mt += t.z;
+    }
+    uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(mt, 1) * 8, s));
+    launch_tile_copy(hits.p, toff.p, tpos.p, tcnt.p, ntiles, eout, s);
+    if (novf) {
+      // tiles whose hits overflowed a warp buffer (dense graphs): re-run all
+      // of them at once in spill mode, sort the spilled hits (tiles cover
+      // disjoint source ranges, so the sorted list is the tiles' lists in
+      // tile order) and drop each tile's part at its canonical offset
+      const uint64_t ms = mt - m;
+      if (ms >= (uint64_t(1) << 32))
+        throw CgError{CG_ETOOBIG, ">= 2^32 edges from dense overflow tiles"};
+      hits.reset();
+      DevBuf<uint8_t> sel(size_t(ntiles), s);
+      DevBuf<uint32_t> scnt(size_t(ntiles), s);
+      DevBuf<uint64_t> sstart(size_t(ntiles), s);
+      CG_CUDA(cudaMemsetAsync(sel.p, 0, size_t(ntiles), s));
+      CG_CUDA(cudaMemsetAsync(scnt.p, 0, size_t(ntiles) * 4, s));
+      launch_spill_select(ovf.p, uint32_t(novf), sel.p, scnt.p, s);
+      launch_scan_u32_u64(scnt.p, sstart.p, ntiles, s);
+      DevBuf<uint64_t> sp1(ms, s), sp2(ms, s);
+      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
+      CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
+      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tcnt.p, tpos.p, ticket.p,
+                          ctr.p + 3, ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
+      uint64_t* so = sp1.p;
+      if (ms > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, int64_t(ms), 64, &so, nullptr, s, nullptr);
+      launch_spill_place(g, so, int64_t(ms), i_lo, toff.p, sstart.p, eout, s);
+    }
+    m = mt;
+    tm.mark();  // 7: edges (placement of the already sorted tile blocks)
+    go->edges = eout;
+    go->m = int64_t(m);
+    go->issued = issued;
+    go->reruns = reruns + int(novf);
+    go->dict_bytes = dict_bytes;
+    go->b = b;
+    go->fextra = fextra;
+    if (keep_index) {
+      go->T = T.release();
+      go->F = F.release();
+    }
+  }
+}
 
 // Runs a2..a7 given packed keys (u64[n][W], consumed as scratch).
 static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
@@ -387,7 +517,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
     done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off, pre_B,
-                                   tile_hist, d_flags, &in_err)
+                                   tile_hist, d_flags, &in_err, sh.pre_skip)
                  : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     sorted = ko;
     if (done && fused) {
@@ -462,110 +592,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     return;
   }
   if (o.dict_kind == CG_DICT_GLOBAL) {
-    tm.mark();  // 4: layers (implicit in the global dictionary)
-    // ---- a5 one prefix index + filter over the canonical table
-    // defaults measured on C5 (tools/tune_probe.sh): 1-2 cells per bucket and
-    // a b+5-bit filter (probe 4.51 ms vs 5.00 ms at 4-8 cells / b+7 bits)
-    const int target_log2 = o.bucket_log2 >= 0 ? o.bucket_log2 : 0;
-    int b = 0;
-    while (b < 28 && (uint64_t(nc) >> (b + 1)) >= (uint64_t(1) << target_log2)) ++b;
-    int fextra = o.filter_extra >= 0 ? o.filter_extra : 5;
-    fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
-    const Mem gix = o.index_out ? Mem::Persist : Mem::Scratch;  // T/F outlive the build
-    DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
-    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
-    CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
-    const int64_t dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
-    build_global_index(cellbuf.p, nc, W, b, fextra, T.p, F.p, s);
-    tm.mark();  // 5: dict
-    GlobalDict g{cellbuf.p, lcp.p, T.p, F.p, b, fextra, W, ell, nc};
-    // ---- a6 + a7: probes write the canonical edge list directly
-    int64_t i_lo = 0, i_hi = nc;
-    if (sh.world > 1) {  // distributed: contiguous canonical ranges
-      i_lo = nc * sh.rank / sh.world;
-      i_hi = nc * (sh.rank + 1) / sh.world;
-    }
-    const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
-    DevBuf<uint32_t> tcnt(size_t(ntiles), s);  // hits per tile
-    DevBuf<uint64_t> tpos(size_t(ntiles), s);  // block position in the scratch list (~0: overflow)
-    DevBuf<uint32_t> ticket(2, s);
-    DevBuf<unsigned long long> ctr(4, s);
-    DevBuf<uint4> ovf(size_t(ntiles), s);
-    // scratch capacity: 4 hits per cell covers planted sets (m/n_c = 0.5) and
-    // arrangement samples (degree ~ 2d, m/n_c <= 3 in R^3) in one probe pass;
-    // a larger m (P:106 allows n_c*ell/2) costs one re-run at the exact size
-    uint64_t cap = std::max<uint64_t>(4 * uint64_t(i_hi - i_lo), 1 << 16);
-    if (o.edge_cap > 0) cap = uint64_t(o.edge_cap);
-    DevBuf<uint64_t> hits(cap, s);  // tile blocks of sorted (i << 32 | j)
-    unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
-    int reruns = 0;
-    uint64_t m = 0, issued = 0, novf = 0;
-    while (true) {
-      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
-      CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
-      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tcnt.p, tpos.p, ticket.p, ctr.p,
-                          ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
-      CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-      CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-      CG_CUDA(cudaStreamSynchronize(s));
-      m = hc[0];
-      issued = hc[1];
-      novf = uint32_t(hc[2] & 0xffffffffu);
-      if (m <= cap) break;
-      cap = m;
-      hits.alloc(cap, s);
-      ++reruns;
-    }
-    tm.mark();  // 6: probe
-    // ---- canonical placement of the tile blocks: 64-bit offsets = exclusive
-    // scan of the tile counts (overflow tiles included; m may exceed 2^32,
-    // P:106), then one copy
-    DevBuf<uint64_t> toff(size_t(ntiles), s);
-    launch_scan_u32_u64(tcnt.p, toff.p, ntiles, s);
-    uint64_t mt = m;  // total including overflow tiles
-    if (novf) {
-      std::vector<uint4> hv(novf);
-      CG_CUDA(cudaMemcpyAsync(hv.data(), ovf.p, novf * sizeof(uint4), cudaMemcpyDeviceToHost, s));
-      CG_CUDA(cudaStreamSynchronize(s));
-      for (const uint4& t : hv) mt += t.z;
-    }
-    uint64_t* eout = static_cast<uint64_t*>(dev_alloc(std::max<uint64_t>(mt, 1) * 8, s));
-    launch_tile_copy(hits.p, toff.p, tpos.p, tcnt.p, ntiles, eout, s);
-    if (novf) {
-      // tiles whose hits overflowed a warp buffer (dense graphs): re-run all
-      // of them at once in spill mode, sort the spilled hits (tiles cover
-      // disjoint source ranges, so the sorted list is the tiles' lists in
-      // tile order) and drop each tile's part at its canonical offset
-      const uint64_t ms = mt - m;
-      if (ms >= (uint64_t(1) << 32))
-        throw CgError{CG_ETOOBIG, ">= 2^32 edges from dense overflow tiles"};
-      hits.reset();
-      DevBuf<uint8_t> sel(size_t(ntiles), s);
-      DevBuf<uint32_t> scnt(size_t(ntiles), s);
-      DevBuf<uint64_t> sstart(size_t(ntiles), s);
-      CG_CUDA(cudaMemsetAsync(sel.p, 0, size_t(ntiles), s));
-      CG_CUDA(cudaMemsetAsync(scnt.p, 0, size_t(ntiles) * 4, s));
-      launch_spill_select(ovf.p, uint32_t(novf), sel.p, scnt.p, s);
-      launch_scan_u32_u64(scnt.p, sstart.p, ntiles, s);
-      DevBuf<uint64_t> sp1(ms, s), sp2(ms, s);
-      CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
-      CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
-      launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tcnt.p, tpos.p, ticket.p,
-                          ctr.p + 3, ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
-      uint64_t* so = sp1.p;
-      if (ms > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, int64_t(ms), 64, &so, nullptr, s, nullptr);
-      launch_spill_place(so, int64_t(ms), i_lo, toff.p, sstart.p, eout, s);
-    }
-    m = mt;
-    tm.mark();  // 7: edges (placement of the already sorted tile blocks)
+    GlobalOut go;
+    global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, o, o.index_out != nullptr, tm, &go);
+    const uint64_t m = uint64_t(go.m);
+    uint64_t* eout = go.edges;
+    const int b = go.b, fextra = go.fextra;
     if (o.index_out) {
       // the index owns its own copy of the table plus T and F
       cg_index* ixp = new cg_index();
       ixp->global = true;
       ixp->keys = static_cast<uint64_t*>(dev_alloc(size_t(nc) * W * 8, s));
       CG_CUDA(cudaMemcpyAsync(ixp->keys, cellbuf.p, size_t(nc) * W * 8, cudaMemcpyDeviceToDevice, s));
-      ixp->T = T.release();
-      ixp->F = F.release();
+      ixp->T = go.T;
+      ixp->F = go.F;
       cudaGetDevice(&ixp->device);
       ixp->gview = GlobalDict{ixp->keys, nullptr, ixp->T, ixp->F, b, fextra, W, ell, nc};
       out->index = ixp;
@@ -586,10 +625,11 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       st->n_cells = nc;
       st->n_edges = int64_t(m);
       st->logical_probes = nc * int64_t(ell);
-      st->issued_probes = int64_t(issued);
+      st->issued_probes = int64_t(go.issued);
       st->sort_passes = sst.passes;
-      st->probe_reruns = reruns + int(novf);
-      st->dict_bytes = dict_bytes;
+      st->probe_reruns = go.reruns;
+      st->dict_bytes = go.dict_bytes;
+      st->dict_cells = nc;
     }
     return;
   }
@@ -640,29 +680,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   DictView dv{lkeys.p, li, loff.p, T.p, tbase.p, tbits.p, F.p, tbase.p + ell + 1, W, ell, nc, fextra};
   launch_build_prefix_index(dv, sp, T.p, F.p, s);
   tm.mark();  // 5: dict
-  // ---- which cells this build probes: all, or (distributed) the rank's
-  // share of the layer-major order cut at equal probe weight (candidate bits)
-  int64_t j_lo = 0, j_hi = nc;
-  if (sh.world > 1) {
-    const int64_t tiles = (nc + kWeightTile - 1) / kWeightTile;
-    DevBuf<uint32_t> tw(size_t(std::max<int64_t>(tiles, 1)), s);
-    launch_probe_weights(dv, llcp.p, sp, o.lcp_prune, tw.p, s);
-    uint32_t* htw = static_cast<uint32_t*>(host_stage(size_t(std::max<int64_t>(tiles, 1)) * 4));
-    CG_CUDA(cudaMemcpyAsync(htw, tw.p, size_t(tiles) * 4, cudaMemcpyDeviceToHost, s));
-    CG_CUDA(cudaStreamSynchronize(s));
-    std::vector<uint64_t> pre(tiles + 1, 0);
-    for (int64_t t = 0; t < tiles; ++t) pre[t + 1] = pre[t] + htw[t];
-    auto cut = [&](int r) -> int64_t {  // first tile whose prefix reaches r/G of the weight
-      if (r <= 0) return 0;
-      if (r >= sh.world) return tiles;
-      const uint64_t target = (pre[tiles] * uint64_t(r)) / uint64_t(sh.world);
-      return int64_t(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
-    };
-    j_lo = std::min<int64_t>(nc, cut(sh.rank) * kWeightTile);
-    j_hi = std::min<int64_t>(nc, cut(sh.rank + 1) * kWeightTile);
-    if (sh.rank + 1 >= sh.world) j_hi = nc;
-    if (j_hi < j_lo) j_hi = j_lo;
-  }
+  const int64_t j_lo = 0, j_hi = nc;
   // ---- a6 probes + a7 warp-aggregated append
   DevBuf<unsigned long long> ctr(2, s);
   uint64_t cap = std::max<uint64_t>(4 * uint64_t(j_hi - j_lo), 1 << 16);
@@ -1286,7 +1304,7 @@ int64_t cg_kernel_launches(void) { return g_launches_total.load(std::memory_orde
 int cg_version(void) { return (0 << 16) | 1; }
 
 int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_opts* o_in,
-                  cg_cells* run) {
+                  int32_t chunk_bits, cg_cells* run, int64_t* chunk_off) {
   if (run) std::memset(run, 0, sizeof(*run));
   cg_opts o;
   cg_opts_init(&o);
@@ -1295,6 +1313,9 @@ int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_op
   try {
     cg_edges dummy;
     validate_common(n_local, ell, vecs, run, &dummy);
+    validate_opts(o);
+    if (chunk_bits < 0 || chunk_bits > 8) throw CgError{CG_EINVAL, "chunk_bits must be in [0, 8]"};
+    if (!chunk_off) throw CgError{CG_EINVAL, "chunk_off is NULL"};
     check_arch();
     check_device_ptr(vecs, "vecs");
     reset_counters();
@@ -1305,12 +1326,33 @@ int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_op
     tm.start(o.stats != nullptr, s);
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-    DevBuf<uint64_t> keys(size_t(n_local) * W, s);
-    launch_pack(vecs, n_local, ell, keys.p, flags.p, s);
+    const bool msd = W <= 2 && o.sort_kind != 1;
+    DevBuf<uint64_t> keys(size_t(n_local) * W, s, msd ? Mem::Persist : Mem::Scratch);
+    const int B = msd_prefix_bits(n_local);
+    const int dlo = (64 - B) / 8;
+    DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
+    DevBuf<uint32_t> tile_hist(msd ? size_t((n_local + msd_tile_rows(W) - 1) / msd_tile_rows(W)) * 256 : 1, s);
+    if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
+    launch_pack(vecs, n_local, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo,
+                msd ? tile_hist.p : nullptr, msd_tile_rows(W));
     tm.mark();
     Shard sh;
     sh.cells_only = true;
-    build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh);
+    build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh, msd ? top_hist.p : nullptr,
+                    nullptr, B, msd ? tile_hist.p : nullptr);
+    // the run's split into 2^chunk_bits prefix chunks (the pipelined exchange)
+    const int C = 1 << chunk_bits;
+    if (chunk_bits == 0) {
+      chunk_off[0] = 0;
+      chunk_off[1] = b.n_cells;
+    } else {
+      DevBuf<uint32_t> off(size_t(C) + 1, s);
+      launch_prefix_bounds(b.cells, b.n_cells, W, chunk_bits, off.p, s);
+      uint32_t* h = static_cast<uint32_t*>(host_stage(size_t(C + 1) * 4));
+      CG_CUDA(cudaMemcpyAsync(h, off.p, size_t(C + 1) * 4, cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      for (int c = 0; c <= C; ++c) chunk_off[c] = h[c];
+    }
     store_counters(o.stats);
   } catch (...) {
     const int rc_ = current_error();
@@ -1324,76 +1366,196 @@ int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_op
   return CG_OK;
 }
 
-int cg_dist_merge_probe(const uint64_t* runs, const int64_t* counts, int32_t G, int64_t stride,
-                        int32_t ell, int32_t rank, const cg_opts* o_in, cg_cells* table,
-                        cg_edges* local_edges) {
-  if (table) std::memset(table, 0, sizeof(*table));
-  if (local_edges) std::memset(local_edges, 0, sizeof(*local_edges));
+int cg_dist_merge_chunk(const uint64_t* pieces, const int64_t* counts, int32_t G, int64_t stride,
+                        int32_t ell, int32_t chunk_bits, const cg_opts* o_in, uint64_t* table,
+                        int64_t table_cap, int64_t* n_table) {
   cg_opts o;
   cg_opts_init(&o);
   if (o_in) o = *o_in;
   o.index_out = nullptr;
   Built b;
   try {
-    if (!runs || !counts || !table || !local_edges) throw CgError{CG_EINVAL, "NULL argument"};
-    if (G < 1 || rank < 0 || rank >= G || stride < 0) throw CgError{CG_EINVAL, "bad G/rank/stride"};
+    if (!counts || !table || !n_table) throw CgError{CG_EINVAL, "NULL argument"};
+    if (G < 1 || stride < 0) throw CgError{CG_EINVAL, "bad G/stride"};
     if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    if (chunk_bits < 0 || chunk_bits > 8) throw CgError{CG_EINVAL, "chunk_bits must be in [0, 8]"};
+    validate_opts(o);
     int64_t total = 0;
     for (int g = 0; g < G; ++g) {
       if (counts[g] < 0 || counts[g] > stride) throw CgError{CG_EINVAL, "counts[g] out of range"};
       total += counts[g];
     }
-    if (total < 1) throw CgError{CG_EINVAL, "no rows in the gathered runs"};
-    if (total > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "too many rows"};
+    if (*n_table < 0 || total + *n_table > table_cap)
+      throw CgError{CG_EINVAL, "table capacity exceeded"};
+    if (total + *n_table > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "too many rows"};
+    if (total == 0) return CG_OK;
+    if (!pieces) throw CgError{CG_EINVAL, "pieces is NULL"};
     check_arch();
-    check_device_ptr(runs, "runs");
+    check_device_ptr(pieces, "pieces");
+    check_device_ptr(table, "table");
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     const int W = (ell + 63) / 64;
     WsScope ws;
     StageTimer tm;
-    tm.start(o.stats != nullptr, s);
+    tm.start(false, s);
+    uint64_t* dst = table + *n_table * W;
+    int nonempty = 0, last = 0;
+    for (int g = 0; g < G; ++g)
+      if (counts[g]) ++nonempty, last = g;
+    if (nonempty == 1) {  // one sorted unique piece: it is the merge
+      CG_CUDA(cudaMemcpyAsync(dst, pieces + int64_t(last) * stride * W, size_t(total) * W * 8,
+                              cudaMemcpyDeviceToDevice, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      *n_table += total;
+      return CG_OK;
+    }
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-    // the runs are sorted: on the MSD path they are gathered straight into
-    // the global top-B-bit buckets (no global radix passes; the bucket pass
-    // sorts each bucket's run segments and removes cross-run duplicates);
-    // otherwise concatenated and sorted in full
+    // the pieces are sorted: on the MSD path they are gathered straight into
+    // the chunk's prefix buckets (bits after the chunk's common top bits; no
+    // radix pass) and the bucket pass sorts each bucket's segments and drops
+    // cross-rank duplicates; otherwise concatenated and sorted in full
     const bool msd = W <= 2 && o.sort_kind != 1;
     DevBuf<uint64_t> keys(size_t(total) * W, s, msd ? Mem::Persist : Mem::Scratch);
-    const int B = msd_prefix_bits(total);
+    // bucket bits after the chunk's common top bits: ~1024 rows per bucket
+    // (no radix pass here, so any B works)
+    int B = 1;
+    while (B < 24 - chunk_bits && total > (int64_t(1024) << B)) ++B;
     DevBuf<uint32_t> boff(msd ? (size_t(1) << B) + 1 : 1, s);
     if (msd) {
-      gather_runs_by_prefix(runs, counts, G, stride, W, B, keys.p, boff.p, s);
+      gather_runs_by_prefix(pieces, counts, G, stride, W, B, chunk_bits, keys.p, boff.p, s);
     } else {
       int64_t at = 0;
       for (int g = 0; g < G; ++g) {
         if (counts[g])
-          CG_CUDA(cudaMemcpyAsync(keys.p + at * W, runs + int64_t(g) * stride * W,
+          CG_CUDA(cudaMemcpyAsync(keys.p + at * W, pieces + int64_t(g) * stride * W,
                                   size_t(counts[g]) * W * 8, cudaMemcpyDeviceToDevice, s));
         at += counts[g];
       }
     }
-    tm.mark();
     Shard sh;
-    sh.rank = rank;
-    sh.world = G;
-    build_from_keys(keys, total, ell, o, flags.p, tm, o.stats, &b, sh, nullptr,
+    sh.cells_only = true;
+    sh.pre_skip = chunk_bits;
+    build_from_keys(keys, total, ell, o, flags.p, tm, nullptr, &b, sh, nullptr,
                     msd ? boff.p : nullptr, B);
-    fill_stats(tm, total, o.stats);
-    store_counters(o.stats);
+    CG_CUDA(cudaMemcpyAsync(dst, b.cells, size_t(b.n_cells) * W * 8, cudaMemcpyDeviceToDevice, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    dev_free(b.cells, s);
+    b.cells = nullptr;
+    *n_table += b.n_cells;
   } catch (...) {
     const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);
-    if (b.edges) dev_free(b.edges, nullptr);
     return rc_;
   }
-  table->words = b.cells;
-  table->n_cells = b.n_cells;
-  table->ell = ell;
-  table->words_per_cell = (ell + 63) / 64;
-  local_edges->ij = b.edges;
-  local_edges->n_edges = b.n_edges;
+  return CG_OK;
+}
+
+int cg_dist_probe(const uint64_t* table, int64_t n_cells, int32_t ell, int32_t G, int32_t rank,
+                  const cg_opts* o_in, cg_edges* local_edges) {
+  if (local_edges) std::memset(local_edges, 0, sizeof(*local_edges));
+  cg_opts o;
+  cg_opts_init(&o);
+  if (o_in) o = *o_in;
+  o.index_out = nullptr;
+  GlobalOut go;
+  try {
+    if (!table || !local_edges) throw CgError{CG_EINVAL, "NULL argument"};
+    if (G < 1 || G > 64 || rank < 0 || rank >= G) throw CgError{CG_EINVAL, "bad G/rank (1 <= G <= 64)"};
+    if (n_cells < 1) throw CgError{CG_EINVAL, "n_cells must be >= 1"};
+    if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
+    if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
+    validate_opts(o);
+    if (o.dict_kind != CG_DICT_GLOBAL) throw CgError{CG_ENOTIMPL, "cg_dist_probe uses CG_DICT_GLOBAL"};
+    check_arch();
+    check_device_ptr(table, "table");
+    reset_counters();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+    const int W = (ell + 63) / 64;
+    WsScope ws;
+    StageTimer tm;
+    tm.start(o.stats != nullptr, s);  // 0
+    int64_t n_src = n_cells, n_keep = n_cells;
+    if (G == 1) {
+      tm.mark();  // 1 (layer split: none)
+      tm.mark();  // 2
+      tm.mark();  // 3
+      global_probe(table, n_cells, nullptr, nullptr, n_cells, W, ell, o, false, tm, &go);
+    } else {
+      // ---- the rank's share of the (popcount layer, canonical block) order,
+      // cut at equal probe weight; blocks of 2^16 canonical cells
+      const int blk_log2 = 16;
+      const int64_t nblk = (n_cells + (int64_t(1) << blk_log2) - 1) >> blk_log2;
+      const int64_t nflat = int64_t(ell + 1) * nblk;
+      DevBuf<uint32_t> hist(size_t(nflat), s);
+      layer_block_weights(table, n_cells, W, ell, o.lcp_prune, blk_log2, hist.p, s);
+      const uint32_t* hh = static_cast<uint32_t*>(host_stage(size_t(nflat) * 4));
+      CG_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(hh), hist.p, size_t(nflat) * 4,
+                              cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      tm.mark();  // 1: weights
+      uint64_t wtot = 0;
+      for (int64_t f = 0; f < nflat; ++f) wtot += hh[f];
+      auto cut = [&](int r) -> int64_t {  // first flat position where the prefix reaches r/G
+        if (r <= 0) return 0;
+        if (r >= G) return nflat;
+        const uint64_t target = (wtot * uint64_t(r)) / uint64_t(G);
+        uint64_t acc = 0;
+        for (int64_t f = 0; f < nflat; ++f) {
+          if (acc >= target) return f;
+          acc += hh[f];
+        }
+        return nflat;
+      };
+      const int64_t c_lo = cut(rank), c_hi = cut(rank + 1);
+      int t_lo = 1, t_hi = 0;  // target layers: one above the source layers
+      if (c_hi > c_lo) {
+        t_lo = int(c_lo / nblk) + 1;
+        t_hi = int((c_hi - 1) / nblk) + 1;
+      }
+      DevBuf<uint64_t> U(size_t(n_cells) * W, s);
+      DevBuf<uint32_t> idx(size_t(n_cells), s), src_pos(size_t(n_cells), s);
+      select_rows(table, n_cells, W, blk_log2, c_lo, c_hi, t_lo, t_hi, U.p, idx.p, src_pos.p,
+                  &n_keep, &n_src, s);
+      tm.mark();  // 2: the rank's subsequence
+      tm.mark();  // 3
+      if (n_src == 0) {
+        tm.mark();
+        tm.mark();
+        tm.mark();
+        tm.mark();
+        go.edges = static_cast<uint64_t*>(dev_alloc(8, s));
+      } else {
+        global_probe(U.p, n_keep, src_pos.p, idx.p, n_src, W, ell, o, false, tm, &go);
+      }
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (o.stats) {
+      cg_stats* st = o.stats;
+      st->n_in = n_cells;
+      st->us_sort = tm.us(0, 1);    // probe weights per (layer, block)
+      st->us_layers = tm.us(1, 2);  // the rank's dictionary subsequence
+      st->us_dict = tm.us(4, 5);
+      st->us_probe = tm.us(5, 6);
+      st->us_edges = tm.us(6, 7);
+      st->us_total = tm.us(0, 7);
+      st->n_cells = n_cells;
+      st->n_edges = go.m;
+      st->logical_probes = n_src * int64_t(ell);
+      st->issued_probes = int64_t(go.issued);
+      st->probe_reruns = go.reruns;
+      st->dict_bytes = go.dict_bytes;
+      st->dict_cells = n_keep;
+      store_counters(st);
+    }
+  } catch (...) {
+    const int rc_ = current_error();
+    if (go.edges) dev_free(go.edges, nullptr);
+    return rc_;
+  }
+  local_edges->ij = reinterpret_cast<uint32_t*>(go.edges);
+  local_edges->n_edges = go.m;
   return CG_OK;
 }
 
@@ -1407,7 +1569,7 @@ int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G,
   int64_t m = 0;
   try {
     if (!gathered || !counts || !edges) throw CgError{CG_EINVAL, "NULL argument"};
-    if (G < 1 || stride < 0) throw CgError{CG_EINVAL, "bad G/stride"};
+    if (G < 1 || G > 64 || stride < 0) throw CgError{CG_EINVAL, "bad G/stride (1 <= G <= 64)"};
     for (int g = 0; g < G; ++g) {
       if (counts[g] < 0 || counts[g] > stride) throw CgError{CG_EINVAL, "counts[g] out of range"};
       m += counts[g];
@@ -1417,34 +1579,11 @@ int cg_dist_finalize(const uint32_t* gathered, const int64_t* counts, int32_t G,
     reset_counters();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
     WsScope ws;
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(gathered);
+    // the ranks' lists are canonical and disjoint (each edge is emitted by
+    // the rank owning its source cell): a G-way merge gives the canonical list
     eout = static_cast<uint64_t*>(dev_alloc(size_t(std::max<int64_t>(m, 1)) * 8, s));
-    if (o.dict_kind == CG_DICT_GLOBAL) {
-      // global dictionary: rank g probed the g-th contiguous canonical range
-      // and its list is sorted, so the concatenation IS the canonical list:
-      // each list is copied once, straight to its offset
-      int64_t at = 0;
-      for (int g = 0; g < G; ++g) {
-        if (counts[g])
-          CG_CUDA(cudaMemcpyAsync(eout + at, src + int64_t(g) * stride, size_t(counts[g]) * 8,
-                                  cudaMemcpyDeviceToDevice, s));
-        at += counts[g];
-      }
-    } else if (m > 0) {
-      // layer-sharded lists: (i, j) pairs -> (i << 32 | j) keys, canonical
-      // sort, back to pairs.  The lists are disjoint (each edge is emitted by
-      // the rank that owns its smaller endpoint), so no dedupe is needed.
-      if (m >= (int64_t(1) << 32)) throw CgError{CG_ETOOBIG, ">= 2^32 edges (layered finalize)"};
-      DevBuf<uint64_t> k1(size_t(m), s), k2(size_t(m), s);
-      int64_t at = 0;
-      for (int g = 0; g < G; ++g) {
-        if (counts[g]) launch_rotate_edges(src + int64_t(g) * stride, counts[g], k1.p + at, s);
-        at += counts[g];
-      }
-      uint64_t* ko = k1.p;
-      if (m > 1) radix_sort<uint64_t>(k1.p, k2.p, nullptr, nullptr, nullptr, false, m, 64, &ko, nullptr, s, nullptr);
-      launch_rotate_edges(ko, m, eout, s);
-    }
+    if (m > 0)
+      merge_edge_lists(reinterpret_cast<const uint64_t*>(gathered), counts, G, stride, eout, s);
     CG_CUDA(cudaStreamSynchronize(s));
   } catch (...) {
     const int rc_ = current_error();

@@ -85,8 +85,13 @@ bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** s
 // their rows grouped by the top B bits into out (u64[total][W]; each bucket
 // holds its runs' segments one after the other) and off[2^B + 1] = bucket
 // starts -- the input of sort_unique_msd(..., pre_off = off, pre_B = B).
+// skip: the top `skip` bits are common to every row (a prefix chunk); the
+// buckets are then bits [skip, skip + B).
 void gather_runs_by_prefix(const uint64_t* runs, const int64_t* counts, int G, int64_t stride,
-                           int W, int B, uint64_t* out, uint32_t* off, cudaStream_t s);
+                           int W, int B, int skip, uint64_t* out, uint32_t* off, cudaStream_t s);
+// off[q] = first row of sorted rows u64[n][W] whose top B bits are >= q, q in [0, 2^B]
+void launch_prefix_bounds(const uint64_t* rows, int64_t n, int W, int B, uint32_t* off,
+                          cudaStream_t s);
 // prefix bits B (8, 16 or 24) the MSD path uses for n keys; digit dlo = (64-B)/8
 int msd_prefix_bits(int64_t n);
 // MSD sort with dedupe fused into the bucket pass: the sorted unique cells
@@ -102,7 +107,7 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
                      const uint32_t* pre_off = nullptr, int pre_B = 0,
                      const uint32_t* tile_hist = nullptr, const uint32_t* side_dev = nullptr,
-                     uint32_t* side_host = nullptr);
+                     uint32_t* side_host = nullptr, int pre_skip = 0);
 int msd_tile_rows(int W);
 // popcount (optional) and lcp with the next cell, for a canonical table
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,
@@ -163,11 +168,6 @@ void launch_build_prefix_index(const DictView& d, const uint32_t* sorted_popc, u
 void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
                   int lcp_prune, int64_t j_lo, int64_t j_hi, uint64_t* edges, uint64_t cap,
                   unsigned long long* count, unsigned long long* issued, cudaStream_t s);
-// Probe weight (candidate bits + 1) summed per tile of kWeightTile
-// layer-major cells: the distributed query split cuts at equal weight.
-constexpr int kWeightTile = 4096;
-void launch_probe_weights(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
-                          int lcp_prune, uint32_t* tile_w, cudaStream_t s);
 // (i << 32 | j) -> u32 pair (i, j) little-endian.
 void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStream_t s);
 
@@ -175,15 +175,17 @@ void launch_rotate_edges(const uint64_t* in, int64_t m, uint64_t* out, cudaStrea
 // (probe_global.cu): one prefix index + filter over the canonical table; the
 // probe writes the canonical edge list directly (tile order + look-back).
 struct GlobalDict {
-  const uint64_t* keys;  // canonical cells u64[n_c][W]
-  const uint16_t* lcp;   // [n_c] lcp with the next cell (0xffff: last)
+  const uint64_t* keys;  // canonical cells u64[n_c][W] (or a subsequence U of them)
+  const uint16_t* lcp;   // unused (the probe derives lcp from the next row)
   const uint32_t* T;     // [2^b + 1]
   const uint32_t* F;     // 2^(b + fextra) bits
   int b;
   int fextra;
   int W;
   int ell;
-  int64_t n_cells;
+  int64_t n_cells;             // rows of keys
+  const uint32_t* src_pos = nullptr;  // subsequence mode: dictionary row of source q
+  const uint32_t* idx = nullptr;      // subsequence mode: canonical index of each row
 };
 void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
                         uint32_t* F, cudaStream_t s);
@@ -203,8 +205,8 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
 void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t* scnt,
                          cudaStream_t s);
 // sorted spilled hits -> out[toff[t] + q - sstart[t]] as (i, j) pairs
-void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint64_t* toff,
-                        const uint64_t* sstart, uint64_t* out, cudaStream_t s);
+void launch_spill_place(const GlobalDict& g, const uint64_t* sorted, int64_t m, int64_t i_lo,
+                        const uint64_t* toff, const uint64_t* sstart, uint64_t* out, cudaStream_t s);
 // place every tile block at its canonical offset off[t] as (i, j) pairs
 void launch_tile_copy(const uint64_t* scratch, const uint64_t* off, const uint64_t* pos,
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s);
@@ -215,6 +217,22 @@ int probe_global_tile_edge_cap();
 void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s);
 // out[i] = sum of in[0..i) in 64 bits (edge offsets: m may exceed 2^32)
 void launch_scan_u32_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- multi-GPU (dist.cu)
+// hist[p * nblk + blk] = probe weight (1 + candidate bits) of the cells of
+// popcount layer p in canonical block blk (2^blk_log2 cells); u32[(ell+1) * nblk]
+void layer_block_weights(const uint64_t* cells, int64_t nc, int W, int ell, int lcp_prune,
+                         int blk_log2, uint32_t* hist, cudaStream_t s);
+// a rank's dictionary subsequence: sources = cells with p * nblk + blk in
+// [c_lo, c_hi), kept = sources + layers [t_lo, t_hi]; U/idx (kept rows and
+// their canonical indices), src_pos (row in U of each source).  Host-synchronising.
+void select_rows(const uint64_t* cells, int64_t nc, int W, int blk_log2, int64_t c_lo, int64_t c_hi,
+                 int t_lo, int t_hi, uint64_t* U, uint32_t* idx, uint32_t* src_pos,
+                 int64_t* n_keep, int64_t* n_src, cudaStream_t s);
+// G sorted, disjoint canonical edge lists (u32 pairs, list g at lists + g *
+// stride, counts on the host) -> their merge into out
+void merge_edge_lists(const uint64_t* lists, const int64_t* counts, int G, int64_t stride,
+                      uint64_t* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- cg_query
 void launch_query(const DictView& d, const uint64_t* q, int64_t nq, int32_t* self_idx,

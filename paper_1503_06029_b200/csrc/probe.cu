@@ -415,35 +415,6 @@ __global__ void __launch_bounds__(256)
   if (lane == 0 && my_issued) atomicAdd(issued, my_issued);
 }
 
-// weight of a cell = its candidate bits (zero bits k <= kmax) + 1; one
-// block sums one tile of kWeightTile layer-major cells
-__global__ void __launch_bounds__(256)
-    k_probe_weights(DictView d, const uint16_t* __restrict__ llcp, const uint32_t* __restrict__ sp,
-                    int lcp_prune, uint32_t* __restrict__ tile_w) {
-  __shared__ uint32_t s_scan[33];
-  const int64_t t = blockIdx.x;
-  uint32_t acc = 0;
-  for (int i = threadIdx.x; i < kWeightTile; i += blockDim.x) {
-    const int64_t j = t * kWeightTile + i;
-    if (j >= d.n_cells) break;
-    const int p = int(sp[j]);
-    int kmax = -1;
-    if (p < d.ell && d.layer_off[p + 1] != d.layer_off[p + 2]) {
-      const int l = llcp[j];
-      kmax = lcp_prune ? ((l == 0xffff) ? -1 : min(l, d.ell - 1)) : d.ell - 1;
-    }
-    uint32_t w = 1;
-    for (int wd = 0; wd <= (kmax >> 6) && kmax >= 0; ++wd) {
-      uint64_t z = ~d.keys[j * d.W + wd];
-      if (wd == (kmax >> 6)) z &= ~0ull << (63 - (kmax & 63));
-      w += __popcll(z);
-    }
-    acc += w;
-  }
-  uint32_t total;
-  block_excl_scan(acc, s_scan, &total);
-  if (threadIdx.x == 0) tile_w[t] = total;
-}
 
 __global__ void k_rotate(const uint64_t* __restrict__ in, int64_t m, uint64_t* __restrict__ out) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
@@ -504,14 +475,6 @@ void launch_probe(const DictView& d, const uint16_t* layer_lcp, const uint32_t* 
     case 2: k_probe<2><<<g, 256, 0, s>>>(d, layer_lcp, sorted_popc, lcp_prune, j_lo, j_hi, edges, cap, count, issued); break;
     default: k_probe<0><<<g, 256, 0, s>>>(d, layer_lcp, sorted_popc, lcp_prune, j_lo, j_hi, edges, cap, count, issued); break;
   }
-  CG_LAUNCH_CHECK();
-}
-
-void launch_probe_weights(const DictView& d, const uint16_t* layer_lcp, const uint32_t* sorted_popc,
-                          int lcp_prune, uint32_t* tile_w, cudaStream_t s) {
-  const int64_t tiles = (d.n_cells + kWeightTile - 1) / kWeightTile;
-  if (tiles <= 0) return;
-  k_probe_weights<<<unsigned(tiles), 256, 0, s>>>(d, layer_lcp, sorted_popc, lcp_prune, tile_w);
   CG_LAUNCH_CHECK();
 }
 

@@ -68,7 +68,13 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 
 // FR: filter loads in flight per lane and round; NR / SR: near rows and
 // survivor-bucket rows compared per round (A/B at C5: FR 3-6, NR/SR 1, 2, 4)
-template <int WC, int FR = PROBE_FR, int NR = 2, int SR = 2>
+// SUB: the dictionary is a subsequence U of the canonical table (a rank's
+// popcount layers): source q is dictionary row
+// g.src_pos[q], and rows map to canonical indices through g.idx.  Hits are
+// keyed (q << 32 | dictionary row) inside the kernel and converted to
+// canonical (i << 32 | j) when written (idx is increasing, so the order is
+// the same).  Without SUB, q = row = canonical index.
+template <int WC, bool SUB = false, int FR = PROBE_FR, int NR = 2, int SR = 2>
 __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ tcnt,
@@ -93,11 +99,13 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     if (tile >= ntiles) break;
     if (tile_sel && !tile_sel[tile]) continue;  // spill re-run: only the overflow tiles
     uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
-    const int64_t i = i_lo + tile * kTileCells + lane;
-    const bool valid = i < i_hi;           // this lane probes cell i
-    const bool row_ok = i < g.n_cells;     // row i exists (a shuffle source past i_hi)
+    const int64_t i = i_lo + tile * kTileCells + lane;  // source sequence number q
+    const bool valid = i < i_hi;           // this lane probes
+    int64_t row = i;                       // its dictionary row
+    if (SUB) row = valid ? int64_t(g.src_pos[i]) : -1;
+    const bool row_ok = SUB ? valid : (i < g.n_cells);  // row exists (a shuffle source past i_hi)
     // ---- the cell
-    const uint64_t* Vp = g.keys + (row_ok ? i : 0) * W;
+    const uint64_t* Vp = g.keys + (row_ok ? row : 0) * W;
     uint64_t v[WC > 0 ? WC : 1];
     if (WC > 0) {
 #pragma unroll
@@ -116,12 +124,17 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     int kmax = -1;
     // the next row is the neighbouring lane's cell: take it by shuffle
     // (lane 31 and the end of the range load it)
-    const bool nx_ok = i + 1 < g.n_cells;  // row i has a successor row
+    const bool nx_ok = row_ok && row + 1 < g.n_cells;  // the row has a successor row
     uint64_t nxt[WC > 0 ? WC : 1];
     if (WC > 0) {
 #pragma unroll
       for (int w = 0; w < (WC > 0 ? WC : 1); ++w) nxt[w] = __shfl_down_sync(kFull, v[w], 1);
-      if (lane == 31 && nx_ok) {
+      bool nx_shfl = lane < 31;
+      if (SUB) {
+        const int64_t rn = __shfl_down_sync(kFull, row, 1);  // every lane shuffles
+        nx_shfl = nx_shfl && rn == row + 1;
+      }
+      if (!nx_shfl && nx_ok) {
 #pragma unroll
         for (int w = 0; w < (WC > 0 ? WC : 1); ++w) nxt[w] = Vp[W + w];
       }
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       if (lcp_prune) {
         // lcp(V_i, V_{i+1}); the last cell has no successor and probes nothing
         if (nx_ok) {
-          const uint64_t* Np = g.keys + (i + 1) * W;
+          const uint64_t* Np = g.keys + (row + 1) * W;
           const bool shfl = WC > 0;
           int l = -1;
           const int n = WC > 0 ? WC : W;
@@ -152,6 +165,11 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     }
     const uint64_t v0 = V(0);
     const uint64_t ci = uint64_t(i) << 32;
+    // in-kernel hit key (q << 32 | row) -> canonical (i << 32 | j)
+    auto canon = [&](uint64_t e) -> uint64_t {
+      if (!SUB) return e;
+      return (uint64_t(g.idx[g.src_pos[uint32_t(e >> 32)]]) << 32) | g.idx[uint32_t(e)];
+    };
 
     // append a round's hits to the tile buffer (one shared atomic per warp);
     // spill mode (overflow re-run): append unordered to the global spill list
@@ -183,7 +201,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     const bool near_on = kmax >= b;
     const uint64_t pv = b ? (v0 >> (64 - b)) : 0ull;
     // row indices fit in 32 bits (T is u32): 32-bit index arithmetic
-    const uint32_t i32 = uint32_t(i);
+    const uint32_t i32 = uint32_t(row);
     uint32_t bucket_end = i32 + 1;
     if (near_on) bucket_end = g.T[pv + 1];
     const bool near_scan = near_on && (bucket_end - (i32 + 1) <= 16u);
@@ -247,7 +265,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
           z ^= bm;
           const int fw = cw;
           ++my_issued;
-          int64_t lo = i + 1, len = bucket_end - (i + 1);
+          int64_t lo = row + 1, len = bucket_end - (row + 1);
           while (len > 0) {
             const int64_t half = len >> 1;
             const uint64_t* R = g.keys + (lo + half) * W;
@@ -383,7 +401,8 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       }
       const uint64_t o_v0 = __shfl_sync(kFull, v0, owner);
       const uint64_t o_v1 = __shfl_sync(kFull, my_v1, owner);
-      const uint32_t o_i = __shfl_sync(kFull, i32, owner);
+      const uint32_t o_i = __shfl_sync(kFull, i32, owner);  // owner's row
+      const uint32_t o_q = SUB ? __shfl_sync(kFull, uint32_t(i), owner) : o_i;
       bool hit = false;
       uint64_t e = 0;
       if (gg < total_sv) {
@@ -441,7 +460,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         }
         if (found >= 0) {
           hit = true;
-          e = (uint64_t(o_i) << 32) | uint64_t(found);
+          e = (uint64_t(o_q) << 32) | uint64_t(found);
         }
       }
       emit(hit, e);
@@ -512,7 +531,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
           same &= bk ^ ~sb;
         }
         const uint32_t r0 = __popc(less) + __popc(same & lt);
-        if (h0 && wpos + r0 < cap) out[wpos + r0] = e0;
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
       } else if (wn <= 64) {
         // rank = number of smaller keys (the (i, j) keys are distinct);
         // every lane reads the same word per step (broadcast)
@@ -524,11 +543,11 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
           r0 += x < e0;
           r1 += x < e1;
         }
-        if (h0 && wpos + r0 < cap) out[wpos + r0] = e0;
-        if (h1 && wpos + r1 < cap) out[wpos + r1] = e1;
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
+        if (h1 && wpos + r1 < cap) out[wpos + r1] = canon(e1);
       } else {
         for (uint32_t q = lane; q < wn; q += 32)
-          if (wpos + q < cap) out[wpos + q] = wbuf[q];  // sorted (i << 32 | j) keys
+          if (wpos + q < cap) out[wpos + q] = canon(wbuf[q]);  // sorted (i << 32 | j) keys
       }
     }
     __syncwarp();
@@ -556,11 +575,25 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
   const int64_t ntiles = (i_hi - i_lo + kTileCells - 1) / kTileCells;
   if (ntiles <= 0) return;
   const int grid = int(std::min<int64_t>((ntiles + kProbeWarps - 1) / kProbeWarps, int64_t(num_sms()) * 8));
+#define CG_PROBE_ARGS                                                                         \
+  g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, \
+      spill_n, ovf, ovf_n, tile_sel
+  const bool sub = g.src_pos != nullptr;
   switch (g.W) {
-    case 1: k_probe_global<1><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    case 2: k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
-    default: k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, spill_n, ovf, ovf_n, tile_sel); break;
+    case 1:
+      if (sub) k_probe_global<1, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      else k_probe_global<1><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      break;
+    case 2:
+      if (sub) k_probe_global<2, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      else k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      break;
+    default:
+      if (sub) k_probe_global<0, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      else k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      break;
   }
+#undef CG_PROBE_ARGS
   CG_LAUNCH_CHECK();
 }
 
@@ -577,12 +610,18 @@ __global__ void k_spill_select(const uint4* __restrict__ ovf, uint32_t novf, uin
 // dst = toff[t] + (q - sstart[t]) with t the tile of the hit's source cell
 __global__ void k_spill_place(const uint64_t* __restrict__ sorted, int64_t m, int64_t i_lo,
                               const uint64_t* __restrict__ toff, const uint64_t* __restrict__ sstart,
+                              const uint32_t* __restrict__ src_pos, const uint32_t* __restrict__ idx,
                               uint64_t* __restrict__ out) {
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < m;
        q += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = sorted[q];
     const int64_t t = (int64_t(k >> 32) - i_lo) / kTileCells;
-    out[toff[t] + (q - sstart[t])] = (k >> 32) | (k << 32);
+    uint32_t ci = uint32_t(k >> 32), cj = uint32_t(k);
+    if (src_pos) {  // subsequence dictionary: (source seq, row) -> canonical
+      ci = idx[src_pos[ci]];
+      cj = idx[cj];
+    }
+    out[toff[t] + (q - sstart[t])] = uint64_t(ci) | (uint64_t(cj) << 32);
   }
 }
 
@@ -592,11 +631,11 @@ void launch_spill_select(const uint4* ovf, uint32_t novf, uint8_t* sel, uint32_t
   CG_LAUNCH_CHECK();
 }
 
-void launch_spill_place(const uint64_t* sorted, int64_t m, int64_t i_lo, const uint64_t* toff,
-                        const uint64_t* sstart, uint64_t* out, cudaStream_t s) {
+void launch_spill_place(const GlobalDict& g, const uint64_t* sorted, int64_t m, int64_t i_lo,
+                        const uint64_t* toff, const uint64_t* sstart, uint64_t* out, cudaStream_t s) {
   if (m <= 0) return;
   const int64_t blocks = std::min<int64_t>((m + 255) / 256, int64_t(num_sms()) * 16);
-  k_spill_place<<<unsigned(blocks), 256, 0, s>>>(sorted, m, i_lo, toff, sstart, out);
+  k_spill_place<<<unsigned(blocks), 256, 0, s>>>(sorted, m, i_lo, toff, sstart, g.src_pos, g.idx, out);
   CG_LAUNCH_CHECK();
 }
 

@@ -230,7 +230,9 @@ __global__ void k_gather_word(const uint64_t* __restrict__ keys, int W, int w,
 // key through the SMs to find the run heads
 template <class K>
 __global__ void k_bucket_bounds_search(const K* __restrict__ keys, int64_t n, int B,
-                                       uint32_t* __restrict__ off) {
+                                       uint32_t* __restrict__ off, int skip = 0) {
+  // buckets = bits [skip, skip + B) of the top word (the top `skip` bits are
+  // common to all keys: a prefix chunk of the distributed merge)
   const int sh = 64 - B;
   const int64_t nb = int64_t(1) << B;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q <= nb;
@@ -238,7 +240,29 @@ __global__ void k_bucket_bounds_search(const K* __restrict__ keys, int64_t n, in
     int64_t lo = 0, len = n;
     while (len > 0) {
       const int64_t half = len >> 1;
-      const uint64_t p = KT<K>::top(__ldg(keys + lo + half)) >> sh;
+      const uint64_t p = (KT<K>::top(__ldg(keys + lo + half)) << skip) >> sh;
+      if (p < uint64_t(q)) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    off[q] = uint32_t(lo);
+  }
+}
+
+// the same for rows of W words (word 0 carries the prefix)
+__global__ void k_row_bounds_search(const uint64_t* __restrict__ rows, int64_t n, int W, int B,
+                                    uint32_t* __restrict__ off) {
+  const int sh = 64 - B;
+  const int64_t nb = int64_t(1) << B;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q <= nb;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, len = n;
+    while (len > 0) {
+      const int64_t half = len >> 1;
+      const uint64_t p = __ldg(rows + (lo + half) * W) >> sh;
       if (p < uint64_t(q)) {
         lo += half + 1;
         len -= half + 1;
@@ -1377,7 +1401,8 @@ template <class K>
 bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaStream_t s,
                       SortStats* st, const uint32_t* top_hist, const uint32_t* pre_off = nullptr,
                       int pre_B = 0, const uint32_t* tile_hist = nullptr,
-                      const uint32_t* side_dev = nullptr, uint32_t* side_host = nullptr) {
+                      const uint32_t* side_dev = nullptr, uint32_t* side_host = nullptr,
+                      int pre_skip = 0) {
   // pre_off: keys are already grouped by their top pre_B bits (scatter pack),
   // pre_off[b] = first row of bucket b -- no global pass needed
   const int B = pre_off ? pre_B : msd_prefix_bits(n);
@@ -1395,7 +1420,9 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
     k_bucket_bounds_search<K><<<unsigned((nb + 256) / 256), 256, 0, s>>>(ko, n, B, offb.p);
     CG_LAUNCH_CHECK();
   }
-  launch_bucket_sort<K>(ko, offp, n, nb, B, flag.p, ucnt.p, s);
+  // the bucket kernels skip the key bytes every key of a bucket shares: the
+  // top pre_skip + B bits
+  launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
   uint32_t* h = static_cast<uint32_t*>(host_stage(4 * sizeof(uint32_t)));
@@ -1429,11 +1456,11 @@ int msd_tile_rows(int W) {
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
                      const uint32_t* pre_off, int pre_B, const uint32_t* tile_hist,
-                     const uint32_t* side_dev, uint32_t* side_host) {
+                     const uint32_t* side_dev, uint32_t* side_host, int pre_skip) {
   if (W == 1) {
     uint64_t* o = nullptr;
     const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist, pre_off,
-                                               pre_B, tile_hist, side_dev, side_host);
+                                               pre_B, tile_hist, side_dev, side_host, pre_skip);
     *cells = o;
     return ok;
   }
@@ -1442,7 +1469,7 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
     const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
                                                  reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
                                                  st, top_hist, pre_off, pre_B, tile_hist, side_dev,
-                                                 side_host);
+                                                 side_host, pre_skip);
     *cells = reinterpret_cast<uint64_t*>(o);
     return ok;
   }
@@ -1481,55 +1508,102 @@ __global__ void k_run_segment_base(const uint32_t* __restrict__ offs, const uint
   }
 }
 
+constexpr int kMaxRuns = 64;
+struct RunCounts {
+  int64_t c[kMaxRuns];
+};
+
+// bucket bounds of every run in one launch: thread (g, q) -> offs[g][q]
 template <class K>
-__global__ void k_run_gather(const K* __restrict__ run, int64_t n, int B,
-                             const uint32_t* __restrict__ roff, const uint32_t* __restrict__ base,
-                             K* __restrict__ out) {
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const K k = run[e];
-    const int64_t bk = int64_t(KT<K>::top(k) >> (64 - B));
-    out[base[bk] + (e - roff[bk])] = k;
+__global__ void k_runs_bounds(const K* __restrict__ runs, int64_t stride, RunCounts rc, int G,
+                              int B, int skip, uint32_t* __restrict__ offs) {
+  const int sh = 64 - B;
+  const int64_t nq = (int64_t(1) << B) + 1;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nq * G;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(t / nq);
+    const int64_t q = t - int64_t(g) * nq;
+    const K* keys = runs + int64_t(g) * stride;
+    int64_t lo = 0, len = rc.c[g];
+    while (len > 0) {
+      const int64_t half = len >> 1;
+      const uint64_t p = (KT<K>::top(__ldg(keys + lo + half)) << skip) >> sh;
+      if (p < uint64_t(q)) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    offs[t] = uint32_t(lo);
+  }
+}
+
+// every run's rows to their bucket segments, one launch over [G][stride]
+template <class K>
+__global__ void k_runs_gather(const K* __restrict__ runs, int64_t stride, RunCounts rc, int G,
+                              int B, int skip, const uint32_t* __restrict__ offs,
+                              const uint32_t* __restrict__ base, K* __restrict__ out) {
+  const int64_t nbk = int64_t(1) << B;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < int64_t(G) * stride;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(t / stride);
+    const int64_t e = t - int64_t(g) * stride;
+    if (e >= rc.c[g]) continue;
+    const K k = runs[t];
+    const int64_t bk = int64_t((KT<K>::top(k) << skip) >> (64 - B));
+    out[base[int64_t(g) * nbk + bk] + (e - offs[int64_t(g) * (nbk + 1) + bk])] = k;
   }
 }
 
 template <class K>
-void gather_runs_impl(const K* runs, const int64_t* counts, int G, int64_t stride, int B, K* out,
-                      uint32_t* off, cudaStream_t s) {
+void gather_runs_impl(const K* runs, const int64_t* counts, int G, int64_t stride, int B, int skip,
+                      K* out, uint32_t* off, cudaStream_t s) {
+  if (G > kMaxRuns) throw CgError{CG_EINVAL, "more than 64 runs"};
   const int64_t nbk = int64_t(1) << B;
   DevBuf<uint32_t> offs(size_t(G) * (nbk + 1), s), base(size_t(G) * nbk, s);
-  CG_CUDA(cudaMemsetAsync(offs.p, 0, offs.n * 4, s));
+  RunCounts rc{};
+  int64_t total = 0;
   for (int g = 0; g < G; ++g) {
-    if (counts[g] <= 0) continue;
-    k_bucket_bounds_search<K><<<unsigned((nbk + 256) / 256), 256, 0, s>>>(runs + g * stride, counts[g],
-                                                                        B, offs.p + g * (nbk + 1));
-    CG_LAUNCH_CHECK();
+    rc.c[g] = counts[g];
+    total += counts[g];
   }
+  k_runs_bounds<K><<<grid_for((nbk + 1) * G, 256, 16), 256, 0, s>>>(runs, stride, rc, G, B, skip,
+                                                                    offs.p);
+  CG_LAUNCH_CHECK();
   k_run_bucket_base<<<grid_for(nbk, 256, 16), 256, 0, s>>>(offs.p, G, nbk, off);
   CG_LAUNCH_CHECK();
   launch_scan_u32(off, nbk, s);  // exclusive: bucket starts
-  int64_t total = 0;
-  for (int g = 0; g < G; ++g) total += counts[g];
   k_set_u32<<<1, 1, 0, s>>>(off + nbk, uint32_t(total));
   CG_LAUNCH_CHECK();
   k_run_segment_base<<<grid_for(nbk, 256, 16), 256, 0, s>>>(offs.p, off, G, nbk, base.p);
   CG_LAUNCH_CHECK();
-  for (int g = 0; g < G; ++g) {
-    if (counts[g] <= 0) continue;
-    k_run_gather<K><<<grid_for(counts[g], 256, 16), 256, 0, s>>>(
-        runs + g * stride, counts[g], B, offs.p + g * (nbk + 1), base.p + g * nbk, out);
-    CG_LAUNCH_CHECK();
-  }
+  k_runs_gather<K><<<grid_for(int64_t(G) * stride, 256, 16), 256, 0, s>>>(runs, stride, rc, G, B,
+                                                                          skip, offs.p, base.p, out);
+  CG_LAUNCH_CHECK();
 }
 }  // namespace
 
 void gather_runs_by_prefix(const uint64_t* runs, const int64_t* counts, int G, int64_t stride,
-                           int W, int B, uint64_t* out, uint32_t* off, cudaStream_t s) {
+                           int W, int B, int skip, uint64_t* out, uint32_t* off, cudaStream_t s) {
   if (W == 1)
-    gather_runs_impl<uint64_t>(runs, counts, G, stride, B, out, off, s);
+    gather_runs_impl<uint64_t>(runs, counts, G, stride, B, skip, out, off, s);
   else
     gather_runs_impl<ulonglong2>(reinterpret_cast<const ulonglong2*>(runs), counts, G, stride, B,
-                                 reinterpret_cast<ulonglong2*>(out), off, s);
+                                 skip, reinterpret_cast<ulonglong2*>(out), off, s);
+}
+
+void launch_prefix_bounds(const uint64_t* rows, int64_t n, int W, int B, uint32_t* off,
+                          cudaStream_t s) {
+  const int64_t nb = int64_t(1) << B;
+  if (W == 1)
+    k_bucket_bounds_search<uint64_t><<<unsigned((nb + 256) / 256), 256, 0, s>>>(rows, n, B, off);
+  else if (W == 2)
+    k_bucket_bounds_search<ulonglong2><<<unsigned((nb + 256) / 256), 256, 0, s>>>(
+        reinterpret_cast<const ulonglong2*>(rows), n, B, off);
+  else
+    k_row_bounds_search<<<unsigned((nb + 256) / 256), 256, 0, s>>>(rows, n, W, B, off);
+  CG_LAUNCH_CHECK();
 }
 
 bool sort_rows_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** sorted,
