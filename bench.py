@@ -137,46 +137,70 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
     # reads and writes every key; W > 2: word-0 gather, 8 passes over
     # (u64 word 0, u32 index) pairs, one row gather (tie fixes not counted)
     sort_key_bytes = 6 * K if W <= 2 else 8 + 8 * 2 * 12 + (K + 4) + K
-    tiles = (nc + 255) // 256
+    # the probe kernel's work unit is a tile of 32 cells (probe_global.cu
+    # kTileCells); per tile it writes a u32 count and a u64 block position
+    tiles = (nc + 31) // 32
     return {
         "pack": n * (ell + K),
         "sort": n * sort_key_bytes,
         "dedupe": 0,
         "layers": 0,
         "dict": nc * K + dict_b,
-        "probe": nc * K + dict_b + m * 8 + tiles * 8,
+        "probe": nc * K + dict_b + m * 8 + tiles * 12,
         "edges": m * 16,
     }
 
 
-STAGE_KERNEL = {"pack": "k_pack", "sort": "k_bucket_rank", "dedupe": "k_dedupe",
-                "dict": "k_global_index", "probe": "k_probe_global", "edges": "k_tile_copy",
-                "layers": "k_gather_rows"}
+def survey_bytes(st: dict, n: int, ell: int) -> dict:
+    """SURVEY.md section 8.d.3's per-unit byte model (a hash dictionary read
+    once per issued probe): 32 B per issued probe + K per cell (own key) +
+    (K + 8) B per edge for the probe; 8 passes x 2 x (8 + 4) B per key plus a
+    gather of 32 + K B for the W >= 2 sort (8 x 16 B for W = 1).  The builder
+    does not run that design (DESIGN.md section 6 says why), so a fraction
+    above 1 under this model means the kernel answers probes without a
+    dictionary sector each (prefix filter, near-bucket scan), not that it
+    beats the HBM peak."""
+    W = (ell + 63) // 64
+    K = 8 * W
+    nc, m = st["n_cells"], st["n_edges"]
+    sort_b = (192 + 32 + K) if W >= 2 else 128
+    return {"probe": 32 * st["issued_probes"] + nc * K + m * (K + 8),
+            "sort": n * sort_b}
 
 
-def _ncu_traffic(stage: str):
-    """DRAM bytes (read + write) per launch of the stage's main kernel from the
-    committed ncu --set full summary (profiles/*_kernels.json), or None."""
+def _ncu_kernel(stage: str):
+    """(DRAM bytes per launch, ncu duration in s, profile file) of the
+    stage's main kernel from the newest committed ncu --set full summary
+    (profiles/*_kernels.json), or (None, None, None)."""
     import glob
 
     name = STAGE_KERNEL.get(stage)
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
     if not name or not files:
-        return None, None
-    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        return None, None, None
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+            "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
+    def val(v):
+        parts = v.split()
+        return float(parts[0]) * unit.get(parts[1] if len(parts) > 1 else "byte", 1)
+
     with open(files[-1]) as f:
         ks = json.load(f)
     for k in ks:
         if name in k["kernel"]:
-            tot = 0.0
-            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                v = k["metrics"].get(m)
-                if v is None:
-                    return None, None
-                num, u = v.split()[0], v.split()[1] if len(v.split()) > 1 else "byte"
-                tot += float(num) * unit.get(u, 1)
-            return int(tot), os.path.basename(files[-1])
-    return None, None
+            mt = k["metrics"]
+            if "dram__bytes_read.sum" not in mt or "dram__bytes_write.sum" not in mt:
+                return None, None, None
+            tot = val(mt["dram__bytes_read.sum"]) + val(mt["dram__bytes_write.sum"])
+            dur = val(mt["gpu__time_duration.sum"]) if "gpu__time_duration.sum" in mt else None
+            return int(tot), dur, os.path.basename(files[-1])
+    return None, None, None
+
+
+STAGE_KERNEL = {"pack": "k_pack", "sort": "k_bucket_rank", "dedupe": "k_dedupe",
+                "dict": "k_global_index", "probe": "k_probe_global", "edges": "k_tile_copy",
+                "layers": "k_gather_rows"}
 
 
 def run_ours(args):
@@ -245,12 +269,30 @@ def run_ours(args):
     # stage is several (2 one-sweep passes, bounds, bucket pass), each shorter
     dom = max(("pack", "probe", "dict"), key=lambda k: stage_us[k])
     achieved = ab[dom] / (stage_us[dom] * 1e-6) / 1e9
-    traffic, tsrc = _ncu_traffic(dom)
+    traffic, ncu_s, tsrc = _ncu_kernel(dom)
+    sb = survey_bytes(st, n, ell)
+    t_dom = stage_us[dom] * 1e-6
+    fracs = {
+        # compulsory bytes / live CUDA-event time: the headline
+        "compulsory": round(achieved / peak, 4),
+        # DRAM bytes ncu measured for one launch / live time (wasted re-reads count)
+        "ncu_dram": round(traffic / t_dom / 1e9 / peak, 4) if traffic else None,
+        # the same bytes over ncu's own (cold-cache, serialised) duration
+        "ncu_dram_ncu_time": round(traffic / ncu_s / 1e9 / peak, 4) if traffic and ncu_s else None,
+        # SURVEY 8.d.3's per-unit model (32 B per issued probe ...) / live time
+        "survey_8d": round(sb[dom] / t_dom / 1e9 / peak, 4) if dom in sb else None,
+    }
     roof = {"bound": "hbm", "kernel_stage": dom, "kernel": STAGE_KERNEL.get(dom),
             "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
             "traffic_source": tsrc, "alg_bytes_per_launch": int(ab[dom]),
-            "alg_bytes_def": "compulsory bytes, DESIGN.md section 6 (bench.alg_bytes)"}
+            "alg_bytes_def": "compulsory bytes, DESIGN.md section 6 (bench.alg_bytes)",
+            "fractions": fracs,
+            "survey_8d_bytes_per_launch": int(sb[dom]) if dom in sb else None}
+    # the sort stage under the survey model too (several kernels, one stage)
+    sort_fracs = {"compulsory": stages.get("sort", {}).get("frac"),
+                  "survey_8d": round(sb["sort"] / (stage_us["sort"] * 1e-6) / 1e9 / peak, 4)
+                  if stage_us.get("sort") else None}
     total_alg = sum(ab.values())
     whole = total_alg / (ms * 1e-3) / 1e9
     # ---- rows f1 / f4, measured alone (not part of the step)
@@ -282,6 +324,7 @@ def run_ours(args):
         "whole_path_alg_GBps": round(whole, 1),
         "whole_path_roofline_frac": round(whole / peak, 4),
         "roofline": roof,
+        "sort_roofline": sort_fracs,
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,

@@ -44,6 +44,9 @@ constexpr int kTileEdgeCap = kWarpEdgeCap;
 #ifndef PROBE_FR
 #define PROBE_FR 5  // filter loads in flight per round
 #endif
+#ifndef PROBE_ND
+#define PROBE_ND 3  // near window: rows i+1..i+ND taken from the warp's registers (W <= 2)
+#endif
 
 template <int WC>
 struct GRow {
@@ -122,6 +125,59 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       return Vp[w];
     };
     int kmax = -1;
+    // Near window (W <= 2, full dictionary): rows i+1..i+ND are the cells of
+    // lanes lane+1..lane+ND, or of the ND rows after the tile (loaded once by
+    // lanes 0..ND-1); taken by shuffle, they give lcp(V_i, V_{i+1}) and the
+    // near-bit hits without a T load or a row load
+    constexpr bool WIN = (WC == 1 || WC == 2) && !SUB && PROBE_ND > 0;
+    constexpr int ND = WIN ? PROBE_ND : 1;
+    constexpr int WW = WC > 0 ? WC : 1;
+    uint64_t rw[ND][WW];
+    bool rin[ND];
+    if (WIN) {
+      const int64_t er = i - lane + kTileCells + lane;  // row after the tile
+      uint64_t e[WW];
+#pragma unroll
+      for (int w = 0; w < WW; ++w) e[w] = 0ull;
+      if (lane < ND && er < g.n_cells) {
+        if (WC == 2) {
+          const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(g.keys + er * 2);
+          e[0] = x.x;
+          e[WW - 1] = x.y;
+        } else {
+          e[0] = g.keys[er];
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        const int src = (lane + d + 1) & 31;
+        const bool inw = lane + d + 1 < 32;
+#pragma unroll
+        for (int w = 0; w < WW; ++w) {
+          const uint64_t a = __shfl_sync(kFull, v[w], src);
+          const uint64_t c = __shfl_sync(kFull, e[w], src);
+          rw[d][w] = inw ? a : c;
+        }
+        rin[d] = row_ok && i + d + 1 < g.n_cells;
+      }
+      if (valid) {
+        if (lcp_prune) {
+          if (rin[0]) {
+            const uint64_t x0 = rw[0][0] ^ v[0];
+            int l;
+            if (WC == 2) {
+              const uint64_t x1 = rw[0][WW - 1] ^ v[WW - 1];
+              l = x0 ? __clzll(x0) : 64 + __clzll(x1);  // rows differ: x1 != 0 if x0 == 0
+            } else {
+              l = __clzll(x0);
+            }
+            kmax = min(l, g.ell - 1);
+          }
+        } else {
+          kmax = g.ell - 1;
+        }
+      }
+    } else {
     // the next row is the neighbouring lane's cell: take it by shuffle
     // (lane 31 and the end of the range load it)
     const bool nx_ok = row_ok && row + 1 < g.n_cells;  // the row has a successor row
@@ -163,6 +219,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         kmax = g.ell - 1;
       }
     }
+    }
     const uint64_t v0 = V(0);
     const uint64_t ci = uint64_t(i) << 32;
     // in-kernel hit key (q << 32 | row) -> canonical (i << 32 | j)
@@ -197,15 +254,33 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       }
     };
 
-    // ---- near: rows i+1.. in V's own b-prefix bucket
-    const bool near_on = kmax >= b;
+    // ---- near: rows i+1.. in V's own b-prefix bucket.  Every such row R is
+    // > V and shares V's first b bits, so it is a hit iff R ^ V is one bit
+    // (R = V | e_k, k >= b); the rows stay in the bucket up to its end.
     const uint64_t pv = b ? (v0 >> (64 - b)) : 0ull;
     // row indices fit in 32 bits (T is u32): 32-bit index arithmetic
     const uint32_t i32 = uint32_t(row);
-    uint32_t bucket_end = i32 + 1;
+    bool near_on = kmax >= b;
+    uint32_t r = i32 + 1;  // first row the scan below compares
+    if (WIN) {
+      // the window: rows i+1..i+ND from registers
+      bool inb = valid && near_on;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        const uint64_t x0 = rw[d][0] ^ v0;
+        inb = inb && rin[d] && (b == 0 || (x0 >> (64 - b)) == 0);
+        int diff = __popcll(x0);
+        if (WC == 2) diff += __popcll(rw[d][WW - 1] ^ v[WW - 1]);
+        my_issued += inb;
+        emit(inb && diff == 1, ci | uint64_t(i32 + uint32_t(d) + 1u));
+      }
+      near_on = inb;  // row i+ND is still in the bucket: scan on from i+ND+1
+      r = i32 + uint32_t(ND) + 1u;
+    }
+    const uint32_t r0 = r;
+    uint32_t bucket_end = r0;
     if (near_on) bucket_end = g.T[pv + 1];
-    const bool near_scan = near_on && (bucket_end - (i32 + 1) <= 16u);
-    uint32_t r = i32 + 1;
+    const bool near_scan = near_on && (bucket_end - r0 <= 16u);
     while (__any_sync(kFull, near_scan && r < bucket_end)) {
       bool hit[NR] = {};
       if (near_scan && r < bucket_end) {
@@ -265,7 +340,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
           z ^= bm;
           const int fw = cw;
           ++my_issued;
-          int64_t lo = row + 1, len = bucket_end - (row + 1);
+          int64_t lo = r0, len = int64_t(bucket_end) - r0;  // rows before r0 were compared
           while (len > 0) {
             const int64_t half = len >> 1;
             const uint64_t* R = g.keys + (lo + half) * W;

@@ -39,11 +39,15 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
 fns = list(lines)
 if not fns:
     sys.exit(f"no function matching {kname}")
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True,
-                     text=True).stdout
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-c", "1"],
+                     capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 h = r[1]
-rows = r[2:]
+rows = []
+for x in r[2:]:
+    if x and x[0] == "Kernel Name":
+        break  # the next profiled launch: keep the first one
+    rows.append(x)
 # the profiled instance: its mangled name from the report, else by SASS length
 mg = subprocess.run(["ncu", "-i", rep, "--print-kernel-base", "mangled", "--page", "details", "--csv"],
                     capture_output=True, text=True).stdout.splitlines()
