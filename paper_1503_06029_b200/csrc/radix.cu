@@ -64,9 +64,15 @@ __device__ __forceinline__ uint32_t digit_of(const K& k, int shift) {
   return uint32_t(KT<K>::top(k) >> shift) & 255u;
 }
 
+#ifndef OS_IPT16
+#define OS_IPT16 12  // 16-byte keys per thread and one-sweep tile
+#endif
+#ifndef OS_MINB
+#define OS_MINB 3  // resident one-sweep CTAs per SM (register bound)
+#endif
 template <class K, bool V>
 struct TileCfg {
-  static constexpr int IPT = sizeof(K) == 16 ? 12 : (V ? 12 : 16);
+  static constexpr int IPT = sizeof(K) == 16 ? OS_IPT16 : (V ? 12 : 16);
   static constexpr int TILE = kSortThreads * IPT;
   static constexpr size_t SMEM = size_t(TILE) * (sizeof(K) + (V ? 4 : 0));
 };
@@ -111,8 +117,11 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
 }
 
+#ifndef OS_UNSTABLE1
+#define OS_UNSTABLE1 1
+#endif
 template <class K, bool V>
-__global__ void __launch_bounds__(kSortThreads, 3)
+__global__ void __launch_bounds__(kSortThreads, OS_MINB)
     k_onesweep(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                uint32_t* __restrict__ vout, int64_t n, int shift,
                const uint32_t* __restrict__ bucket_base, uint64_t* status,
@@ -152,8 +161,17 @@ __global__ void __launch_bounds__(kSortThreads, 3)
     }
   }
   // warp-level stable ranking: items are visited in index order
-  // (item i of every lane precedes item i+1; lanes in order within an item)
+  // (item i of every lane precedes item i+1; lanes in order within an item).
+  // The first LSD pass (tile_pre given) needs no stability -- the input
+  // order is arbitrary -- so a shared atomic per item ranks it there
   const uint32_t lt = lanemask_lt();
+  if (OS_UNSTABLE1 && tile_pre) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const bool valid = wbase + i * 32 + lane < n;
+      if (valid) rank[i] = atomicAdd(&wcnt[w][digit_of(key[i], shift)], 1u);
+    }
+  } else
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const bool valid = wbase + i * 32 + lane < n;
