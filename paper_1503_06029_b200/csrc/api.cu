@@ -508,6 +508,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   DevBuf<uint32_t> popc(size_t(n), s);
   DevBuf<uint16_t> lcp(size_t(n), s);
   const uint64_t* sorted = nullptr;
+  DevBuf<uint32_t> order;  // W > 2: canonical order of the rows (gather + dedupe fused)
   bool done = false;
   int64_t nc = -1;
   uint32_t in_err = 0;
@@ -548,6 +549,9 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       radix_sort<uint64_t>(keys.p, alt.p, nullptr, nullptr, nullptr, false, ns, 64, &ko, nullptr,
                            s, &sst);
       sorted = ko;
+    } else if (gather_dedupe_ok(W)) {
+      order.alloc(size_t(ns), s);  // canonical order; the rows move once, in the dedupe
+      sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p);
     } else {
       sort_rows_multiword(keys.p, ns, W, alt.p, s, &sst);
       sorted = alt.p;
@@ -557,7 +561,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   if (nc < 0) {
     // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
     cellbuf.alloc(size_t(ns) * W, s, Mem::Persist);
-    launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+    if (order.p) launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+    else launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
   } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the
     // layered dictionary (the global-dictionary probe derives lcp itself)

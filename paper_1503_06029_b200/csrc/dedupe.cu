@@ -116,6 +116,108 @@ __global__ void __launch_bounds__(kDedupThreads)
   }
 }
 
+// ---- W > 2: gather + dedupe in one warp-cooperative pass.  The multi-word
+// sort returns the canonical order as row indices; this kernel moves the
+// rows in that order and flags the first row of each run of equal rows
+// in the same pass.  L lanes per row (W <= L <= 32), lane w moving
+// word w, so a row is ONE contiguous access of the warp (the north star's
+// warp-cooperative compares for long ell: with a thread per row every load
+// instruction touched 32 different rows).  A warp owns 32 consecutive sorted
+// positions, R = 32 / L rows per step; the previous row of a group is the
+// group before it (or the last group of the previous step) by shuffle.
+template <int L>
+__global__ void __launch_bounds__(256)
+    k_gather_dedupe(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
+                    int64_t n, int W, uint64_t* __restrict__ cells, uint32_t* __restrict__ popc,
+                    uint16_t* __restrict__ lcp_out, uint64_t* status, uint32_t* tile_counter,
+                    uint32_t* n_cells) {
+  constexpr int R = 32 / L;  // rows per warp step
+  constexpr int S = 32 / R;  // steps per warp (32 rows)
+  constexpr int NWARP = 8;
+  constexpr int TILE = NWARP * 32;
+  __shared__ uint32_t s_warp[NWARP];
+  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_pop[NWARP][32];
+  __shared__ uint16_t s_lcp[NWARP][32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int q = lane / L, w = lane % L;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t wb = tile * TILE + int64_t(wid) * 32;
+  uint64_t val[S];
+  uint32_t flags = 0;  // bit r: sorted position wb + r starts a cell (all lanes)
+  uint64_t xp = 0;     // previous step's word (group R-1 holds the row before group 0)
+  {
+    const int64_t g = wb - 1;  // the row before the warp's first position
+    if (q == R - 1 && g >= 0 && g < n && w < W) xp = keys[int64_t(order[g]) * W + w];
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int64_t g = wb + s * R + q;
+    const bool ok = g < n;
+    const uint64_t x = (ok && w < W) ? keys[int64_t(order[g]) * W + w] : 0ull;
+    const uint64_t a = __shfl_sync(kFull, x, (lane + 32 - L) & 31);
+    const uint64_t c = __shfl_sync(kFull, xp, (R - 1) * L + w);
+    const uint64_t d = x ^ (q > 0 ? a : c);
+    xp = x;
+    const uint32_t gm = L == 32 ? kFull : (((1u << L) - 1u) << (q * L));
+    const uint32_t gd = __ballot_sync(kFull, d != 0) & gm;
+    const bool flag = ok && (g == 0 || gd != 0);
+    const uint32_t fb = __ballot_sync(kFull, flag && w == 0);
+#pragma unroll
+    for (int qq = 0; qq < R; ++qq) flags |= ((fb >> (qq * L)) & 1u) << (s * R + qq);
+    uint32_t pc = __popcll(x);
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) pc += __shfl_xor_sync(kFull, pc, o);
+    // lcp(previous row, this row): the first differing word of the group
+    const int f = gd ? __ffs(gd) - 1 : lane;
+    const uint64_t xd = __shfl_sync(kFull, d, f);
+    if (w == 0 && ok) {
+      s_pop[wid][s * R + q] = pc;
+      s_lcp[wid][s * R + q] = gd ? uint16_t((f - q * L) * 64 + __clzll(xd)) : uint16_t(0xffff);
+    }
+    val[s] = x;
+  }
+  if (lane == 0) s_warp[wid] = __popc(flags);
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t run = 0, mine = 0;
+    for (int ww = 0; ww < NWARP; ++ww) {
+      const uint32_t c = s_warp[ww];
+      if (lane == ww) mine = run;
+      run += c;
+    }
+    __syncwarp();
+    if (lane < NWARP) s_warp[lane] = mine;
+    const uint32_t base = lookback_warp(status, tile, run, 1);
+    if (lane == 0) {
+      s_base = base;
+      if (tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
+    }
+  }
+  __syncthreads();
+  const uint32_t c0 = s_base + s_warp[wid];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int r = s * R + q;
+    const int64_t g = wb + r;
+    if (g < n) {
+      // cell of row g = (flags at rows <= g) - 1
+      const uint32_t cell = c0 + __popc(flags & (0xffffffffu >> (31 - r))) - 1;
+      if ((flags >> r) & 1u) {
+        if (w < W) cells[int64_t(cell) * W + w] = val[s];
+        if (w == 0) {
+          popc[cell] = s_pop[wid][r];
+          if (g > 0) lcp_out[cell - 1] = s_lcp[wid][r];  // the previous cell vs this one
+        }
+      }
+      if (w == 0 && g + 1 == n) lcp_out[cell] = 0xffff;
+    }
+  }
+}
+
 template <int WC>
 __global__ void k_cell_meta(const uint64_t* __restrict__ cells, int64_t nc, int W,
                             uint32_t* __restrict__ popc, uint16_t* __restrict__ lcp) {
@@ -211,6 +313,27 @@ void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, 
     case 2: k_cell_meta<2><<<g, 256, 0, s>>>(cells, nc, W, popc, lcp); break;
     default: k_cell_meta<0><<<g, 256, 0, s>>>(cells, nc, W, popc, lcp); break;
   }
+  CG_LAUNCH_CHECK();
+}
+
+bool gather_dedupe_ok(int W) { return W > 2 && W <= 32; }
+
+void launch_gather_dedupe(const uint64_t* keys, const uint32_t* order, int64_t n, int W,
+                          uint64_t* cells, uint32_t* popc, uint16_t* lcp, uint32_t* n_cells,
+                          cudaStream_t s) {
+  constexpr int TILE = 256;
+  const int64_t tiles = (n + TILE - 1) / TILE;
+  DevBuf<uint64_t> status(size_t(tiles), s);
+  DevBuf<uint32_t> counter(1, s);
+  CG_CUDA(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint64_t), s));
+  CG_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(uint32_t), s));
+  const unsigned g = unsigned(tiles);
+#define CG_GD_ARGS keys, order, n, W, cells, popc, lcp, status.p, counter.p, n_cells
+  if (W <= 4) k_gather_dedupe<4><<<g, 256, 0, s>>>(CG_GD_ARGS);
+  else if (W <= 8) k_gather_dedupe<8><<<g, 256, 0, s>>>(CG_GD_ARGS);
+  else if (W <= 16) k_gather_dedupe<16><<<g, 256, 0, s>>>(CG_GD_ARGS);
+  else k_gather_dedupe<32><<<g, 256, 0, s>>>(CG_GD_ARGS);
+#undef CG_GD_ARGS
   CG_LAUNCH_CHECK();
 }
 

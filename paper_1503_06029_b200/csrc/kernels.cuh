@@ -70,9 +70,11 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
                 cudaStream_t s, SortStats* st);
 
 // Canonical sort of packed rows u64[n][W] (W >= 2): LSD over words W-1..0
-// on (word, u32 index) pairs, then a row gather into `sorted` (u64[n][W]).
+// on (word, u32 index) pairs, then a row gather into `sorted` (u64[n][W]);
+// with `order` given, the canonical order (row indices) goes there instead
+// and no rows move.
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st);
+                         cudaStream_t s, SortStats* st, uint32_t* order = nullptr);
 
 // MSD fast path for W in {1, 2}: LSD passes over the top B bits only (whole
 // keys move), then a shared-memory bitonic sort of each 2^B prefix bucket.
@@ -123,6 +125,12 @@ int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, 
 // *n_cells (device u32).
 void launch_dedupe(const uint64_t* sorted, int64_t n, int W, uint64_t* cells, uint32_t* popc,
                    uint16_t* lcp, uint32_t* n_cells, cudaStream_t s);
+// 2 < W <= 32: the same from the UNSORTED rows keys[.][W] and the canonical
+// order (row indices): gather + dedupe in one warp-cooperative pass.
+bool gather_dedupe_ok(int W);
+void launch_gather_dedupe(const uint64_t* keys, const uint32_t* order, int64_t n, int W,
+                          uint64_t* cells, uint32_t* popc, uint16_t* lcp, uint32_t* n_cells,
+                          cudaStream_t s);
 
 // ---------------------------------------------------------------- a4/a5 layers + dictionary
 // Prefix filter: per layer p a bitmap over the top (b_p + kFilterExtra) bits

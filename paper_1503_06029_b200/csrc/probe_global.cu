@@ -44,6 +44,9 @@ constexpr int kTileEdgeCap = kWarpEdgeCap;
 #ifndef PROBE_FR
 #define PROBE_FR 5  // filter loads in flight per round
 #endif
+#ifndef PROBE_STG
+#define PROBE_STG 1  // W in (2, 16]: tile rows staged in shared memory
+#endif
 #ifndef PROBE_ND
 #define PROBE_ND 3  // near window: rows i+1..i+ND taken from the warp's registers (W <= 2)
 #endif
@@ -77,8 +80,20 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
 // keyed (q << 32 | dictionary row) inside the kernel and converted to
 // canonical (i << 32 | j) when written (idx is increasing, so the order is
 // the same).  Without SUB, q = row = canonical index.
-template <int WC, bool SUB = false, int FR = PROBE_FR, int NR = 2, int SR = 2>
-__global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
+// STG (2 < W <= kStgMaxW, full dictionary): the warp first copies its tile's
+// 32 rows and the kStgExtra rows after it into shared memory with coalesced
+// loads (a row is W contiguous words, lanes over words); the cells' own
+// words, lcp(V_i, V_{i+1}), the near-bucket compares and the survivors'
+// owner words are then read from there.  With a thread per cell straight
+// from global memory every load instruction touched 32 different rows (the
+// north star's warp-cooperative handling of long ell).
+constexpr int kStgMaxW = 16;
+constexpr int kStgExtra = 4;
+constexpr int kStgRows = kTileCells + kStgExtra;
+size_t probe_stg_smem(int W) { return size_t(kProbeWarps) * kStgRows * (W + 1) * 8; }
+
+template <int WC, bool SUB = false, int FR = PROBE_FR, int NR = 2, int SR = 2, bool STG = false>
+__global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ tcnt,
                    uint64_t* __restrict__ tpos, uint32_t* ticket,
@@ -87,6 +102,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
                    uint4* __restrict__ ovf, uint32_t* ovf_n,
                    const uint8_t* __restrict__ tile_sel) {
   __shared__ uint64_t ebuf[kProbeWarps][kWarpEdgeCap];
+  extern __shared__ __align__(16) uint64_t stg_raw[];  // STG: [warp][kStgRows][W + 1]
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t lt = lanemask_lt();
   const int W = WC > 0 ? WC : g.W;
@@ -109,6 +125,23 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
     const bool row_ok = SUB ? valid : (i < g.n_cells);  // row exists (a shuffle source past i_hi)
     // ---- the cell
     const uint64_t* Vp = g.keys + (row_ok ? row : 0) * W;
+    const int SW = W + 1;  // STG row stride in words (odd: lanes hit different banks)
+    uint64_t* srw = nullptr;
+    int64_t stg_r0 = 0, stg_n = 0;  // STG: first staged row, staged rows
+    if (STG) {
+      srw = stg_raw + (tid >> 5) * (kStgRows * SW);
+      stg_r0 = i - lane;
+      stg_n = min(int64_t(kStgRows), g.n_cells - stg_r0);
+      // lanes over words: Wp = pow2 >= W lanes per row, 32 / Wp rows per step
+      const int lw = W <= 4 ? 2 : (W <= 8 ? 3 : 4);
+      const int wq = lane & ((1 << lw) - 1), rq = lane >> lw;
+      const int per = 32 >> lw;
+      __syncwarp();  // the previous tile's reads of the buffer are done
+      for (int rr = rq; rr < int(stg_n); rr += per)
+        if (wq < W) srw[rr * SW + wq] = g.keys[(stg_r0 + rr) * W + wq];
+      __syncwarp();
+      if (row_ok) Vp = srw + lane * SW;
+    }
     uint64_t v[WC > 0 ? WC : 1];
     if (WC > 0) {
 #pragma unroll
@@ -199,7 +232,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
       if (lcp_prune) {
         // lcp(V_i, V_{i+1}); the last cell has no successor and probes nothing
         if (nx_ok) {
-          const uint64_t* Np = g.keys + (row + 1) * W;
+          const uint64_t* Np = (STG && lane + 1 < stg_n) ? Vp + SW : g.keys + (row + 1) * W;
           const bool shfl = WC > 0;
           int l = -1;
           const int n = WC > 0 ? WC : W;
@@ -288,7 +321,8 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         for (int u = 0; u < NR; ++u) {
           const uint32_t rr = r + u;
           if (rr < bucket_end) {
-            const uint64_t* R = g.keys + size_t(rr) * W;
+            const int64_t so = int64_t(rr) - stg_r0;
+            const uint64_t* R = (STG && so < stg_n) ? srw + so * SW : g.keys + size_t(rr) * W;
             uint64_t miss = 0;
             int diff = 0;
             if (WC == 2) {
@@ -485,7 +519,8 @@ __global__ void __launch_bounds__(32 * kProbeWarps, PROBE_MIN_BLOCKS)
         const uint64_t t0 = o_v0 | bm;
         const int64_t x = int64_t(t0 >> (64 - b));
         const uint32_t lo = g.T[x], hi = g.T[x + 1];
-        const uint64_t* OV = g.keys + size_t(o_i) * W;  // owner's row (W > 2 path)
+        // owner's row (W > 2 path; STG: the owner's staged row)
+        const uint64_t* OV = STG ? srw + owner * SW : g.keys + size_t(o_i) * W;
         int64_t found = -1;
         if (hi - lo <= 12) {
           for (uint32_t rr = lo; rr < hi && found < 0; rr += SR) {
@@ -664,8 +699,17 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
       else k_probe_global<2><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
       break;
     default:
-      if (sub) k_probe_global<0, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
-      else k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      if (sub) {
+        k_probe_global<0, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      } else if (g.W <= kStgMaxW && PROBE_STG) {
+        auto kern = k_probe_global<0, false, PROBE_FR, 2, 2, true>;
+        const size_t sm = probe_stg_smem(g.W);
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        const int gs = int(std::min<int64_t>((ntiles + kProbeWarps - 1) / kProbeWarps, int64_t(num_sms()) * 3));
+        kern<<<gs, 32 * kProbeWarps, sm, s>>>(CG_PROBE_ARGS);
+      } else {
+        k_probe_global<0><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+      }
       break;
   }
 #undef CG_PROBE_ARGS

@@ -1332,7 +1332,11 @@ __global__ void k_tie_fix(const uint64_t* __restrict__ keys, int W, const uint64
 }  // namespace
 
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st) {
+                         cudaStream_t s, SortStats* st, uint32_t* order) {
+  auto finish = [&](const uint32_t* idx) {
+    if (order) CG_CUDA(cudaMemcpyAsync(order, idx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+    else launch_gather_rows(keys, idx, n, W, sorted, s);
+  };
   DevBuf<uint64_t> kw(size_t(n), s), kw_alt(size_t(n), s);
   DevBuf<uint32_t> ia(size_t(n), s), ib(size_t(n), s);
   {
@@ -1352,7 +1356,7 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
     CG_CUDA(cudaStreamSynchronize(s));
     if (h[0] == 0) {
-      launch_gather_rows(keys, vo, n, W, sorted, s);
+      finish(vo);
       return;
     }
   }
@@ -1367,7 +1371,7 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     radix_sort<uint64_t>(kw.p, kw_alt.p, idx, vals, vals_alt, true, n, 64, &ko, &vo, s, st);
     idx = vo;
   }
-  launch_gather_rows(keys, idx, n, W, sorted, s);
+  finish(idx);
 }
 
 int msd_prefix_bits(int64_t n) {

@@ -13,21 +13,23 @@ import synth  # noqa: E402
 from paper_1503_06029_b200 import cg  # noqa: E402
 
 dev = torch.device("cuda:0")
-for name in ("C1", "C2", "C3", "C3F", "C4"):
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C1", "C2", "C3", "C3F", "C4"]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+for name in names:
     d = synth.config(name)
     if "bytes" in d and d["bytes"] is not None:
         x = torch.from_numpy(d["bytes"]).to(dev)
     else:
         x = synth.unpack_words_torch(torch.from_numpy(d["words"].view(np.int64)).to(dev), d["ell"])
     ts, st = [], None
-    for i in range(7):
+    for i in range(reps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         r = cg.build(x, want_stats=True)
         e1.record()
         torch.cuda.synchronize()
-        if i >= 2:
+        if i >= min(2, reps - 1):
             ts.append(e0.elapsed_time(e1))
         st = r.stats
     print(json.dumps({"config": name, "n": int(x.shape[0]), "ell": int(x.shape[1]),
