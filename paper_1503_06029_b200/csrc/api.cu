@@ -561,7 +561,12 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   if (nc < 0) {
     // ---- a3 dedupe + compaction (separate pass: LSD / multi-word paths)
     cellbuf.alloc(size_t(ns) * W, s, Mem::Persist);
-    if (order.p) launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
+    // (the global dictionary needs neither popcounts nor lcp: the probe
+    // derives lcp from the next row)
+    const bool meta = sh.cells_only || o.dict_kind != CG_DICT_GLOBAL;
+    if (order.p)
+      launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, meta ? popc.p : nullptr,
+                           meta ? lcp.p : nullptr, d_flags + 1, s);
     else launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
   } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the

@@ -218,6 +218,58 @@ __device__ __forceinline__ uint32_t lookback_warp(uint64_t* status, int64_t tile
   return excl;
 }
 
+// Single-slot look-back run by the WHOLE CTA (blockDim.x threads, a multiple
+// of 32, <= 1024): each round loads the statuses of blockDim.x predecessors
+// at once.  With short tiles the nearest inclusive prefix lies about as many
+// tiles back as are in flight (hundreds); a warp needed one L2 round trip per
+// 32 of them.  `tmp` needs 3 * 32 + 1 words of shared memory.  Every thread
+// gets the exclusive prefix.
+__device__ __forceinline__ uint32_t lookback_block(uint64_t* status, int64_t tile, uint32_t agg,
+                                                   uint32_t epoch, uint32_t* tmp) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int nt = blockDim.x;
+  if (tile == 0) {
+    if (tid == 0) st_relaxed_u64(status, lb_pack(2, epoch, agg));
+    return 0;
+  }
+  if (tid == 0) st_relaxed_u64(status + tile, lb_pack(1, epoch, agg));
+  const uint32_t ep = epoch & 0x3fffffffu;
+  uint32_t excl = 0;
+  int64_t j = tile - 1;
+  while (true) {
+    const int64_t jj = j - tid;
+    const uint64_t s = jj >= 0 ? ld_relaxed_u64(status + jj) : lb_pack(2, epoch, 0);
+    const uint32_t flag = uint32_t(s >> 62);
+    const bool ready = flag != 0 && ((uint32_t(s >> 32) & 0x3fffffffu) == ep);
+    const uint32_t nr = __ballot_sync(kFull, !ready);
+    const uint32_t inc = __ballot_sync(kFull, ready && flag == 2);
+    if (lane == 0) {
+      tmp[wid] = nr ? uint32_t(wid * 32 + __ffs(nr) - 1) : uint32_t(nt);
+      tmp[32 + wid] = inc ? uint32_t(wid * 32 + __ffs(inc) - 1) : uint32_t(nt);
+    }
+    __syncthreads();
+    int first_nr = nt, first_inc = nt;
+    for (int w = 0; w < nw; ++w) {
+      first_nr = min(first_nr, int(tmp[w]));
+      first_inc = min(first_inc, int(tmp[32 + w]));
+    }
+    const int take = first_nr < first_inc ? first_nr : (first_inc < nt ? first_inc + 1 : nt);
+    uint32_t v = tid < take ? uint32_t(s) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) tmp[64 + wid] = v;
+    __syncthreads();
+    uint32_t sum = 0;
+    for (int w = 0; w < nw; ++w) sum += tmp[64 + w];
+    excl += sum;
+    __syncthreads();  // tmp is rewritten by the next round
+    if (first_inc < nt && first_inc < first_nr) break;
+    j -= take;  // take == first_nr (spin there) or nt (all aggregates)
+  }
+  if (tid == 0) st_relaxed_u64(status + tile, lb_pack(2, epoch, excl + agg));
+  return excl;
+}
+
 // Block-wide exclusive scan of one u32 per thread (blockDim.x multiple of 32,
 // <= 1024).  `tmp` needs 33 words of shared memory.  Returns the total in *total.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {

@@ -136,10 +136,10 @@ __global__ void __launch_bounds__(256)
   constexpr int NWARP = 8;
   constexpr int TILE = NWARP * 32;
   __shared__ uint32_t s_warp[NWARP];
-  __shared__ uint32_t s_base;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_pop[NWARP][32];
   __shared__ uint16_t s_lcp[NWARP][32];
+  __shared__ uint32_t s_lb[97];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int q = lane / L, w = lane % L;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -153,11 +153,17 @@ __global__ void __launch_bounds__(256)
     const int64_t g = wb - 1;  // the row before the warp's first position
     if (q == R - 1 && g >= 0 && g < n && w < W) xp = keys[int64_t(order[g]) * W + w];
   }
+  // all of the warp's rows in flight first, then the compares
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int64_t g = wb + s * R + q;
+    val[s] = (g < n && w < W) ? keys[int64_t(order[g]) * W + w] : 0ull;
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int64_t g = wb + s * R + q;
     const bool ok = g < n;
-    const uint64_t x = (ok && w < W) ? keys[int64_t(order[g]) * W + w] : 0ull;
+    const uint64_t x = val[s];
     const uint64_t a = __shfl_sync(kFull, x, (lane + 32 - L) & 31);
     const uint64_t c = __shfl_sync(kFull, xp, (R - 1) * L + w);
     const uint64_t d = x ^ (q > 0 ? a : c);
@@ -168,37 +174,31 @@ __global__ void __launch_bounds__(256)
     const uint32_t fb = __ballot_sync(kFull, flag && w == 0);
 #pragma unroll
     for (int qq = 0; qq < R; ++qq) flags |= ((fb >> (qq * L)) & 1u) << (s * R + qq);
-    uint32_t pc = __popcll(x);
+    if (popc) {  // per-cell metadata for the layered dictionary (uniform branch)
+      uint32_t pc = __popcll(x);
 #pragma unroll
-    for (int o = L / 2; o > 0; o >>= 1) pc += __shfl_xor_sync(kFull, pc, o);
-    // lcp(previous row, this row): the first differing word of the group
-    const int f = gd ? __ffs(gd) - 1 : lane;
-    const uint64_t xd = __shfl_sync(kFull, d, f);
-    if (w == 0 && ok) {
-      s_pop[wid][s * R + q] = pc;
-      s_lcp[wid][s * R + q] = gd ? uint16_t((f - q * L) * 64 + __clzll(xd)) : uint16_t(0xffff);
+      for (int o = L / 2; o > 0; o >>= 1) pc += __shfl_xor_sync(kFull, pc, o);
+      // lcp(previous row, this row): the first differing word of the group
+      const int f = gd ? __ffs(gd) - 1 : lane;
+      const uint64_t xd = __shfl_sync(kFull, d, f);
+      if (w == 0 && ok) {
+        s_pop[wid][s * R + q] = pc;
+        s_lcp[wid][s * R + q] = gd ? uint16_t((f - q * L) * 64 + __clzll(xd)) : uint16_t(0xffff);
+      }
     }
-    val[s] = x;
   }
   if (lane == 0) s_warp[wid] = __popc(flags);
   __syncthreads();
-  if (wid == 0) {
-    uint32_t run = 0, mine = 0;
-    for (int ww = 0; ww < NWARP; ++ww) {
-      const uint32_t c = s_warp[ww];
-      if (lane == ww) mine = run;
-      run += c;
-    }
-    __syncwarp();
-    if (lane < NWARP) s_warp[lane] = mine;
-    const uint32_t base = lookback_warp(status, tile, run, 1);
-    if (lane == 0) {
-      s_base = base;
-      if (tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
-    }
+  uint32_t run = 0, mine = 0;
+  for (int ww = 0; ww < NWARP; ++ww) {
+    const uint32_t c = s_warp[ww];
+    if (ww == wid) mine = run;
+    run += c;
   }
-  __syncthreads();
-  const uint32_t c0 = s_base + s_warp[wid];
+  // the whole CTA looks back (256 predecessors per round)
+  const uint32_t base = lookback_block(status, tile, run, 1, s_lb);
+  if (tid == 0 && tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
+  const uint32_t c0 = base + mine;
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int r = s * R + q;
@@ -208,12 +208,12 @@ __global__ void __launch_bounds__(256)
       const uint32_t cell = c0 + __popc(flags & (0xffffffffu >> (31 - r))) - 1;
       if ((flags >> r) & 1u) {
         if (w < W) cells[int64_t(cell) * W + w] = val[s];
-        if (w == 0) {
+        if (popc && w == 0) {
           popc[cell] = s_pop[wid][r];
           if (g > 0) lcp_out[cell - 1] = s_lcp[wid][r];  // the previous cell vs this one
         }
       }
-      if (w == 0 && g + 1 == n) lcp_out[cell] = 0xffff;
+      if (popc && w == 0 && g + 1 == n) lcp_out[cell] = 0xffff;
     }
   }
 }

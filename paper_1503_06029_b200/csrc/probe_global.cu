@@ -137,8 +137,16 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
       const int wq = lane & ((1 << lw) - 1), rq = lane >> lw;
       const int per = 32 >> lw;
       __syncwarp();  // the previous tile's reads of the buffer are done
-      for (int rr = rq; rr < int(stg_n); rr += per)
-        if (wq < W) srw[rr * SW + wq] = g.keys[(stg_r0 + rr) * W + wq];
+      // asynchronous copies (cp.async, no register round trip): all of the
+      // lane's words are in flight at once
+      if (wq < W)
+        for (int rr = rq; rr < int(stg_n); rr += per) {
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(srw + rr * SW + wq));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d),
+                       "l"(g.keys + (stg_r0 + rr) * W + wq)
+                       : "memory");
+        }
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
       if (row_ok) Vp = srw + lane * SW;
     }

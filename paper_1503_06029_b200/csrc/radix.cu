@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
 }
 
+#ifndef MW_PREFIX32
+#define MW_PREFIX32 1  // W > 2: sort on (32-bit prefix, index) first (4 passes)
+#endif
 #ifndef OS_UNSTABLE1
 #define OS_UNSTABLE1 1
 #endif
@@ -1331,15 +1334,92 @@ __global__ void k_tie_fix(const uint64_t* __restrict__ keys, int W, const uint64
 }
 }  // namespace
 
+namespace {
+// (top 32 bits of word 0) << 32 | row index: one u64 sort key per row
+__global__ void k_prefix_idx(const uint64_t* __restrict__ keys, int W, int64_t n,
+                             uint64_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = (keys[i * W] & 0xffffffff00000000ull) | uint64_t(i);
+}
+
+// pk sorted on the high halves (stable: equal prefixes in index order) ->
+// the canonical order of the rows: positions outside runs of equal prefixes
+// keep their index; the head of a run (<= kTieRun rows) insertion-sorts the
+// run's indices on the full rows (equal rows keep index order).  A longer
+// run raises *long_run (the caller then sorts every word).
+__global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
+                                 const uint64_t* __restrict__ pk, int64_t n,
+                                 uint32_t* __restrict__ order, uint32_t* __restrict__ long_run) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t k = uint32_t(pk[i] >> 32);
+    const bool head = i == 0 || uint32_t(pk[i - 1] >> 32) != k;
+    const bool run = i + 1 < n && uint32_t(pk[i + 1] >> 32) == k;
+    if (!head) continue;  // inside a run: its head writes it
+    if (!run) {
+      order[i] = uint32_t(pk[i]);
+      continue;
+    }
+    int64_t e = i + 2;
+    while (e < n && uint32_t(pk[e] >> 32) == k && e - i <= kTieRun) ++e;
+    if (e - i > kTieRun) {
+      atomicOr(long_run, 1u);
+      continue;
+    }
+    for (int64_t a = i; a < e; ++a) {
+      const uint32_t v = uint32_t(pk[a]);
+      const uint64_t* rv = keys + int64_t(v) * W;
+      int64_t z = a;
+      while (z > i) {
+        const uint32_t u = order[z - 1];
+        const uint64_t* ru = keys + int64_t(u) * W;
+        int c = 0;
+        for (int w = 0; w < W && c == 0; ++w) c = ru[w] < rv[w] ? -1 : (ru[w] > rv[w] ? 1 : 0);
+        if (c < 0 || (c == 0 && u < v)) break;
+        order[z] = u;
+        --z;
+      }
+      order[z] = v;
+    }
+  }
+}
+}  // namespace
+
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
                          cudaStream_t s, SortStats* st, uint32_t* order) {
   auto finish = [&](const uint32_t* idx) {
     if (order) CG_CUDA(cudaMemcpyAsync(order, idx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     else launch_gather_rows(keys, idx, n, W, sorted, s);
   };
+  bool tried = false;
+  if (order && MW_PREFIX32) {
+    // u64 keys (top 32 bits of word 0, row index): 4 stable keys-only passes
+    // on the high half (digit bases scanned on the device: no host round
+    // trip), then the runs of equal 32-bit prefixes are ordered on the full
+    // rows -- planted/random rows leave runs of 1-2 rows
+    DevBuf<uint64_t> pk(size_t(n), s), pk_alt(size_t(n), s);
+    DevBuf<uint32_t> hist(4 * kRadix, s), flag(1, s);
+    k_prefix_idx<<<grid_for(n, 256), 256, 0, s>>>(keys, W, n, pk.p);
+    CG_LAUNCH_CHECK();
+    CG_CUDA(cudaMemsetAsync(hist.p, 0, hist.n * sizeof(uint32_t), s));
+    CG_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+    k_digit_hist<uint64_t><<<grid_for(n, 256, 4), 256, 0, s>>>(pk.p, n, 4, 8, hist.p);
+    CG_LAUNCH_CHECK();
+    uint64_t* ko = nullptr;
+    radix_passes<uint64_t>(pk.p, pk_alt.p, nullptr, nullptr, nullptr, false, n, 4, 8, &ko, nullptr,
+                           s, st, hist.p);
+    k_tie_fix_prefix<<<grid_for(n, 256), 256, 0, s>>>(keys, W, ko, n, order, flag.p);
+    CG_LAUNCH_CHECK();
+    uint32_t* h = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+    CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (h[0] == 0) return;
+    tried = true;  // long runs of equal prefixes (arrangement data): every word
+  }
   DevBuf<uint64_t> kw(size_t(n), s), kw_alt(size_t(n), s);
   DevBuf<uint32_t> ia(size_t(n), s), ib(size_t(n), s);
-  {
+  if (!tried) {
     // word 0 decides most orders: sort (word 0, index), then order the runs
     // of equal word 0 on the remaining words; only if a run is long (heavy
     // word-0 ties, e.g. arrangement signatures) sort every word (LSD below)
