@@ -509,6 +509,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   DevBuf<uint16_t> lcp(size_t(n), s);
   const uint64_t* sorted = nullptr;
   DevBuf<uint32_t> order;  // W > 2: canonical order of the rows (gather + dedupe fused)
+  bool no_dups = false;    // W > 2: the sort saw no two equal rows
   bool done = false;
   int64_t nc = -1;
   uint32_t in_err = 0;
@@ -551,7 +552,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       sorted = ko;
     } else if (gather_dedupe_ok(W)) {
       order.alloc(size_t(ns), s);  // canonical order; the rows move once, in the dedupe
-      sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p);
+      sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups);
     } else {
       sort_rows_multiword(keys.p, ns, W, alt.p, s, &sst);
       sorted = alt.p;
@@ -564,7 +565,13 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     // (the global dictionary needs neither popcounts nor lcp: the probe
     // derives lcp from the next row)
     const bool meta = sh.cells_only || o.dict_kind != CG_DICT_GLOBAL;
-    if (order.p)
+    if (order.p && no_dups) {
+      // every row is a cell (the sort compared all ties): one gather, a
+      // thread per word; n_c = n
+      launch_gather_rows(keys.p, order.p, ns, W, cellbuf.p, s);
+      nc = ns;
+      if (meta) launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
+    } else if (order.p)
       launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, meta ? popc.p : nullptr,
                            meta ? lcp.p : nullptr, d_flags + 1, s);
     else launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);

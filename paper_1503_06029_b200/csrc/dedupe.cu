@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kDedupThreads)
 // instruction touched 32 different rows).  A warp owns 32 consecutive sorted
 // positions, R = 32 / L rows per step; the previous row of a group is the
 // group before it (or the last group of the previous step) by shuffle.
+#ifndef GD_NOLB
+#define GD_NOLB 0
+#endif
 template <int L>
 __global__ void __launch_bounds__(256)
     k_gather_dedupe(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
@@ -151,13 +154,14 @@ __global__ void __launch_bounds__(256)
   uint64_t xp = 0;     // previous step's word (group R-1 holds the row before group 0)
   {
     const int64_t g = wb - 1;  // the row before the warp's first position
-    if (q == R - 1 && g >= 0 && g < n && w < W) xp = keys[int64_t(order[g]) * W + w];
+    if (q == R - 1 && g >= 0 && g < n && w < W) xp = keys[(order ? int64_t(order[g]) : g) * W + w];
   }
   // all of the warp's rows in flight first, then the compares
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int64_t g = wb + s * R + q;
-    val[s] = (g < n && w < W) ? keys[int64_t(order[g]) * W + w] : 0ull;
+    const int64_t src = order ? int64_t(order[g < n ? g : 0]) : g;  // no order: rows already sorted
+    val[s] = (g < n && w < W) ? keys[src * W + w] : 0ull;
   }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -196,7 +200,11 @@ __global__ void __launch_bounds__(256)
     run += c;
   }
   // the whole CTA looks back (256 predecessors per round)
+#if GD_NOLB  // diagnostics only (wrong output): the kernel without its look-back
+  const uint32_t base = uint32_t(tile) * TILE;
+#else
   const uint32_t base = lookback_block(status, tile, run, 1, s_lb);
+#endif
   if (tid == 0 && tile * TILE < n && (tile + 1) * TILE >= n) *n_cells = base + run;
   const uint32_t c0 = base + mine;
 #pragma unroll

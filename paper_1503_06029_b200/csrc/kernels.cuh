@@ -73,8 +73,11 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
 // on (word, u32 index) pairs, then a row gather into `sorted` (u64[n][W]);
 // with `order` given, the canonical order (row indices) goes there instead
 // and no rows move.
+// *no_dups (optional) = true when the order is known to hold no two equal
+// rows (the 32-bit-prefix path compared every tie and found none).
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st, uint32_t* order = nullptr);
+                         cudaStream_t s, SortStats* st, uint32_t* order = nullptr,
+                         bool* no_dups = nullptr);
 
 // MSD fast path for W in {1, 2}: LSD passes over the top B bits only (whole
 // keys move), then a shared-memory bitonic sort of each 2^B prefix bucket.

@@ -1376,6 +1376,7 @@ __global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
         const uint64_t* ru = keys + int64_t(u) * W;
         int c = 0;
         for (int w = 0; w < W && c == 0; ++w) c = ru[w] < rv[w] ? -1 : (ru[w] > rv[w] ? 1 : 0);
+        if (c == 0) atomicOr(long_run, 2u);  // equal rows: the dedupe has work
         if (c < 0 || (c == 0 && u < v)) break;
         order[z] = u;
         --z;
@@ -1387,7 +1388,8 @@ __global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
 }  // namespace
 
 void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st, uint32_t* order) {
+                         cudaStream_t s, SortStats* st, uint32_t* order, bool* no_dups) {
+  if (no_dups) *no_dups = false;
   auto finish = [&](const uint32_t* idx) {
     if (order) CG_CUDA(cudaMemcpyAsync(order, idx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     else launch_gather_rows(keys, idx, n, W, sorted, s);
@@ -1414,7 +1416,10 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     uint32_t* h = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
     CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
     CG_CUDA(cudaStreamSynchronize(s));
-    if (h[0] == 0) return;
+    if ((h[0] & 1u) == 0) {
+      if (no_dups) *no_dups = (h[0] & 2u) == 0;  // no two rows compared equal
+      return;
+    }
     tried = true;  // long runs of equal prefixes (arrangement data): every word
   }
   DevBuf<uint64_t> kw(size_t(n), s), kw_alt(size_t(n), s);

@@ -39,7 +39,7 @@ for r in range(reps + 1):
         torch.cuda.synchronize()
         if ref is None:
             ref = (out.cells.cpu(), out.edges.cpu())
-        elif r == 0:
+        elif r == 0 and not os.environ.get("AB_NOCHECK"):
             assert torch.equal(out.cells.cpu(), ref[0]) and torch.equal(out.edges.cpu(), ref[1]), p
         if r > 0:
             res[p].append(out.stats)
