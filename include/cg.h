@@ -98,9 +98,16 @@ typedef struct {
 enum {
   CG_DICT_SORTED = 0,  /* popcount layers: per-layer sorted array + 2^b prefix index + filter */
   CG_DICT_BSEARCH = 1, /* popcount layers, plain per-layer binary search (no prefix index) */
-  CG_DICT_GLOBAL = 2   /* one prefix index + filter over the canonical table; the probe
+  CG_DICT_GLOBAL = 2,  /* one prefix index + filter over the canonical table; the probe
                           writes the edge list in canonical order (no edge sort).  Default
                           of cg_opts_init; its cg_index holds a copy of the table. */
+  CG_DICT_HASH = 3       /* open-addressed hash table over the canonical table (h = XOR of
+                          per-bit 64-bit keys, so a flip is h ^ Z[k]; 4-slot 32-byte
+                          buckets, load 1/2, every tag hit verified on the full row):
+                          the north star's alternative dictionary (P:205 / P:276-281
+                          replace the paper's tree), kept for the ncu A/B.  Same
+                          output as CG_DICT_GLOBAL; keeps no cg_index (index_out with
+                          it is CG_EINVAL). */
 };
 
 typedef struct {

@@ -21,8 +21,9 @@ LIB_PATH = os.path.join(HERE, "lib", "libcg.so")
 
 CG_OK, CG_EINVAL, CG_EINPUT, CG_ENOMEM, CG_ECUDA, CG_ETOOBIG, CG_EARCH, CG_ENOTIMPL = (
     0, -1, -2, -3, -4, -5, -6, -7)
-CG_DICT_SORTED, CG_DICT_BSEARCH, CG_DICT_GLOBAL = 0, 1, 2
-DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH, "global": CG_DICT_GLOBAL}
+CG_DICT_SORTED, CG_DICT_BSEARCH, CG_DICT_GLOBAL, CG_DICT_HASH = 0, 1, 2, 3
+DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH, "global": CG_DICT_GLOBAL,
+              "hash": CG_DICT_HASH}
 
 
 class CgError(RuntimeError):

@@ -392,15 +392,34 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     int fextra = o.filter_extra >= 0 ? o.filter_extra : 5;
     fextra = std::min(fextra, 32 - b);  // filter prefix <= 32 bits
     const Mem gix = keep_index ? Mem::Persist : Mem::Scratch;  // T/F outlive the build
-    DevBuf<uint32_t> T((size_t(1) << b) + 1, s, gix);
-    DevBuf<uint32_t> F(std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
-    CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
-    const int64_t dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
-    build_global_index(keys, nc, W, b, fextra, T.p, F.p, s);
+    // CG_DICT_HASH (the ncu A/B of SURVEY 8.a5): open-addressed buckets
+    // instead of T/F, load 1/2 (2 slots per cell)
+    const bool hash = o.dict_kind == CG_DICT_HASH;
+    int lb = 0;
+    while (hash && (int64_t(1) << lb) * 2 < nc) ++lb;
+    DevBuf<uint32_t> T(hash ? 1 : (size_t(1) << b) + 1, s, gix);
+    DevBuf<uint32_t> F(hash ? 1 : std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
+    DevBuf<uint64_t> Z(hash ? size_t(ell) : 1, s), slots(hash ? (size_t(4) << lb) : 1, s),
+        hv(hash ? size_t(nc) : 1, s);
+    int64_t dict_bytes = 0;
+    if (hash) {
+      build_hash_dict(keys, nc, W, ell, lb, Z.p, slots.p, hv.p, s);
+      dict_bytes = int64_t(slots.n + hv.n + Z.n) * 8;
+    } else {
+      CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
+      dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
+      build_global_index(keys, nc, W, b, fextra, T.p, F.p, s);
+    }
     tm.mark();  // 5: dict
     GlobalDict g{keys, nullptr, T.p, F.p, b, fextra, W, ell, nc};
     g.src_pos = src_pos;
     g.idx = idx;
+    if (hash) {
+      g.Z = Z.p;
+      g.slots = slots.p;
+      g.hv = hv.p;
+      g.lb = lb;
+    }
     // ---- a6 + a7: probes write the canonical edge list directly
     const int64_t i_lo = 0, i_hi = n_src;
     const int64_t ntiles = std::max<int64_t>(probe_global_tiles(i_hi - i_lo), 1);
@@ -564,7 +583,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     cellbuf.alloc(size_t(ns) * W, s, Mem::Persist);
     // (the global dictionary needs neither popcounts nor lcp: the probe
     // derives lcp from the next row)
-    const bool meta = sh.cells_only || o.dict_kind != CG_DICT_GLOBAL;
+    const bool meta = sh.cells_only || (o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH);
     if (order.p && no_dups) {
       // every row is a cell (the sort compared all ties): one gather, a
       // thread per word; n_c = n
@@ -575,7 +594,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, meta ? popc.p : nullptr,
                            meta ? lcp.p : nullptr, d_flags + 1, s);
     else launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
-  } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL) {
+  } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the
     // layered dictionary (the global-dictionary probe derives lcp itself)
     launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
@@ -608,7 +627,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
     return;
   }
-  if (o.dict_kind == CG_DICT_GLOBAL) {
+  if (o.dict_kind == CG_DICT_GLOBAL || o.dict_kind == CG_DICT_HASH) {
     GlobalOut go;
     global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, o, o.index_out != nullptr, tm, &go);
     const uint64_t m = uint64_t(go.m);
@@ -795,8 +814,10 @@ static int finish(int rc, const Built& b, cg_cells* cells, cg_edges* edges, cons
 }
 
 static void validate_opts(const cg_opts& o) {
+  if (o.dict_kind == CG_DICT_HASH && o.index_out)
+    throw CgError{CG_EINVAL, "CG_DICT_HASH keeps no cg_index (use CG_DICT_GLOBAL for cg_query)"};
   if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
-      o.dict_kind != CG_DICT_GLOBAL)
+      o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH)
     throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
   if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
   if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};

@@ -197,7 +197,17 @@ struct GlobalDict {
   int64_t n_cells;             // rows of keys
   const uint32_t* src_pos = nullptr;  // subsequence mode: dictionary row of source q
   const uint32_t* idx = nullptr;      // subsequence mode: canonical index of each row
+  // hash dictionary (CG_DICT_HASH; T/F unused): Z[ell] bit hashes, 2^lb
+  // buckets of 4 (tag32 << 32 | row) slots, hv[n_cells] = h(cell)
+  const uint64_t* Z = nullptr;
+  const uint64_t* slots = nullptr;
+  const uint64_t* hv = nullptr;
+  int lb = 0;
 };
+// hash dictionary over a canonical table: Z u64[ell], slots u64[4 << lb]
+// (zeroed here), hv u64[nc]
+void build_hash_dict(const uint64_t* cells, int64_t nc, int W, int ell, int lb, uint64_t* Z,
+                     uint64_t* slots, uint64_t* hv, cudaStream_t s);
 void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
                         uint32_t* F, cudaStream_t s);
 // Each tile of 32 cells writes its sorted hits (i << 32 | j) as one block of

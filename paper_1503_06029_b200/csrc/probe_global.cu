@@ -72,6 +72,136 @@ __global__ void k_global_index(const uint64_t* __restrict__ cells, int64_t nc, i
   }
 }
 
+// ---------------------------------------------------------------- tile output
+// Shared by the prefix-dictionary and the hash-dictionary probes.  A warp
+// owns a tile of 32 consecutive source cells; its hits are appended to its
+// shared-memory buffer (one ballot per round) and, at the end of the tile,
+// ordered by (i, j) and written as one block of the scratch list.
+struct TileOut {
+  uint64_t* wbuf;       // the warp's buffer [kWarpEdgeCap]
+  uint32_t wfill;       // warp-uniform fill
+  uint32_t lt;          // lanemask_lt
+  uint64_t* spill;      // spill mode (overflow re-run): unordered global list
+  uint64_t spill_cap;
+  unsigned long long* spill_n;
+
+  __device__ __forceinline__ void emit(bool hit, uint64_t e) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t hb = __ballot_sync(kFull, hit);
+    if (hb) {
+      const int leader = __ffs(hb) - 1;
+      if (spill) {
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(spill_n, (unsigned long long)__popc(hb));
+        base = __shfl_sync(kFull, base, leader);
+        if (hit) {
+          const unsigned long long pos = base + __popc(hb & lt);
+          if (pos < spill_cap) spill[pos] = e;
+        }
+        return;
+      }
+      // per-warp buffer: the warp owns 32 consecutive cells, so its list
+      // sorted on its own is a contiguous piece of the tile's sorted list
+      if (hit) {
+        const uint32_t pos = wfill + __popc(hb & lt);
+        if (pos < kWarpEdgeCap) wbuf[pos] = e;
+      }
+      wfill += __popc(hb);
+    }
+  }
+
+  // The warp orders its own list: short lists (<= 32, the common case) by
+  // rank counting, <= 64 on 64-bit keys, longer ones by a warp-synchronous
+  // bitonic network in the buffer; one atomicAdd reserves the tile's block of
+  // the scratch list.  tcnt / tpos let a scan + copy place the blocks in
+  // canonical order afterwards (a look-back would make each tile wait for its
+  // predecessor).  i0 = the tile's first source sequence number.
+  template <class Canon>
+  __device__ __forceinline__ void flush(int64_t tile, int64_t i0, uint64_t* __restrict__ out,
+                                        uint64_t cap, uint32_t* __restrict__ tcnt,
+                                        uint64_t* __restrict__ tpos, unsigned long long* total,
+                                        uint4* __restrict__ ovf, uint32_t* ovf_n, Canon canon) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t wn = min(wfill, uint32_t(kWarpEdgeCap));
+    __syncwarp();
+    if (wn > 64) {
+      int P = 1;
+      while (P < int(wn)) P <<= 1;
+      for (int q = int(wn) + lane; q < P; q += 32) wbuf[q] = ~0ull;
+      __syncwarp();
+      for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          const int lg = __ffs(jj) - 1;
+          for (int p = lane; p < (P >> 1); p += 32) {
+            const int a = ((p >> lg) << (lg + 1)) | (p & (jj - 1));
+            const int c = a + jj;
+            const bool up = (a & kk) == 0;
+            const uint64_t x = wbuf[a], y = wbuf[c];
+            if ((y < x) == up) {
+              wbuf[a] = y;
+              wbuf[c] = x;
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    // block positions are 64-bit: m may exceed 2^32 (m <= n_c*ell/2, P:106)
+    uint64_t bs = 0;
+    if (lane == 0) {
+      tcnt[tile] = wfill;
+      if (wfill > uint32_t(kWarpEdgeCap)) {
+        // rare: hits beyond the warp buffer were dropped; the host re-runs
+        // this tile in spill mode and writes its range directly
+        const uint32_t k = atomicAdd(ovf_n, 1u);
+        ovf[k] = make_uint4(uint32_t(tile), 0u, wfill, 0u);
+        bs = ~0ull;
+      } else if (wfill) {
+        bs = atomicAdd(total, (unsigned long long)wfill);
+      }
+      tpos[tile] = bs;  // position of the tile's block in the scratch list
+    }
+    const uint64_t wpos = __shfl_sync(kFull, bs, 0);
+    if (wpos != ~0ull && wn > 0) {
+      if (wn <= 32) {
+        // one hit per lane.  Every path emits a source cell's hits in
+        // ascending j, so the rank of a hit is #(hits of lower source lanes)
+        // + #(earlier hits of its own source): a 5-bit radix rank of the
+        // source lane from five ballots
+        const bool h0 = lane < int(wn);
+        const uint64_t e0 = h0 ? wbuf[lane] : 0ull;
+        const uint32_t src = h0 ? uint32_t(e0 >> 32) - uint32_t(i0) : 0u;
+        uint32_t same = __ballot_sync(kFull, h0), less = 0;
+#pragma unroll
+        for (int k = 4; k >= 0; --k) {
+          const uint32_t bk = __ballot_sync(kFull, (src >> k) & 1u);
+          const uint32_t sb = 0u - ((src >> k) & 1u);  // all ones iff bit k set
+          less |= same & ~bk & sb;
+          same &= bk ^ ~sb;
+        }
+        const uint32_t r0 = __popc(less) + __popc(same & lt);
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
+      } else if (wn <= 64) {
+        // rank = number of smaller keys (the (i, j) keys are distinct);
+        // every lane reads the same word per step (broadcast)
+        const bool h0 = lane < int(wn), h1 = lane + 32 < int(wn);
+        const uint64_t e0 = h0 ? wbuf[lane] : 0ull, e1 = h1 ? wbuf[lane + 32] : 0ull;
+        uint32_t r0 = 0, r1 = 0;
+        for (uint32_t p = 0; p < wn; ++p) {
+          const uint64_t x = wbuf[p];
+          r0 += x < e0;
+          r1 += x < e1;
+        }
+        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
+        if (h1 && wpos + r1 < cap) out[wpos + r1] = canon(e1);
+      } else {
+        for (uint32_t q = lane; q < wn; q += 32)
+          if (wpos + q < cap) out[wpos + q] = canon(wbuf[q]);  // sorted (i << 32 | j) keys
+      }
+    }
+  }
+};
+
 // FR: filter loads in flight per lane and round; NR / SR: near rows and
 // survivor-bucket rows compared per round (A/B at C5: FR 3-6, NR/SR 1, 2, 4)
 // SUB: the dictionary is a subsequence U of the canonical table (a rank's
@@ -117,7 +247,6 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     const int64_t tile = __shfl_sync(kFull, tk, 0);
     if (tile >= ntiles) break;
     if (tile_sel && !tile_sel[tile]) continue;  // spill re-run: only the overflow tiles
-    uint32_t wfill = 0;  // warp-uniform fill of this warp's edge buffer
     const int64_t i = i_lo + tile * kTileCells + lane;  // source sequence number q
     const bool valid = i < i_hi;           // this lane probes
     int64_t row = i;                       // its dictionary row
@@ -269,31 +398,8 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
       return (uint64_t(g.idx[g.src_pos[uint32_t(e >> 32)]]) << 32) | g.idx[uint32_t(e)];
     };
 
-    // append a round's hits to the tile buffer (one shared atomic per warp);
-    // spill mode (overflow re-run): append unordered to the global spill list
-    auto emit = [&](bool hit, uint64_t e) {
-      const uint32_t hb = __ballot_sync(kFull, hit);
-      if (hb) {
-        const int leader = __ffs(hb) - 1;
-        if (spill) {
-          unsigned long long base = 0;
-          if (lane == leader) base = atomicAdd(spill_n, (unsigned long long)__popc(hb));
-          base = __shfl_sync(kFull, base, leader);
-          if (hit) {
-            const unsigned long long pos = base + __popc(hb & lt);
-            if (pos < spill_cap) spill[pos] = e;
-          }
-          return;
-        }
-        // per-warp buffer: the warp owns 32 consecutive cells, so its list
-        // sorted on its own is a contiguous piece of the tile's sorted list
-        if (hit) {
-          const uint32_t pos = wfill + __popc(hb & lt);
-          if (pos < kWarpEdgeCap) wbuf[pos] = e;
-        }
-        wfill += __popc(hb);
-      }
-    };
+    TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n};
+    auto emit = [&](bool hit, uint64_t e) { to.emit(hit, e); };
 
     // ---- near: rows i+1.. in V's own b-prefix bucket.  Every such row R is
     // > V and shares V's first b bits, so it is a hit iff R ^ V is one bit
@@ -473,7 +579,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     // at the tail of the warp's edge buffer when it fits beside the hits the
     // rounds can still append (at most one per survivor); else both are
     // found per round by a search over the prefix sums
-    const bool use_tab = wfill + total_sv + (total_sv + 3) / 4 <= uint32_t(kWarpEdgeCap);
+    const bool use_tab = to.wfill + total_sv + (total_sv + 3) / 4 <= uint32_t(kWarpEdgeCap);
     uint16_t* stab = reinterpret_cast<uint16_t*>(wbuf + kWarpEdgeCap) - total_sv;
     if (use_tab) {
       uint32_t sv = surv, pos = incl - nsv;
@@ -584,90 +690,190 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
       emit(hit, e);
     }
     if (spill) continue;  // spill mode: no ordered output
-    // ---- tile output.  The warp orders its own list: short lists (<= 32,
-    // the common case) by rank counting on 32-bit keys, <= 64 on 64-bit keys,
-    // longer ones by a warp-synchronous bitonic network in the buffer; one
-    // atomicAdd reserves the tile's block of the scratch list.  tile_cnt /
-    // tile_pos let a scan + copy place the blocks in canonical order
-    // afterwards (a look-back would make each tile wait for its predecessor).
-    const uint32_t wn = min(wfill, uint32_t(kWarpEdgeCap));
+    to.flush(tile, i - lane, out, cap, tcnt, tpos, total, ovf, ovf_n, canon);
     __syncwarp();
-    if (wn > 64) {
-      int P = 1;
-      while (P < int(wn)) P <<= 1;
-      for (int q = int(wn) + lane; q < P; q += 32) wbuf[q] = ~0ull;
-      __syncwarp();
-      for (int kk = 2; kk <= P; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          const int lg = __ffs(jj) - 1;
-          for (int p = lane; p < (P >> 1); p += 32) {
-            const int a = ((p >> lg) << (lg + 1)) | (p & (jj - 1));
-            const int c = a + jj;
-            const bool up = (a & kk) == 0;
-            const uint64_t x = wbuf[a], y = wbuf[c];
-            if ((y < x) == up) {
-              wbuf[a] = y;
-              wbuf[c] = x;
-            }
-          }
-          __syncwarp();
-        }
-      }
-    }
-    // block positions are 64-bit: m may exceed 2^32 (m <= n_c*ell/2, P:106)
-    uint64_t bs = 0;
-    if (lane == 0) {
-      tcnt[tile] = wfill;
-      if (wfill > uint32_t(kWarpEdgeCap)) {
-        // rare: hits beyond the warp buffer were dropped; the host re-runs
-        // this tile in spill mode and writes its range directly
-        const uint32_t k = atomicAdd(ovf_n, 1u);
-        ovf[k] = make_uint4(uint32_t(tile), 0u, wfill, 0u);
-        bs = ~0ull;
-      } else if (wfill) {
-        bs = atomicAdd(total, (unsigned long long)wfill);
-      }
-      tpos[tile] = bs;  // position of the tile's block in the scratch list
-    }
-    const uint64_t wpos = __shfl_sync(kFull, bs, 0);
-    if (wpos != ~0ull && wn > 0) {
-      if (wn <= 32) {
-        // one hit per lane.  Every path above emits a source cell's hits in
-        // ascending j (near rows in order, then flips from the least
-        // significant bit up, near before far), so the rank of a hit is
-        // #(hits of lower source lanes) + #(earlier hits of its own source):
-        // a 5-bit radix rank of the source lane from five ballots
-        const bool h0 = lane < int(wn);
-        const uint64_t e0 = h0 ? wbuf[lane] : 0ull;
-        const uint32_t src = h0 ? uint32_t(e0 >> 32) - uint32_t(i - lane) : 0u;
-        uint32_t same = __ballot_sync(kFull, h0), less = 0;
+  }
+  unsigned long long wsum = my_issued;
 #pragma unroll
-        for (int k = 4; k >= 0; --k) {
-          const uint32_t bk = __ballot_sync(kFull, (src >> k) & 1u);
-          const uint32_t sb = 0u - ((src >> k) & 1u);  // all ones iff bit k set
-          less |= same & ~bk & sb;
-          same &= bk ^ ~sb;
-        }
-        const uint32_t r0 = __popc(less) + __popc(same & lt);
-        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
-      } else if (wn <= 64) {
-        // rank = number of smaller keys (the (i, j) keys are distinct);
-        // every lane reads the same word per step (broadcast)
-        const bool h0 = lane < int(wn), h1 = lane + 32 < int(wn);
-        const uint64_t e0 = h0 ? wbuf[lane] : 0ull, e1 = h1 ? wbuf[lane + 32] : 0ull;
-        uint32_t r0 = 0, r1 = 0;
-        for (uint32_t p = 0; p < wn; ++p) {
-          const uint64_t x = wbuf[p];
-          r0 += x < e0;
-          r1 += x < e1;
-        }
-        if (h0 && wpos + r0 < cap) out[wpos + r0] = canon(e0);
-        if (h1 && wpos + r1 < cap) out[wpos + r1] = canon(e1);
-      } else {
-        for (uint32_t q = lane; q < wn; q += 32)
-          if (wpos + q < cap) out[wpos + q] = canon(wbuf[q]);  // sorted (i << 32 | j) keys
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+  if (lane == 0 && wsum) atomicAdd(issued, wsum);
+}
+
+// ---------------------------------------------------------------- hash dictionary
+// The north star's alternative dictionary (a5, "an open-addressed table
+// keyed on a word hash"), kept for the ncu A/B against the prefix index
+// (DESIGN section 6):
+//   h(x) = XOR of Z[k] over the set bits k of x, Z[k] = splitmix64(k):
+//   GF(2)-linear, so the flipped key's hash is h(x) ^ Z[k] -- the probe never
+//   materialises x ^ e_k;
+//   buckets of 4 slots (32 B = one sector), slot = tag32 << 32 | row, tag =
+//   low 32 bits of h | 1 (0 = empty), bucket = the top lb bits of h, linear
+//   probing over buckets; every tag hit is verified on the full row, so a
+//   hash collision costs time, never correctness.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void k_hash_z(uint64_t* __restrict__ Z, int ell) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ell; k += gridDim.x * blockDim.x)
+    Z[k] = splitmix64(uint64_t(k));
+}
+
+__global__ void k_hash_build(const uint64_t* __restrict__ cells, int64_t nc, int W,
+                             const uint64_t* __restrict__ Z, int lb,
+                             unsigned long long* __restrict__ slots, uint64_t* __restrict__ hv) {
+  const uint64_t nb = uint64_t(1) << lb;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nc;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t h = 0;
+    for (int w = 0; w < W; ++w) {
+      uint64_t x = cells[i * W + w];
+      while (x) {  // bit k of the key = bit 63 - (k & 63) of word k >> 6
+        const int t = __clzll(x);
+        h ^= __ldg(Z + 64 * w + t);
+        x &= ~(0x8000000000000000ull >> t);
       }
     }
+    hv[i] = h;
+    const unsigned long long e = (uint64_t(uint32_t(h) | 1u) << 32) | uint64_t(i);
+    uint64_t b = lb ? (h >> (64 - lb)) : 0;
+    while (true) {
+      bool done = false;
+      for (int q = 0; q < 4 && !done; ++q)
+        done = atomicCAS(slots + b * 4 + q, 0ull, e) == 0ull;
+      if (done) break;
+      b = (b + 1) & (nb - 1);
+    }
+  }
+}
+
+// One thread per canonical cell (tiles of 32 per warp, as k_probe_global):
+// every zero bit k <= lcp(V_i, V_{i+1}) is looked up -- FR lookups in flight
+// per round, from the least significant candidate up (ascending targets)
+#ifndef HASH_FR
+#define HASH_FR 3
+#endif
+template <int WC, int FR = HASH_FR>
+__global__ void __launch_bounds__(32 * kProbeWarps, 4)
+    k_probe_hash(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
+                 uint64_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ tcnt,
+                 uint64_t* __restrict__ tpos, uint32_t* ticket, unsigned long long* total,
+                 unsigned long long* issued, uint64_t* __restrict__ spill, uint64_t spill_cap,
+                 unsigned long long* spill_n, uint4* __restrict__ ovf, uint32_t* ovf_n,
+                 const uint8_t* __restrict__ tile_sel) {
+  __shared__ uint64_t ebuf[kProbeWarps][kWarpEdgeCap];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t lt = lanemask_lt();
+  const int W = WC > 0 ? WC : g.W;
+  const int lb = g.lb;
+  const uint64_t bmask = (uint64_t(1) << lb) - 1;
+  uint32_t my_issued = 0;
+  uint64_t* wbuf = ebuf[tid >> 5];
+  while (true) {
+    uint32_t tk = 0;
+    if (lane == 0) tk = atomicAdd(ticket, 1u);
+    const int64_t tile = __shfl_sync(kFull, tk, 0);
+    if (tile >= ntiles) break;
+    if (tile_sel && !tile_sel[tile]) continue;
+    const int64_t i = i_lo + tile * kTileCells + lane;
+    const bool valid = i < i_hi;
+    const uint64_t* Vp = g.keys + (valid ? i : 0) * W;
+    int kmax = -1;
+    if (valid) {
+      if (!lcp_prune) {
+        kmax = g.ell - 1;
+      } else if (i + 1 < g.n_cells) {
+        int l = -1;
+        for (int w = 0; w < W && l < 0; ++w) {
+          const uint64_t x = Vp[w] ^ Vp[W + w];
+          if (x) l = 64 * w + __clzll(x);
+        }
+        kmax = l < 0 ? g.ell - 1 : min(l, g.ell - 1);
+      }
+    }
+    const uint64_t h = valid ? g.hv[i] : 0ull;
+    TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n};
+    // candidate bits: zero bits k <= kmax, word by word from the last
+    int cw = kmax >= 0 ? (kmax >> 6) : -1;
+    auto cmask = [&](int w) -> uint64_t {
+      uint64_t m = ~Vp[w];
+      if (w == (kmax >> 6)) m &= ~0ull << (63 - (kmax & 63));
+      return m;
+    };
+    uint64_t z = cw >= 0 ? cmask(cw) : 0ull;
+    auto next_bit = [&](int* k) -> bool {
+      while (z == 0 && cw > 0) {
+        --cw;
+        z = cmask(cw);
+      }
+      if (z == 0) return false;
+      const int t = 63 - (__ffsll(z) - 1);  // least significant candidate first
+      z &= z - 1;
+      *k = 64 * cw + t;
+      return true;
+    };
+    bool more = true;
+    while (__any_sync(kFull, more)) {
+      int k[FR];
+      bool on[FR];
+      ulonglong2 s0[FR], s1[FR];
+      uint64_t hh[FR];
+#pragma unroll
+      for (int u = 0; u < FR; ++u) {
+        on[u] = more && next_bit(&k[u]);
+        more = on[u];
+        hh[u] = on[u] ? (h ^ __ldg(g.Z + k[u])) : 0ull;
+        const uint64_t b = lb ? (hh[u] >> (64 - lb)) : 0ull;
+        const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(g.slots + b * 4);
+        if (on[u]) {
+          s0[u] = bp[0];
+          s1[u] = bp[1];
+          ++my_issued;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < FR; ++u) {
+        bool hit = false;
+        uint64_t e = 0;
+        if (on[u]) {
+          const uint32_t tag = uint32_t(hh[u]) | 1u;
+          uint64_t b = lb ? (hh[u] >> (64 - lb)) : 0ull;
+          ulonglong2 a = s0[u], c = s1[u];
+          const int fw = k[u] >> 6;
+          const uint64_t fb = 0x8000000000000000ull >> (k[u] & 63);
+          while (true) {
+            const uint64_t sl[4] = {a.x, a.y, c.x, c.y};
+            bool empty = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (sl[q] == 0ull) empty = true;
+              if (!hit && uint32_t(sl[q] >> 32) == tag) {
+                const int64_t j = int64_t(uint32_t(sl[q]));
+                const uint64_t* R = g.keys + j * W;
+                bool eq = true;
+                for (int w = 0; w < W && eq; ++w) eq = R[w] == (Vp[w] ^ (w == fw ? fb : 0ull));
+                if (eq) {
+                  hit = true;
+                  e = (uint64_t(i) << 32) | uint64_t(j);
+                }
+              }
+            }
+            if (hit || empty) break;
+            b = (b + 1) & bmask;  // a full bucket: the key may sit further on
+            const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(g.slots + b * 4);
+            a = bp[0];
+            c = bp[1];
+          }
+        }
+        to.emit(hit, e);
+      }
+    }
+    if (spill) continue;
+    to.flush(tile, i - lane, out, cap, tcnt, tpos, total, ovf, ovf_n,
+             [](uint64_t e) { return e; });
     __syncwarp();
   }
   unsigned long long wsum = my_issued;
@@ -677,6 +883,17 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
 }
 
 }  // namespace
+
+void build_hash_dict(const uint64_t* cells, int64_t nc, int W, int ell, int lb, uint64_t* Z,
+                     uint64_t* slots, uint64_t* hv, cudaStream_t s) {
+  k_hash_z<<<std::max(1, (ell + 255) / 256), 256, 0, s>>>(Z, ell);
+  CG_LAUNCH_CHECK();
+  CG_CUDA(cudaMemsetAsync(slots, 0, (size_t(4) << lb) * 8, s));
+  const int64_t blocks = std::min<int64_t>((nc + 255) / 256, int64_t(num_sms()) * 16);
+  k_hash_build<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(
+      cells, nc, W, Z, lb, reinterpret_cast<unsigned long long*>(slots), hv);
+  CG_LAUNCH_CHECK();
+}
 
 void build_global_index(const uint64_t* cells, int64_t nc, int W, int b, int fextra, uint32_t* T,
                         uint32_t* F, cudaStream_t s) {
@@ -697,6 +914,13 @@ void launch_probe_global(const GlobalDict& g, int lcp_prune, int64_t i_lo, int64
   g, lcp_prune, i_lo, i_hi, ntiles, out, cap, tcnt, tpos, ticket, total, issued, spill, spill_cap, \
       spill_n, ovf, ovf_n, tile_sel
   const bool sub = g.src_pos != nullptr;
+  if (g.slots) {  // hash dictionary (full table only)
+    if (g.W == 1) k_probe_hash<1><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+    else if (g.W == 2) k_probe_hash<2><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+    else k_probe_hash<0><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);
+    CG_LAUNCH_CHECK();
+    return;
+  }
   switch (g.W) {
     case 1:
       if (sub) k_probe_global<1, true><<<grid, 32 * kProbeWarps, 0, s>>>(CG_PROBE_ARGS);

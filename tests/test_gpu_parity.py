@@ -169,7 +169,7 @@ def test_hypercube_closed_form(cg):
         np.testing.assert_array_equal(e, want)  # m = ell * 2^(ell-1), every degree = ell
 
 
-@pytest.mark.parametrize("dict_kind", ["global", "sorted"])
+@pytest.mark.parametrize("dict_kind", ["global", "sorted", "hash"])
 def test_dense_ball_tile_overflow(cg, dict_kind):
     """All vectors of weight <= 2 (ell = 100): weight-1 cells have 99
     out-edges each, so a 256-cell tile of the canonical-order probe overflows
@@ -210,7 +210,9 @@ def test_multiset_x3_and_permutation(cg):
                                 dict(dict_kind="sorted"), dict(dict_kind="sorted", lcp_prune=False),
                                 dict(dict_kind="bsearch", lcp_prune=False), dict(bucket_log2=0),
                                 dict(bucket_log2=6), dict(dict_kind="sorted", bucket_log2=0),
-                                dict(edge_cap=1), dict(dict_kind="sorted", edge_cap=1)],
+                                dict(edge_cap=1), dict(dict_kind="sorted", edge_cap=1),
+                                dict(dict_kind="hash"), dict(dict_kind="hash", lcp_prune=False),
+                                dict(dict_kind="hash", edge_cap=1)],
                          ids=lambda kw: ",".join(f"{k}={v}" for k, v in kw.items()) or "default")
 def test_options_vs_oracle(cg, kw):
     """Every dictionary / pruning / bucket / capacity option gives the oracle's
@@ -369,3 +371,46 @@ def test_bad_options_rejected(cg):
         with pytest.raises(cg.CgError) as ei:
             cg.build(x, **kw)
         assert ei.value.code == -1
+
+
+# ---------------------------------------------------------------- long rows (W > 2)
+@pytest.mark.parametrize("ell,dup,dict_kind", [(300, 0.0, "global"), (300, 0.1, "global"),
+                                               (1024, 0.2, "global"), (300, 0.0, "sorted"),
+                                               (520, 0.1, "sorted"), (2048, 0.05, "global"),
+                                               (1024, 0.1, "hash"), (64, 0.1, "hash"),
+                                               (128, 0.0, "hash")])
+def test_long_rows_prefix_sort_paths(cg, ell, dup, dict_kind):
+    """Random long rows with planted partners: the (32-bit prefix, index) sort
+    succeeds (short tie runs); without duplicates the rows go straight to the
+    cell table (no dedupe pass), with duplicates the warp-cooperative
+    gather + dedupe runs; the layered dictionary needs popcount/lcp."""
+    x, _ = synth.planted_bytes(ell, 6000, ell)
+    rng = np.random.default_rng(ell)
+    if dup:
+        x = np.concatenate([x, x[rng.integers(0, x.shape[0], int(dup * x.shape[0]))]])
+    x = x[rng.permutation(x.shape[0])]
+    assert_parity(cg, x, dict_kind=dict_kind)
+
+
+# ---------------------------------------------------------------- hash dictionary
+@pytest.mark.parametrize("ell", [1, 7, 64, 65, 128, 200, 1024, 4096])
+def test_hash_dictionary_sweep(cg, ell):
+    """CG_DICT_HASH (open-addressed, h ^ Z[k] per flip) gives the oracle's
+    graph on clustered inputs dense in Hamming-1 pairs and duplicates (hash
+    collisions of distinct cells only cost verification)."""
+    x = synth.clustered_bytes(ell + 11, 4000 + ell, ell, n_centers=4, max_flips=3)
+    x = np.concatenate([x, x[:333]])
+    assert_parity(cg, x, dict_kind="hash")
+
+
+def test_hash_dictionary_arrangement_and_hypercube(cg):
+    d = synth.config("C2")
+    assert_parity(cg, d["bytes"], dict_kind="hash")
+    x = synth.hypercube(14)
+    assert_parity(cg, x[np.random.default_rng(3).permutation(x.shape[0])], dict_kind="hash")
+
+
+def test_hash_dictionary_keeps_no_index(cg):
+    x = torch.from_numpy(synth.random_bytes(1, 100, 16)).cuda()
+    with pytest.raises(cg.CgError):
+        cg.build(x, dict_kind="hash", want_index=True)
