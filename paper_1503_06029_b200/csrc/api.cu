@@ -821,6 +821,7 @@ static void validate_opts(const cg_opts& o) {
     throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
   if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
   if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};
+  if (o.sort_kind < 0 || o.sort_kind > 2) throw CgError{CG_EINVAL, "sort_kind must be 0, 1 or 2"};
   if (o.reserved0 != 0) throw CgError{CG_EINVAL, "reserved0 must be 0"};
 }
 
@@ -873,6 +874,34 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     StageTimer tm;
     tm.start(o.stats != nullptr, s);  // 0
     setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+    if (vecs && o.sort_kind == 0 && small_build_ok(n, ell) && !o.index_out && o.edge_cap == 0 &&
+        (o.dict_kind == CG_DICT_GLOBAL || o.dict_kind == CG_DICT_HASH)) {
+      // small input: the whole path in one CTA, one host read-back (small.cu)
+      uint64_t* cw = static_cast<uint64_t*>(dev_alloc(size_t(n) * W * 8, s));
+      b.cells = cw;
+      // m <= n_c * ell / 2: the buffer can never overflow
+      const uint64_t ecap = std::max<uint64_t>(1, uint64_t(n) * uint64_t(ell) / 2);
+      uint64_t* ew = static_cast<uint64_t*>(dev_alloc(ecap * 8, s));
+      b.edges = reinterpret_cast<uint32_t*>(ew);
+      DevBuf<int64_t> res(8, s);
+      launch_small_build(vecs, n, ell, o.lcp_prune, cw, ew, res.p, s);
+      tm.mark();  // the whole build is one kernel: reported as the pack stage
+      int64_t* hr = static_cast<int64_t*>(host_stage(8 * sizeof(int64_t)));
+      CG_CUDA(cudaMemcpyAsync(hr, res.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaStreamSynchronize(s));
+      if (hr[2]) throw CgError{CG_EINPUT, "input byte not in {0,1}"};
+      b.n_cells = hr[0];
+      b.n_edges = hr[1];
+      for (int q = 0; q < 6; ++q) tm.mark();
+      fill_stats(tm, n, o.stats);
+      if (o.stats) {
+        o.stats->n_cells = b.n_cells;
+        o.stats->n_edges = b.n_edges;
+        o.stats->logical_probes = b.n_cells * int64_t(ell);
+        o.stats->dict_cells = b.n_cells;
+      }
+      store_counters(o.stats);
+    } else {
     DevBuf<uint32_t> flags(4, s);
     CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
     // the MSD sort's top-digit histogram, counted by the pack kernel; on the
@@ -903,6 +932,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
                     (vecs && msd) ? tile_hist.p : nullptr);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
+    }
   } catch (...) {
     const int rc_ = current_error();
     if (b.cells) dev_free(b.cells, nullptr);

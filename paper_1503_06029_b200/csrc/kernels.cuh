@@ -17,6 +17,14 @@ void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32
 // packed input: copy + check pad bits (err |= 1 if a pad bit is set)
 void launch_check_pad(const uint64_t* words, int64_t n, int ell, uint32_t* err, cudaStream_t s);
 
+// ---------------------------------------------------------------- small inputs (small.cu)
+// n <= 2048 rows, ell <= 256: pack, sort, dedupe, probe and the canonical
+// edge list in one CTA.  cells u64[n][W], edges u64[n * ell / 2] as (i, j)
+// u32 pairs (capacity: the P:106 bound), res[3] = n_c, m, input error.
+bool small_build_ok(int64_t n, int ell);
+void launch_small_build(const uint8_t* vecs, int64_t n, int ell, int lcp_prune, uint64_t* cells,
+                        uint64_t* edges, int64_t* res, cudaStream_t s);
+
 // ---------------------------------------------------------------- f1 signatures
 // points f64[n][dim], planes f64[ell][dim+1] (a_0..a_{dim-1}, b) -> packed
 // keys u64[n][W]: bit k = [fma chain b + sum a_t p_t >= 0] (sign.cu);

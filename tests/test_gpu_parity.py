@@ -144,9 +144,41 @@ def test_ell_sweep_clustered_with_duplicates(cg, ell):
 
 
 @pytest.mark.parametrize("n", [1, 2, 31, 33, 3071, 3073, 4095, 4097, 12289])
-def test_ragged_sizes(cg, n):
+@pytest.mark.parametrize("sort_kind", ["auto", "nosmall"])
+def test_ragged_sizes(cg, n, sort_kind):
     x = synth.clustered_bytes(n, n, 40, n_centers=3, max_flips=4)
-    assert_parity(cg, x)
+    assert_parity(cg, x, sort_kind=sort_kind)
+
+
+# ---------------------------------------------------------------- one-CTA small path
+@pytest.mark.parametrize("n,ell", [(1, 1), (2, 3), (1000, 32), (2047, 64), (2048, 64),
+                                   (2048, 256), (2049, 256), (1500, 255), (1500, 257),
+                                   (700, 129), (1024, 192)])
+@pytest.mark.parametrize("kind", ["planted", "clustered"])
+def test_small_path_edges(cg, n, ell, kind):
+    """n <= 2048, ell <= 256 run in one CTA (bitonic sort, block-scan dedupe,
+    binary-search probes); just past either limit the general path runs.
+    Both against the oracle, with duplicates and dense Hamming-1 clusters."""
+    if kind == "planted":
+        x, _ = synth.planted_bytes(n + ell, max(1, n // 2), ell)
+        x = x[:n] if x.shape[0] >= n else np.concatenate([x, x[: n - x.shape[0]]])
+    else:
+        x = synth.clustered_bytes(n + 3 * ell, n, ell, n_centers=3, max_flips=3)
+    c, e, _ = assert_parity(cg, x)
+    c2, e2, _ = gpu_build(cg, x, sort_kind="nosmall")
+    np.testing.assert_array_equal(c, c2)
+    np.testing.assert_array_equal(e, e2)
+
+
+def test_small_path_errors_and_options(cg):
+    x = synth.clustered_bytes(9, 500, 40, n_centers=3, max_flips=3)
+    assert_parity(cg, x, lcp_prune=False)
+    assert_parity(cg, x, dict_kind="hash")
+    bad = x.copy()
+    bad[17, 5] = 2
+    with pytest.raises(cg.CgError) as ei:
+        cg.build(torch.from_numpy(bad).cuda())
+    assert ei.value.code == -2  # CG_EINPUT
 
 
 def test_random_uniform_many_layers(cg):
