@@ -301,6 +301,7 @@ def run_ours(args):
     f3 = run_f3(torch, cg, dev) if args.f1 else None
     f2 = run_f2(torch, cg, x, dev) if args.f1 else None
     qb = run_query(torch, cg, x, dev) if args.f1 else None
+    cfgs = run_configs(torch, cg, dev) if args.configs else None
     # ---- e2e through the host-buffer C-ABI entry
     e2e = run_e2e(torch, cg, x, args, dev)
     # ---- CPU oracle baseline on a bounded sample
@@ -334,6 +335,7 @@ def run_ours(args):
         "f3_allpairs": f3,
         "f2_insert": f2,
         "b_query": qb,
+        "configs_latency": cfgs,
     }
     print(json.dumps(out))
 
@@ -613,6 +615,49 @@ def run_f3(torch, cg, dev):
     return out
 
 
+def run_configs(torch, cg, dev, names=("C1", "C2", "C3", "C4")):
+    """The other BASELINE configs on one GPU (latency-bound at these sizes,
+    SURVEY 8.d.2): device-resident input, 3 warm-ups, then per build the
+    wall time of cg.build + a stream synchronize (what a caller waits for:
+    host round trips and allocations included) and, separately, CUDA-event
+    time on the stream; medians over 20 builds, no stats collection."""
+    import time
+
+    import synth
+
+    out = {}
+    for name in names:
+        d = synth.config(name)
+        if d.get("bytes") is not None:
+            x = torch.from_numpy(d["bytes"]).to(dev)
+        else:
+            x = synth.unpack_words_torch(torch.from_numpy(d["words"].view(np.int64)).to(dev), d["ell"])
+        stream = torch.cuda.current_stream(dev)
+        for _ in range(3):
+            r = cg.build(x, stream=stream)
+            del r
+        torch.cuda.synchronize(dev)
+        walls, evs = [], []
+        for _ in range(20):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            r = cg.build(x, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            walls.append((time.perf_counter() - t0) * 1e3)
+            evs.append(e0.elapsed_time(e1))
+            nc, m = int(r.cells.shape[0]), int(r.edges.shape[0])
+            del r
+        w = float(np.median(walls))
+        out[name] = {"n": int(x.shape[0]), "ell": int(x.shape[1]), "n_cells": nc, "n_edges": m,
+                     "wall_ms": round(w, 4), "event_ms": round(float(np.median(evs)), 4),
+                     "cells_per_s": round(nc / (w * 1e-3), 1)}
+        del x
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_e2e(torch, cg, x, args, dev):
     """Same metric through cg_build_host: pinned host input, H2D + build +
     D2H of the cell table and edge list inside the timed region."""
@@ -711,6 +756,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-f1", dest="f1", action="store_false",
                     help="skip the row-f1 signature measurement")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the per-config (C1-C4) latency lines")
     ap.add_argument("--cpu-sample-log2", type=int, default=22)
     ap.add_argument("--ref-sample-log2", type=int, default=20)
     args = ap.parse_args()

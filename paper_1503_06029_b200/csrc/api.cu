@@ -883,11 +883,11 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
       const uint64_t ecap = std::max<uint64_t>(1, uint64_t(n) * uint64_t(ell) / 2);
       uint64_t* ew = static_cast<uint64_t*>(dev_alloc(ecap * 8, s));
       b.edges = reinterpret_cast<uint32_t*>(ew);
-      DevBuf<int64_t> res(8, s);
+      DevBuf<int64_t> res(8, s);  // n_c, m, error (+ 4 phase clocks with SMALL_CLK)
       launch_small_build(vecs, n, ell, o.lcp_prune, cw, ew, res.p, s);
       tm.mark();  // the whole build is one kernel: reported as the pack stage
-      int64_t* hr = static_cast<int64_t*>(host_stage(8 * sizeof(int64_t)));
-      CG_CUDA(cudaMemcpyAsync(hr, res.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      int64_t* hr = static_cast<int64_t*>(host_stage(3 * sizeof(int64_t)));
+      CG_CUDA(cudaMemcpyAsync(hr, res.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       CG_CUDA(cudaStreamSynchronize(s));
       if (hr[2]) throw CgError{CG_EINPUT, "input byte not in {0,1}"};
       b.n_cells = hr[0];

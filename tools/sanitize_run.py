@@ -12,11 +12,14 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1503_06029_b200 import cg  # noqa: E402
 
+lp, _ = synth.planted_bytes(7, 3000, 700)  # W = 11: prefix sort + staged probe
 cases = [synth.config("C1")["bytes"], synth.clustered_bytes(3, 3000, 100, 4, 3),
-         synth.hypercube(10), synth.random_bytes(1, 5000, 200, dup_frac=0.5)]
+         synth.hypercube(10), synth.random_bytes(1, 5000, 200, dup_frac=0.5),
+         np.concatenate([lp, lp[:500]])]
 for x in cases:
     xt = torch.from_numpy(x).cuda()
-    for kw in (dict(), dict(dict_kind="sorted", want_index=True), dict(sort_kind="lsd")):
+    for kw in (dict(), dict(dict_kind="sorted", want_index=True), dict(sort_kind="lsd"),
+               dict(sort_kind="nosmall"), dict(dict_kind="hash")):
         r = cg.build(xt, **kw)
         if r.index is not None:
             q = r.cells[:64].contiguous()
