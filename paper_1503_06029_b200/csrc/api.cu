@@ -12,6 +12,8 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+
+#include <nvtx3/nvToolsExt.h>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -272,16 +274,33 @@ static void host_pool_free(void* p) {
 }
 
 // ---------------------------------------------------------------- stage timer
+// Stage boundaries: CUDA events on the build stream (only with stats) and
+// NVTX ranges "cg:<stage>" (always; no-ops unless a profiler is attached),
+// so nsys/ncu timelines show the stages of every build.
 struct StageTimer {
   bool on = false;
   cudaStream_t s = nullptr;
   std::vector<cudaEvent_t> ev;
+  int nmark = 0;
+  bool open = false;
+  static const char* name(int k) {
+    static const char* const n[] = {"cg:pack", "cg:sort", "cg:dedupe", "cg:layers",
+                                    "cg:dict", "cg:probe", "cg:edges"};
+    return k >= 0 && k < 7 ? n[k] : "cg:stage";
+  }
   void start(bool enable, cudaStream_t st) {
     on = enable;
     s = st;
-    if (on) mark();
+    mark();
   }
   void mark() {
+    if (open) nvtxRangePop();
+    open = false;
+    if (nmark < 7) {
+      nvtxRangePushA(name(nmark));
+      open = true;
+    }
+    ++nmark;
     if (!on) return;
     cudaEvent_t e;
     CG_CUDA(cudaEventCreate(&e));
@@ -295,6 +314,7 @@ struct StageTimer {
     return double(ms) * 1e3;
   }
   ~StageTimer() {
+    if (open) nvtxRangePop();
     for (auto e : ev) cudaEventDestroy(e);
   }
 };
