@@ -446,7 +446,7 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     DevBuf<uint32_t> tcnt(size_t(ntiles), s);  // hits per tile
     DevBuf<uint64_t> tpos(size_t(ntiles), s);  // block position in the scratch list (~0: overflow)
     DevBuf<uint32_t> ticket(2, s);
-    DevBuf<unsigned long long> ctr(4, s);
+    DevBuf<unsigned long long> ctr(6, s);
     DevBuf<uint4> ovf(size_t(ntiles), s);
     // scratch capacity: 4 hits per cell covers planted sets (m/n_c = 0.5) and
     // arrangement samples (degree ~ 2d, m/n_c <= 3 in R^3) in one probe pass;
@@ -457,19 +457,26 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
     int reruns = 0;
     uint64_t m = 0, issued = 0, novf = 0;
+    // ctr: [0] scratch slots reserved (warps reserve chunks), [1] hits placed,
+    // [2] issued probes; [3] spill count, [4..5] the spill run's (unused) pair
     while (true) {
       CG_CUDA(cudaMemsetAsync(ticket.p, 0, 8, s));
-      CG_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), s));
+      CG_CUDA(cudaMemsetAsync(ctr.p, 0, 6 * sizeof(unsigned long long), s));
       launch_probe_global(g, o.lcp_prune, i_lo, i_hi, hits.p, cap, tcnt.p, tpos.p, ticket.p, ctr.p,
-                          ctr.p + 1, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
-      CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-      CG_CUDA(cudaMemcpyAsync(hc + 2, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+                          ctr.p + 2, ovf.p, ticket.p + 1, nullptr, 0, nullptr, s);
+      CG_CUDA(cudaMemcpyAsync(hc, ctr.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CG_CUDA(cudaMemcpyAsync(hc + 3, ticket.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
       CG_CUDA(cudaStreamSynchronize(s));
-      m = hc[0];
-      issued = hc[1];
-      novf = uint32_t(hc[2] & 0xffffffffu);
-      if (m <= cap) break;
-      cap = m;
+      const uint64_t reserved = hc[0];
+      m = hc[1];
+      issued = hc[2];
+      novf = uint32_t(hc[3] & 0xffffffffu);
+      if (reserved <= cap) break;  // every block landed inside the scratch list
+      // re-run with room for m plus the chunk tails: a closed chunk wastes
+      // less than one block (<= tile cap), an open one less than a chunk
+      const uint64_t nw = uint64_t(num_sms()) * 64, ch = probe_global_scratch_chunk(),
+                     bc = uint64_t(probe_global_tile_edge_cap());
+      cap = m + (m / (ch - bc) + nw + 1) * bc + nw * ch;
       hits.alloc(cap, s);
       ++reruns;
     }
@@ -506,9 +513,9 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
       launch_scan_u32_u64(scnt.p, sstart.p, ntiles, s);
       DevBuf<uint64_t> sp1(ms, s), sp2(ms, s);
       CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
-      CG_CUDA(cudaMemsetAsync(ctr.p + 2, 0, sizeof(unsigned long long), s));
+      CG_CUDA(cudaMemsetAsync(ctr.p + 3, 0, 3 * sizeof(unsigned long long), s));
       launch_probe_global(g, o.lcp_prune, i_lo, i_hi, nullptr, 0, tcnt.p, tpos.p, ticket.p,
-                          ctr.p + 3, ctr.p + 3, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 2, s, sel.p);
+                          ctr.p + 4, ctr.p + 4, ovf.p, ticket.p + 1, sp1.p, ms, ctr.p + 3, s, sel.p);
       uint64_t* so = sp1.p;
       if (ms > 1) radix_sort<uint64_t>(sp1.p, sp2.p, nullptr, nullptr, nullptr, false, int64_t(ms), 64, &so, nullptr, s, nullptr);
       launch_spill_place(g, so, int64_t(ms), i_lo, toff.p, sstart.p, eout, s);

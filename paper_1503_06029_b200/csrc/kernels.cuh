@@ -241,6 +241,7 @@ void launch_tile_copy(const uint64_t* scratch, const uint64_t* off, const uint64
                       const uint32_t* cnt, int64_t ntiles, uint64_t* out, cudaStream_t s);
 int64_t probe_global_tiles(int64_t n);
 int probe_global_tile_cells();
+uint64_t probe_global_scratch_chunk();
 int probe_global_tile_edge_cap();
 // exclusive prefix sum of u32 in place (total < 2^32); edges.cu
 void launch_scan_u32(uint32_t* v, int64_t n, cudaStream_t s);

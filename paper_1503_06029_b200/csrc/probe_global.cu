@@ -38,6 +38,10 @@ constexpr int kTileCells = 32;      // cells per tile = lanes per warp
 constexpr int kProbeWarps = 8;      // warps per CTA (independent)
 constexpr int kWarpEdgeCap = 512;   // shared-memory edge buffer per warp
 constexpr int kTileEdgeCap = kWarpEdgeCap;
+constexpr uint32_t kScratchChunk = 4096;  // scratch slots a warp reserves at once (>= kWarpEdgeCap)
+#ifndef PROBE_TB
+#define PROBE_TB 4  // tiles a warp takes per ticket
+#endif
 #ifndef PROBE_MIN_BLOCKS
 #define PROBE_MIN_BLOCKS 6  // 40 registers, 6 CTAs (48 warps) per SM
 #endif
@@ -84,6 +88,13 @@ struct TileOut {
   uint64_t* spill;      // spill mode (overflow re-run): unordered global list
   uint64_t spill_cap;
   unsigned long long* spill_n;
+  // lane 0: the warp's current reservation of the scratch list (chunks of
+  // kScratchChunk slots, one atomic per chunk instead of one per tile: the
+  // per-tile atomic on a single counter was 38 % of the stall samples) and
+  // the warp's total hits (one atomic at the end of the kernel)
+  // (kept in shared memory, [0] chunk position, [1] slots left, [2] hits:
+  // registers are the probe's occupancy limit)
+  unsigned long long* st;
 
   __device__ __forceinline__ void emit(bool hit, uint64_t e) {
     const int lane = threadIdx.x & 31;
@@ -116,6 +127,11 @@ struct TileOut {
   // the scratch list.  tcnt / tpos let a scan + copy place the blocks in
   // canonical order afterwards (a look-back would make each tile wait for its
   // predecessor).  i0 = the tile's first source sequence number.
+  // at the end of the kernel: the warp's hits into total[1]
+  __device__ __forceinline__ void finish(unsigned long long* total) {
+    if ((threadIdx.x & 31) == 0 && st[2]) atomicAdd(total + 1, st[2]);
+  }
+
   template <class Canon>
   __device__ __forceinline__ void flush(int64_t tile, int64_t i0, uint64_t* __restrict__ out,
                                         uint64_t cap, uint32_t* __restrict__ tcnt,
@@ -150,6 +166,7 @@ struct TileOut {
     uint64_t bs = 0;
     if (lane == 0) {
       tcnt[tile] = wfill;
+      if (wfill <= uint32_t(kWarpEdgeCap)) st[2] += wfill;  // hits placed in the scratch list
       if (wfill > uint32_t(kWarpEdgeCap)) {
         // rare: hits beyond the warp buffer were dropped; the host re-runs
         // this tile in spill mode and writes its range directly
@@ -157,7 +174,13 @@ struct TileOut {
         ovf[k] = make_uint4(uint32_t(tile), 0u, wfill, 0u);
         bs = ~0ull;
       } else if (wfill) {
-        bs = atomicAdd(total, (unsigned long long)wfill);
+        if (st[1] < wfill) {  // a fresh chunk (the rest of the old one stays unused)
+          st[0] = atomicAdd(total, (unsigned long long)kScratchChunk);
+          st[1] = kScratchChunk;
+        }
+        bs = st[0];
+        st[0] += wfill;
+        st[1] -= wfill;
       }
       tpos[tile] = bs;  // position of the tile's block in the scratch list
     }
@@ -240,11 +263,21 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
   const int fb = g.b + g.fextra;
   uint32_t my_issued = 0;  // per thread (< 2^32); summed as 64-bit at the end
   uint64_t* wbuf = ebuf[tid >> 5];
+  __shared__ unsigned long long s_to[kProbeWarps][3];
+  if (lane == 0) s_to[tid >> 5][0] = s_to[tid >> 5][1] = s_to[tid >> 5][2] = 0;
+  __syncwarp();
+  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
+  uint32_t tb_left = 0, tb_next = 0;
 
   while (true) {
-    uint32_t tk = 0;
-    if (lane == 0) tk = atomicAdd(ticket, 1u);
-    const int64_t tile = __shfl_sync(kFull, tk, 0);
+    if (tb_left == 0) {  // PROBE_TB consecutive tiles per ticket
+      uint32_t tk = 0;
+      if (lane == 0) tk = atomicAdd(ticket, uint32_t(PROBE_TB));
+      tb_next = __shfl_sync(kFull, tk, 0);
+      tb_left = PROBE_TB;
+    }
+    const int64_t tile = int64_t(tb_next++);
+    --tb_left;
     if (tile >= ntiles) break;
     if (tile_sel && !tile_sel[tile]) continue;  // spill re-run: only the overflow tiles
     const int64_t i = i_lo + tile * kTileCells + lane;  // source sequence number q
@@ -398,7 +431,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
       return (uint64_t(g.idx[g.src_pos[uint32_t(e >> 32)]]) << 32) | g.idx[uint32_t(e)];
     };
 
-    TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n};
+    to.wfill = 0;
     auto emit = [&](bool hit, uint64_t e) { to.emit(hit, e); };
 
     // ---- near: rows i+1.. in V's own b-prefix bucket.  Every such row R is
@@ -693,6 +726,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     to.flush(tile, i - lane, out, cap, tcnt, tpos, total, ovf, ovf_n, canon);
     __syncwarp();
   }
+  to.finish(total);
   unsigned long long wsum = my_issued;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
@@ -772,10 +806,20 @@ __global__ void __launch_bounds__(32 * kProbeWarps, 4)
   const uint64_t bmask = (uint64_t(1) << lb) - 1;
   uint32_t my_issued = 0;
   uint64_t* wbuf = ebuf[tid >> 5];
+  __shared__ unsigned long long s_to[kProbeWarps][3];
+  if (lane == 0) s_to[tid >> 5][0] = s_to[tid >> 5][1] = s_to[tid >> 5][2] = 0;
+  __syncwarp();
+  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
+  uint32_t tb_left = 0, tb_next = 0;
   while (true) {
-    uint32_t tk = 0;
-    if (lane == 0) tk = atomicAdd(ticket, 1u);
-    const int64_t tile = __shfl_sync(kFull, tk, 0);
+    if (tb_left == 0) {  // PROBE_TB consecutive tiles per ticket
+      uint32_t tk = 0;
+      if (lane == 0) tk = atomicAdd(ticket, uint32_t(PROBE_TB));
+      tb_next = __shfl_sync(kFull, tk, 0);
+      tb_left = PROBE_TB;
+    }
+    const int64_t tile = int64_t(tb_next++);
+    --tb_left;
     if (tile >= ntiles) break;
     if (tile_sel && !tile_sel[tile]) continue;
     const int64_t i = i_lo + tile * kTileCells + lane;
@@ -795,7 +839,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, 4)
       }
     }
     const uint64_t h = valid ? g.hv[i] : 0ull;
-    TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n};
+    to.wfill = 0;
     // candidate bits: zero bits k <= kmax, word by word from the last
     int cw = kmax >= 0 ? (kmax >> 6) : -1;
     auto cmask = [&](int w) -> uint64_t {
@@ -876,6 +920,7 @@ __global__ void __launch_bounds__(32 * kProbeWarps, 4)
              [](uint64_t e) { return e; });
     __syncwarp();
   }
+  to.finish(total);
   unsigned long long wsum = my_issued;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
@@ -1120,6 +1165,7 @@ void launch_query_global(const GlobalDict& g, const uint64_t* q, int64_t nq, int
 
 int64_t probe_global_tiles(int64_t n) { return (n + kTileCells - 1) / kTileCells; }
 int probe_global_tile_edge_cap() { return kTileEdgeCap; }
+uint64_t probe_global_scratch_chunk() { return kScratchChunk; }
 int probe_global_tile_cells() { return kTileCells; }
 
 }  // namespace cgk
