@@ -96,6 +96,21 @@ def test_logical_ranks_words(cg, ell):
     np.testing.assert_array_equal(e, oe)
 
 
+@pytest.mark.parametrize("ell,G,chunk_bits", [(64, 4, 0), (128, 4, 2), (128, 8, 3), (100, 3, 1)])
+def test_merge_with_cross_rank_duplicates(cg, ell, G, chunk_bits):
+    """Random rows (the bucket merge path: every bucket fits the shared-memory
+    capacity) with 20 % of the rows repeated on other ranks: the direct
+    G-way merge must drop the copies and close the gaps."""
+    d, _ = synth.planted_bytes(ell + G, 30000, ell)
+    rng = np.random.default_rng(ell + G)
+    x = np.concatenate([d, d[rng.integers(0, d.shape[0], d.shape[0] // 5)]])
+    x = x[rng.permutation(x.shape[0])]
+    c, e, _, _ = logical_ranks(cg, x, G, chunk_bits)
+    rc, oc, oe = oracle.build(x)
+    np.testing.assert_array_equal(c, oc)
+    np.testing.assert_array_equal(e, oe)
+
+
 def test_logical_ranks_c5_recipe_vs_oracle(cg):
     d = synth.config("C5", scale_log2=18)
     x = synth.unpack_words_np(d["words"], 128)

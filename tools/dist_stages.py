@@ -16,7 +16,7 @@ from paper_1503_06029_b200 import cg  # noqa: E402
 
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 Gs = [int(g) for g in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 4, 8]
-chunk_bits = 3
+chunk_bits = int(os.environ.get("CHUNK_BITS", "3"))
 dev = torch.device("cuda:0")
 x, d = bench.make_c5_device(torch, lg, dev)
 n, ell = x.shape
