@@ -598,7 +598,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       sorted = ko;
     } else if (gather_dedupe_ok(W)) {
       order.alloc(size_t(ns), s);  // canonical order; the rows move once, in the dedupe
-      sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups);
+      const bool big = ns >= (int64_t(1) << 15);
+      if (!sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, big ? 1 : 0)) {
+        // long runs of equal 32-bit prefixes (arrangement signatures, which
+        // come with heavy duplication): drop the copies by hashing,
+        // then sort the distinct rows word by word
+        ns = hash_unique_rows(keys.p, ns, W, alt.p, s);
+        std::swap(keys.p, alt.p);
+        std::swap(keys.arena, alt.arena);
+        std::swap(keys.scratch, alt.scratch);
+        order.alloc(size_t(ns), s);
+        sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, 2);
+        no_dups = true;  // every row is distinct now
+      }
     } else {
       sort_rows_multiword(keys.p, ns, W, alt.p, s, &sst);
       sorted = alt.p;

@@ -83,9 +83,12 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
 // and no rows move.
 // *no_dups (optional) = true when the order is known to hold no two equal
 // rows (the 32-bit-prefix path compared every tie and found none).
-void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
+// mode: 0 = 32-bit-prefix sort, per-word LSD if long prefix-tie runs; 1 =
+// prefix sort only (returns false on long runs: nothing sorted); 2 = per-word
+// LSD only.  Returns true when the order is complete.
+bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
                          cudaStream_t s, SortStats* st, uint32_t* order = nullptr,
-                         bool* no_dups = nullptr);
+                         bool* no_dups = nullptr, int mode = 0);
 
 // MSD fast path for W in {1, 2}: LSD passes over the top B bits only (whole
 // keys move), then a shared-memory bitonic sort of each 2^B prefix bucket.

@@ -268,13 +268,17 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
   __syncwarp();
   TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
   uint32_t tb_left = 0, tb_next = 0;
+  // PROBE_TB tiles per ticket only when every warp gets many tickets (small
+  // inputs: one tile per ticket, or a few warps would take all the work)
+  const uint32_t tb =
+      ntiles >= int64_t(64) * gridDim.x * kProbeWarps ? uint32_t(PROBE_TB) : 1u;
 
   while (true) {
-    if (tb_left == 0) {  // PROBE_TB consecutive tiles per ticket
+    if (tb_left == 0) {  // tb consecutive tiles per ticket
       uint32_t tk = 0;
-      if (lane == 0) tk = atomicAdd(ticket, uint32_t(PROBE_TB));
+      if (lane == 0) tk = atomicAdd(ticket, tb);
       tb_next = __shfl_sync(kFull, tk, 0);
-      tb_left = PROBE_TB;
+      tb_left = tb;
     }
     const int64_t tile = int64_t(tb_next++);
     --tb_left;
@@ -811,12 +815,16 @@ __global__ void __launch_bounds__(32 * kProbeWarps, 4)
   __syncwarp();
   TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
   uint32_t tb_left = 0, tb_next = 0;
+  // PROBE_TB tiles per ticket only when every warp gets many tickets (small
+  // inputs: one tile per ticket, or a few warps would take all the work)
+  const uint32_t tb =
+      ntiles >= int64_t(64) * gridDim.x * kProbeWarps ? uint32_t(PROBE_TB) : 1u;
   while (true) {
-    if (tb_left == 0) {  // PROBE_TB consecutive tiles per ticket
+    if (tb_left == 0) {  // tb consecutive tiles per ticket
       uint32_t tk = 0;
-      if (lane == 0) tk = atomicAdd(ticket, uint32_t(PROBE_TB));
+      if (lane == 0) tk = atomicAdd(ticket, tb);
       tb_next = __shfl_sync(kFull, tk, 0);
-      tb_left = PROBE_TB;
+      tb_left = tb;
     }
     const int64_t tile = int64_t(tb_next++);
     --tb_left;

@@ -1387,15 +1387,15 @@ __global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
 }
 }  // namespace
 
-void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st, uint32_t* order, bool* no_dups) {
+bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
+                         cudaStream_t s, SortStats* st, uint32_t* order, bool* no_dups, int mode) {
   if (no_dups) *no_dups = false;
   auto finish = [&](const uint32_t* idx) {
     if (order) CG_CUDA(cudaMemcpyAsync(order, idx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     else launch_gather_rows(keys, idx, n, W, sorted, s);
   };
-  bool tried = false;
-  if (order && MW_PREFIX32) {
+  bool tried = mode == 2;  // mode 2: every word, no prefix attempt
+  if (order && MW_PREFIX32 && mode != 2) {
     // u64 keys (top 32 bits of word 0, row index): 4 stable keys-only passes
     // on the high half (digit bases scanned on the device: no host round
     // trip), then the runs of equal 32-bit prefixes are ordered on the full
@@ -1418,8 +1418,9 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     CG_CUDA(cudaStreamSynchronize(s));
     if ((h[0] & 1u) == 0) {
       if (no_dups) *no_dups = (h[0] & 2u) == 0;  // no two rows compared equal
-      return;
+      return true;
     }
+    if (mode == 1) return false;  // long runs: the caller decides (dedupe first)
     tried = true;  // long runs of equal prefixes (arrangement data): every word
   }
   DevBuf<uint64_t> kw(size_t(n), s), kw_alt(size_t(n), s);
@@ -1442,7 +1443,7 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     CG_CUDA(cudaStreamSynchronize(s));
     if (h[0] == 0) {
       finish(vo);
-      return;
+      return true;
     }
   }
   const uint32_t* idx = nullptr;  // identity before the first word pass
@@ -1457,6 +1458,7 @@ void sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     idx = vo;
   }
   finish(idx);
+  return true;
 }
 
 int msd_prefix_bits(int64_t n) {

@@ -446,3 +446,12 @@ def test_hash_dictionary_keeps_no_index(cg):
     x = torch.from_numpy(synth.random_bytes(1, 100, 16)).cuda()
     with pytest.raises(cg.CgError):
         cg.build(x, dict_kind="hash", want_index=True)
+
+
+@pytest.mark.parametrize("ell", [200, 700])
+def test_long_rows_long_ties_hash_then_sort(cg, ell):
+    """n >= 2^15 rows of W > 2 words with long runs of equal 32-bit prefixes
+    (clustered rows, heavy duplication): the prefix sort gives up, the copies
+    are dropped by hashing and the distinct rows are sorted word by word."""
+    x = synth.clustered_bytes(ell, 40000, ell, n_centers=5, max_flips=3)
+    assert_parity(cg, x)
