@@ -451,7 +451,9 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     // scratch capacity: 4 hits per cell covers planted sets (m/n_c = 0.5) and
     // arrangement samples (degree ~ 2d, m/n_c <= 3 in R^3) in one probe pass;
     // a larger m (P:106 allows n_c*ell/2) costs one re-run at the exact size
-    uint64_t cap = std::max<uint64_t>(4 * uint64_t(i_hi - i_lo), 1 << 16);
+    // (+ the warps' first chunk reservations: at least one tile cap each)
+    uint64_t cap = std::max<uint64_t>(4 * uint64_t(i_hi - i_lo), 1 << 16) +
+                   uint64_t(num_sms()) * 64 * uint64_t(probe_global_tile_edge_cap());
     if (o.edge_cap > 0) cap = uint64_t(o.edge_cap);
     DevBuf<uint64_t> hits(cap, s);  // tile blocks of sorted (i << 32 | j)
     unsigned long long* hc = static_cast<unsigned long long*>(host_stage(4 * sizeof(unsigned long long)));
@@ -600,15 +602,15 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       order.alloc(size_t(ns), s);  // canonical order; the rows move once, in the dedupe
       const bool big = ns >= (int64_t(1) << 15);
       if (!sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, big ? 1 : 0)) {
-        // long runs of equal 32-bit prefixes (arrangement signatures, which
-        // come with heavy duplication): drop the copies by hashing,
-        // then sort the distinct rows word by word
+        // runs of equal 32-bit prefixes too long for the run sort
+        // (arrangement signatures, which come with heavy duplication):
+        // drop the copies by hashing, then sort the distinct rows
         ns = hash_unique_rows(keys.p, ns, W, alt.p, s);
         std::swap(keys.p, alt.p);
         std::swap(keys.arena, alt.arena);
         std::swap(keys.scratch, alt.scratch);
         order.alloc(size_t(ns), s);
-        sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, 2);
+        sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, 0);
         no_dups = true;  // every row is distinct now
       }
     } else {

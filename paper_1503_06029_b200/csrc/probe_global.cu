@@ -95,6 +95,8 @@ struct TileOut {
   // (kept in shared memory, [0] chunk position, [1] slots left, [2] hits:
   // registers are the probe's occupancy limit)
   unsigned long long* st;
+  uint32_t chunk;  // slots per reservation: up to kScratchChunk, at most a quarter
+                   // of the scratch list spread over all warps (small inputs)
 
   __device__ __forceinline__ void emit(bool hit, uint64_t e) {
     const int lane = threadIdx.x & 31;
@@ -175,8 +177,8 @@ struct TileOut {
         bs = ~0ull;
       } else if (wfill) {
         if (st[1] < wfill) {  // a fresh chunk (the rest of the old one stays unused)
-          st[0] = atomicAdd(total, (unsigned long long)kScratchChunk);
-          st[1] = kScratchChunk;
+          st[0] = atomicAdd(total, (unsigned long long)chunk);
+          st[1] = chunk;
         }
         bs = st[0];
         st[0] += wfill;
@@ -266,7 +268,11 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
   __shared__ unsigned long long s_to[kProbeWarps][3];
   if (lane == 0) s_to[tid >> 5][0] = s_to[tid >> 5][1] = s_to[tid >> 5][2] = 0;
   __syncwarp();
-  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
+  uint32_t chunk = kScratchChunk;
+  while (chunk > uint32_t(kWarpEdgeCap) &&
+         uint64_t(chunk) * 4ull * gridDim.x * kProbeWarps > cap)
+    chunk >>= 1;
+  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5], chunk};
   uint32_t tb_left = 0, tb_next = 0;
   // PROBE_TB tiles per ticket only when every warp gets many tickets (small
   // inputs: one tile per ticket, or a few warps would take all the work)
@@ -813,7 +819,11 @@ __global__ void __launch_bounds__(32 * kProbeWarps, 4)
   __shared__ unsigned long long s_to[kProbeWarps][3];
   if (lane == 0) s_to[tid >> 5][0] = s_to[tid >> 5][1] = s_to[tid >> 5][2] = 0;
   __syncwarp();
-  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5]};
+  uint32_t chunk = kScratchChunk;
+  while (chunk > uint32_t(kWarpEdgeCap) &&
+         uint64_t(chunk) * 4ull * gridDim.x * kProbeWarps > cap)
+    chunk >>= 1;
+  TileOut to{wbuf, 0u, lt, spill, spill_cap, spill_n, s_to[tid >> 5], chunk};
   uint32_t tb_left = 0, tb_next = 0;
   // PROBE_TB tiles per ticket only when every warp gets many tickets (small
   // inputs: one tile per ticket, or a few warps would take all the work)

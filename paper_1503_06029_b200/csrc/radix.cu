@@ -1350,40 +1350,127 @@ __global__ void k_prefix_idx(const uint64_t* __restrict__ keys, int W, int64_t n
 // run raises *long_run (the caller then sorts every word).
 __global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
                                  const uint64_t* __restrict__ pk, int64_t n,
-                                 uint32_t* __restrict__ order, uint32_t* __restrict__ long_run) {
+                                 uint32_t* __restrict__ order, uint32_t* __restrict__ long_run,
+                                 int64_t run_cap, uint2* __restrict__ runs,
+                                 uint32_t* __restrict__ nruns) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t k = uint32_t(pk[i] >> 32);
     const bool head = i == 0 || uint32_t(pk[i - 1] >> 32) != k;
-    const bool run = i + 1 < n && uint32_t(pk[i + 1] >> 32) == k;
-    if (!head) continue;  // inside a run: its head writes it
-    if (!run) {
+    const bool tail = i + 1 >= n || uint32_t(pk[i + 1] >> 32) != k;
+    if (head && tail) {
       order[i] = uint32_t(pk[i]);
       continue;
     }
-    int64_t e = i + 2;
-    while (e < n && uint32_t(pk[e] >> 32) == k && e - i <= kTieRun) ++e;
-    if (e - i > kTieRun) {
-      atomicOr(long_run, 1u);
+    if (head) {
+      // a short run (<= kTieRun rows): its head insertion-sorts it on the
+      // full rows (equal rows keep index order)
+      int64_t e = i + 2;
+      while (e < n && uint32_t(pk[e] >> 32) == k && e - i <= kTieRun) ++e;
+      if (e - i > kTieRun) continue;  // a long run: its tail lists it
+      // a run beyond run_cap was found already: the caller discards this order
+      if (*reinterpret_cast<volatile uint32_t*>(long_run) & 1u) continue;
+      for (int64_t a = i; a < e; ++a) {
+        const uint32_t v = uint32_t(pk[a]);
+        const uint64_t* rv = keys + int64_t(v) * W;
+        int64_t z = a;
+        while (z > i) {
+          const uint32_t u = order[z - 1];
+          const uint64_t* ru = keys + int64_t(u) * W;
+          int c = 0;
+          for (int w = 0; w < W && c == 0; ++w) c = ru[w] < rv[w] ? -1 : (ru[w] > rv[w] ? 1 : 0);
+          if (c == 0) atomicOr(long_run, 2u);  // equal rows: the dedupe has work
+          if (c < 0 || (c == 0 && u < v)) break;
+          order[z] = u;
+          --z;
+        }
+        order[z] = v;
+      }
       continue;
     }
-    for (int64_t a = i; a < e; ++a) {
-      const uint32_t v = uint32_t(pk[a]);
-      const uint64_t* rv = keys + int64_t(v) * W;
-      int64_t z = a;
-      while (z > i) {
-        const uint32_t u = order[z - 1];
-        const uint64_t* ru = keys + int64_t(u) * W;
-        int c = 0;
-        for (int w = 0; w < W && c == 0; ++w) c = ru[w] < rv[w] ? -1 : (ru[w] > rv[w] ? 1 : 0);
-        if (c == 0) atomicOr(long_run, 2u);  // equal rows: the dedupe has work
-        if (c < 0 || (c == 0 && u < v)) break;
-        order[z] = u;
-        --z;
+    if (!tail) continue;
+    // the tail of a run: its head by a binary search over the last run_cap + 1
+    // positions (pk is sorted on the prefix); a run longer than kTieRun is
+    // listed for k_run_sort, one longer than run_cap goes to the caller
+    const int64_t lo0 = i - run_cap > 0 ? i - run_cap : 0;
+    int64_t lo = lo0, len = i - lo0;
+    while (len > 0) {
+      const int64_t half = len >> 1;
+      if (uint32_t(pk[lo + half] >> 32) < k) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
       }
-      order[z] = v;
+    }
+    const int64_t rl = i - lo + 1;
+    if (rl <= kTieRun) continue;  // its head sorted it
+    if (lo == lo0 && lo0 > 0 && uint32_t(pk[lo0 - 1] >> 32) == k) {
+      atomicOr(long_run, 1u);  // longer than run_cap
+    } else {
+      const uint32_t q = atomicAdd(nruns, 1u);
+      runs[q] = make_uint2(uint32_t(lo), uint32_t(rl));
     }
   }
+}
+
+// A long run of equal 32-bit prefixes (arrangement signatures): one CTA
+// loads its rows into shared memory and bitonic-sorts (row, index) pairs --
+// rows compared word by word, equal rows by index -- then writes the run's
+// part of the order.  Equal rows raise bit 2 of *flag (dedupe needed).
+__global__ void __launch_bounds__(256)
+    k_run_sort(const uint64_t* __restrict__ keys, int W, const uint64_t* __restrict__ pk,
+               const uint2* __restrict__ runs, uint32_t* __restrict__ order,
+               uint32_t* __restrict__ flag) {
+  extern __shared__ __align__(16) uint64_t rsm[];
+  const uint2 run = runs[blockIdx.x];
+  const int len = int(run.y);
+  int P = 1;
+  while (P < len) P <<= 1;
+  uint64_t* rw = rsm;                                    // [P][W]
+  uint32_t* ix = reinterpret_cast<uint32_t*>(rsm + size_t(P) * W);  // [P]
+  for (int t = threadIdx.x; t < P * W; t += blockDim.x) {
+    const int r = t / W, w = t - r * W;
+    rw[t] = r < len ? keys[int64_t(uint32_t(pk[run.x + r])) * W + w] : ~0ull;
+  }
+  for (int r = threadIdx.x; r < P; r += blockDim.x)
+    ix[r] = r < len ? uint32_t(pk[run.x + r]) : 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int o = i ^ j;
+        if (o > i) {
+          uint64_t* A = rw + size_t(i) * W;
+          uint64_t* B = rw + size_t(o) * W;
+          int c = 0;
+          for (int w = 0; w < W && c == 0; ++w) c = A[w] < B[w] ? -1 : (A[w] > B[w] ? 1 : 0);
+          if (c == 0) c = ix[i] < ix[o] ? -1 : (ix[i] > ix[o] ? 1 : 0);
+          if ((i & k) == 0 ? c > 0 : c < 0) {
+            for (int w = 0; w < W; ++w) {
+              const uint64_t x = A[w];
+              A[w] = B[w];
+              B[w] = x;
+            }
+            const uint32_t y = ix[i];
+            ix[i] = ix[o];
+            ix[o] = y;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  bool dup = false;
+  for (int r = threadIdx.x; r < len; r += blockDim.x) {
+    order[run.x + r] = ix[r];
+    if (r > 0) {
+      bool eq = true;
+      for (int w = 0; w < W && eq; ++w) eq = rw[size_t(r) * W + w] == rw[size_t(r - 1) * W + w];
+      dup |= eq;
+    }
+  }
+  if (dup) atomicOr(flag, 2u);
 }
 }  // namespace
 
@@ -1411,11 +1498,29 @@ bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     uint64_t* ko = nullptr;
     radix_passes<uint64_t>(pk.p, pk_alt.p, nullptr, nullptr, nullptr, false, n, 4, 8, &ko, nullptr,
                            s, st, hist.p);
-    k_tie_fix_prefix<<<grid_for(n, 256), 256, 0, s>>>(keys, W, ko, n, order, flag.p);
+    // long tie runs up to run_cap rows are sorted by k_run_sort (96 KB of
+    // shared memory per run at most)
+    constexpr size_t kRunSmem = 96 * 1024;
+    int64_t run_cap = 1;
+    while ((run_cap * 2) * (int64_t(W) * 8 + 4) <= int64_t(kRunSmem)) run_cap *= 2;
+    DevBuf<uint2> runs(size_t(n / (kTieRun + 1) + 1), s);
+    DevBuf<uint32_t> nr(1, s);
+    CG_CUDA(cudaMemsetAsync(nr.p, 0, 4, s));
+    k_tie_fix_prefix<<<grid_for(n, 256), 256, 0, s>>>(keys, W, ko, n, order, flag.p, run_cap, runs.p,
+                                                      nr.p);
     CG_LAUNCH_CHECK();
-    uint32_t* h = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+    uint32_t* h = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
     CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaMemcpyAsync(h + 1, nr.p, 4, cudaMemcpyDeviceToHost, s));
     CG_CUDA(cudaStreamSynchronize(s));
+    if ((h[0] & 1u) == 0 && h[1]) {
+      CG_CUDA(cudaFuncSetAttribute(k_run_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRunSmem)));
+      k_run_sort<<<h[1], 256, size_t(run_cap) * (size_t(W) * 8 + 4), s>>>(keys, W, ko, runs.p, order,
+                                                                           flag.p);
+      CG_LAUNCH_CHECK();
+      if (no_dups) *no_dups = false;  // (k_run_sort's duplicate bit is not read back)
+      return true;
+    }
     if ((h[0] & 1u) == 0) {
       if (no_dups) *no_dups = (h[0] & 2u) == 0;  // no two rows compared equal
       return true;
