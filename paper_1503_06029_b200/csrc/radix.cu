@@ -751,8 +751,11 @@ __device__ __forceinline__ uint32_t key_before(const ulonglong2& a, int ia, cons
   return uint32_t(a.x < b.x) | (ex & uint32_t(a.y < b.y)) | (ex & uint32_t(a.y == b.y) & uint32_t(ia < ib));
 }
 
+#ifndef BKT_RCAP
+#define BKT_RCAP 1152  // bucket-rank capacity (keys) for a ~1024-key mean bucket: 4 CTAs/SM
+#endif
 template <class K, int MAXC, bool PREF>
-__global__ void __launch_bounds__(kBktThreads, PREF ? 3 : 4)
+__global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
                   uint32_t* __restrict__ nlist) {
@@ -1074,7 +1077,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
   {
     // rank pass: keys (double-buffered with PREF) + two u16 orders + the
     // long-digit list; 1.5x the mean bucket; larger buckets go to the byte passes
-    const int rcap = avg <= 1024 ? 1536 : 2048;
+    const int rcap = avg <= 1024 ? BKT_RCAP : 2048;
     const size_t smem = size_t(rcap) * (2 * sizeof(K) + 8);
     const int per_sm = std::max(1, int((222 << 10) / (smem + 10 * 1024)));
     const int grid = int(std::min<int64_t>(nb, int64_t(num_sms()) * per_sm));
@@ -1083,7 +1086,8 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
     };
-    if (rcap == 1536) go(k_bucket_rank<K, 6, true>);
+    if (rcap <= 1280) go(k_bucket_rank<K, 5, true>);
+    else if (rcap <= 1536) go(k_bucket_rank<K, 6, true>);
     else go(k_bucket_rank<K, 8, true>);
     CG_LAUNCH_CHECK();
   }
