@@ -69,7 +69,7 @@ typedef struct {
 } cg_edges;
 
 /* Opaque, immutable dictionary over a cell table, built by cg_build_ex when
- * cg_opts.index_out is set: with CG_DICT_GLOBAL (default) a copy of the
+ * cg_opts.index_out is set: with CG_DICT_GLOBAL (or AUTO) a copy of the
  * canonical table plus its 2^b prefix index and prefix filter; with
  * CG_DICT_SORTED / CG_DICT_BSEARCH the popcount-layered arrays (DESIGN.md
  * a4-a5).  The dictionary replaces the paper's search tree (P:205-212,
@@ -99,15 +99,19 @@ enum {
   CG_DICT_SORTED = 0,  /* popcount layers: per-layer sorted array + 2^b prefix index + filter */
   CG_DICT_BSEARCH = 1, /* popcount layers, plain per-layer binary search (no prefix index) */
   CG_DICT_GLOBAL = 2,  /* one prefix index + filter over the canonical table; the probe
-                          writes the edge list in canonical order (no edge sort).  Default
-                          of cg_opts_init; its cg_index holds a copy of the table. */
-  CG_DICT_HASH = 3       /* open-addressed hash table over the canonical table (h = XOR of
+                          writes the edge list in canonical order (no edge sort); its
+                          cg_index holds a copy of the table. */
+  CG_DICT_HASH = 3,    /* open-addressed hash table over the canonical table (h = XOR of
                           per-bit 64-bit keys, so a flip is h ^ Z[k]; 4-slot 32-byte
                           buckets, load 1/2, every tag hit verified on the full row):
                           the north star's alternative dictionary (P:205 / P:276-281
                           replace the paper's tree), kept for the ncu A/B.  Same
                           output as CG_DICT_GLOBAL; keeps no cg_index (index_out with
                           it is CG_EINVAL). */
+  CG_DICT_AUTO = 4     /* default of cg_opts_init: CG_DICT_HASH when the rows are long
+                          (ell > 128) and heavily duplicated (n >= 4 n_c, arrangement
+                          signatures) and no index is requested, else
+                          CG_DICT_GLOBAL (DESIGN.md section 6 A/B) */
 };
 
 typedef struct {
@@ -130,7 +134,7 @@ typedef struct {
                            size; only speed depends on it */
 } cg_opts;
 
-/* Fill *o with defaults: stream NULL, CG_DICT_GLOBAL, lcp_prune 1,
+/* Fill *o with defaults: stream NULL, CG_DICT_AUTO, lcp_prune 1,
  * bucket_log2 -1, no index, no stats, filter_extra -1, edge_cap 0. */
 void cg_opts_init(cg_opts* o);
 

@@ -21,9 +21,9 @@ LIB_PATH = os.path.join(HERE, "lib", "libcg.so")
 
 CG_OK, CG_EINVAL, CG_EINPUT, CG_ENOMEM, CG_ECUDA, CG_ETOOBIG, CG_EARCH, CG_ENOTIMPL = (
     0, -1, -2, -3, -4, -5, -6, -7)
-CG_DICT_SORTED, CG_DICT_BSEARCH, CG_DICT_GLOBAL, CG_DICT_HASH = 0, 1, 2, 3
+CG_DICT_SORTED, CG_DICT_BSEARCH, CG_DICT_GLOBAL, CG_DICT_HASH, CG_DICT_AUTO = 0, 1, 2, 3, 4
 DICT_KINDS = {"sorted": CG_DICT_SORTED, "bsearch": CG_DICT_BSEARCH, "global": CG_DICT_GLOBAL,
-              "hash": CG_DICT_HASH}
+              "hash": CG_DICT_HASH, "auto": CG_DICT_AUTO}
 
 
 class CgError(RuntimeError):
@@ -303,7 +303,7 @@ def _stats_dict(st: cg_stats) -> dict:
 
 
 def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
-          dict_kind="global", lcp_prune: bool = True, bucket_log2: int = -1,
+          dict_kind="auto", lcp_prune: bool = True, bucket_log2: int = -1,
           want_index: bool = False, want_stats: bool = False,
           sort_kind="auto", filter_extra: int = -1, edge_cap: int = 0) -> BuildResult:
     """cg_build_ex on a CUDA uint8 tensor [n, ell] of 0/1 bytes."""
@@ -331,7 +331,7 @@ def build(vecs: torch.Tensor, *, stream: torch.cuda.Stream | None = None,
     return res
 
 
-def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="global",
+def build_packed(words: torch.Tensor, ell: int, *, stream=None, dict_kind="auto",
                  lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False,
                  sort_kind="auto", filter_extra=-1, edge_cap=0):
     """cg_build_packed_ex on CUDA int64 [n, ceil(ell/64)] MSB-first words."""
@@ -381,7 +381,7 @@ def signatures(points: torch.Tensor, planes: torch.Tensor, *, stream=None) -> to
     return words
 
 
-def build_points(points: torch.Tensor, planes: torch.Tensor, *, stream=None, dict_kind="global",
+def build_points(points: torch.Tensor, planes: torch.Tensor, *, stream=None, dict_kind="auto",
                  lcp_prune=True, bucket_log2=-1, want_index=False, want_stats=False,
                  sort_kind="auto") -> BuildResult:
     """cg_build_points (f1): the cell graph of the sampled points' signatures,
@@ -406,7 +406,7 @@ def build_points(points: torch.Tensor, planes: torch.Tensor, *, stream=None, dic
     return res
 
 
-def build_host(vecs_host: torch.Tensor, *, device=None, stream=None, dict_kind="global",
+def build_host(vecs_host: torch.Tensor, *, device=None, stream=None, dict_kind="auto",
                lcp_prune=True, bucket_log2=-1, want_stats=False):
     """cg_build_host: uint8 [n, ell] HOST tensor (pinned for full speed) in,
     numpy-compatible host results out: (cells int64 [nc, W], edges int32 [m, 2],

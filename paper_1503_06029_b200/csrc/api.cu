@@ -538,6 +538,9 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
   }
 }
 
+// the dictionaries over the whole canonical table (no popcount layers)
+static bool flat_dict(int k) { return k == CG_DICT_GLOBAL || k == CG_DICT_HASH || k == CG_DICT_AUTO; }
+
 // Runs a2..a7 given packed keys (u64[n][W], consumed as scratch).
 static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg_opts& o,
                             uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out,
@@ -601,7 +604,12 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     } else if (gather_dedupe_ok(W)) {
       order.alloc(size_t(ns), s);  // canonical order; the rows move once, in the dedupe
       const bool big = ns >= (int64_t(1) << 15);
-      if (!sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, big ? 1 : 0)) {
+      // heavy duplication (sampled: >= 8 of 1024 rows repeat; arrangement
+      // signatures) goes straight to the hash dedupe below (one
+      // sampling kernel + read-back, ~20 us; the prefix attempt it saves on
+      // such data costs ~100 us)
+      const bool dupy = big && sample_duplicates(keys.p, ns, W, s) >= 8;
+      if (dupy || !sort_rows_multiword(keys.p, ns, W, nullptr, s, &sst, order.p, &no_dups, big ? 1 : 0)) {
         // runs of equal 32-bit prefixes too long for the run sort
         // (arrangement signatures, which come with heavy duplication):
         // drop the copies by hashing, then sort the distinct rows
@@ -624,7 +632,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     cellbuf.alloc(size_t(ns) * W, s, Mem::Persist);
     // (the global dictionary needs neither popcounts nor lcp: the probe
     // derives lcp from the next row)
-    const bool meta = sh.cells_only || (o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH);
+    const bool meta = sh.cells_only || !flat_dict(o.dict_kind);
     if (order.p && no_dups) {
       // every row is a cell (the sort compared all ties): one gather, a
       // thread per word; n_c = n
@@ -635,7 +643,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       launch_gather_dedupe(keys.p, order.p, ns, W, cellbuf.p, meta ? popc.p : nullptr,
                            meta ? lcp.p : nullptr, d_flags + 1, s);
     else launch_dedupe(sorted, ns, W, cellbuf.p, popc.p, lcp.p, d_flags + 1, s);
-  } else if (!sh.cells_only && o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH) {
+  } else if (!sh.cells_only && !flat_dict(o.dict_kind)) {
     // cells came out of the fused MSD pass: per-cell popcount and LCP for the
     // layered dictionary (the global-dictionary probe derives lcp itself)
     launch_cell_meta(cellbuf.p, nc, W, popc.p, lcp.p, s);
@@ -668,9 +676,15 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     }
     return;
   }
-  if (o.dict_kind == CG_DICT_GLOBAL || o.dict_kind == CG_DICT_HASH) {
+  if (flat_dict(o.dict_kind)) {
+    // CG_DICT_AUTO: the hash dictionary for long rows with heavy duplication
+    // (arrangement signatures: huge prefix buckets, DESIGN section 6 A/B --
+    // C2 probe 267 -> 168 us), the prefix index otherwise
+    cg_opts od = o;
+    if (od.dict_kind == CG_DICT_AUTO)
+      od.dict_kind = (W > 2 && !o.index_out && nc * 4 <= n) ? CG_DICT_HASH : CG_DICT_GLOBAL;
     GlobalOut go;
-    global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, o, o.index_out != nullptr, tm, &go);
+    global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, od, o.index_out != nullptr, tm, &go);
     const uint64_t m = uint64_t(go.m);
     uint64_t* eout = go.edges;
     const int b = go.b, fextra = go.fextra;
@@ -858,7 +872,7 @@ static void validate_opts(const cg_opts& o) {
   if (o.dict_kind == CG_DICT_HASH && o.index_out)
     throw CgError{CG_EINVAL, "CG_DICT_HASH keeps no cg_index (use CG_DICT_GLOBAL for cg_query)"};
   if (o.dict_kind != CG_DICT_SORTED && o.dict_kind != CG_DICT_BSEARCH &&
-      o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH)
+      o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_HASH && o.dict_kind != CG_DICT_AUTO)
     throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
   if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
   if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};
@@ -916,7 +930,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     tm.start(o.stats != nullptr, s);  // 0
     setup_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
     if (vecs && o.sort_kind == 0 && small_build_ok(n, ell) && !o.index_out && o.edge_cap == 0 &&
-        (o.dict_kind == CG_DICT_GLOBAL || o.dict_kind == CG_DICT_HASH)) {
+        flat_dict(o.dict_kind)) {
       // small input: the whole path in one CTA, one host read-back (small.cu)
       uint64_t* cw = static_cast<uint64_t*>(dev_alloc(size_t(n) * W * 8, s));
       b.cells = cw;
@@ -1000,7 +1014,7 @@ extern "C" {
 void cg_opts_init(cg_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
-  o->dict_kind = CG_DICT_GLOBAL;
+  o->dict_kind = CG_DICT_AUTO;
   o->lcp_prune = 1;
   o->bucket_log2 = -1;
   o->filter_extra = -1;
@@ -1576,7 +1590,9 @@ int cg_dist_probe(const uint64_t* table, int64_t n_cells, int32_t ell, int32_t G
     if (n_cells > int64_t(0xffffffffll)) throw CgError{CG_ETOOBIG, "n_cells >= 2^32"};
     if (ell < 1 || ell > CG_MAX_ELL) throw CgError{CG_EINVAL, "ell must be in [1, 4096]"};
     validate_opts(o);
-    if (o.dict_kind != CG_DICT_GLOBAL) throw CgError{CG_ENOTIMPL, "cg_dist_probe uses CG_DICT_GLOBAL"};
+    if (o.dict_kind != CG_DICT_GLOBAL && o.dict_kind != CG_DICT_AUTO)
+      throw CgError{CG_ENOTIMPL, "cg_dist_probe uses CG_DICT_GLOBAL"};
+    o.dict_kind = CG_DICT_GLOBAL;
     check_arch();
     check_device_ptr(table, "table");
     reset_counters();

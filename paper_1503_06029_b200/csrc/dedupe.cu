@@ -289,7 +289,46 @@ __global__ void k_hash_compact(const uint64_t* __restrict__ rows, int64_t n, int
       for (int w = 0; w < W; ++w) out[int64_t(pos[i]) * W + w] = rows[i * W + w];
 }
 
+// Duplication estimate: 1024 rows sampled at a fixed stride, their 64-bit
+// row hashes inserted into a shared-memory table; *hits = sampled rows whose
+// hash was already there (a repeated row, or a 2^-64-rare collision).
+constexpr int kDupSample = 1024;
+__global__ void __launch_bounds__(kDupSample)
+    k_dup_sample(const uint64_t* __restrict__ rows, int64_t n, int W, uint32_t* hits) {
+  __shared__ unsigned long long tab[2 * kDupSample];
+  __shared__ uint32_t s_hits;
+  for (int t = threadIdx.x; t < 2 * kDupSample; t += blockDim.x) tab[t] = 0ull;
+  if (threadIdx.x == 0) s_hits = 0;
+  __syncthreads();
+  const int64_t stride = n / kDupSample > 0 ? n / kDupSample : 1;
+  for (int q = threadIdx.x; q < kDupSample && int64_t(q) * stride < n; q += blockDim.x) {
+    const uint64_t h = row_hash64(rows + int64_t(q) * stride * W, W) | 1ull;
+    uint32_t b = uint32_t(h >> 53) & (2 * kDupSample - 1);
+    while (true) {
+      const unsigned long long o = atomicCAS(&tab[b], 0ull, h);
+      if (o == 0ull) break;
+      if (o == h) {
+        atomicAdd(&s_hits, 1u);
+        break;
+      }
+      b = (b + 1) & (2 * kDupSample - 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *hits = s_hits;
+}
+
 }  // namespace
+
+uint32_t sample_duplicates(const uint64_t* rows, int64_t n, int W, cudaStream_t s) {
+  DevBuf<uint32_t> h(1, s);
+  k_dup_sample<<<1, kDupSample, 0, s>>>(rows, n, W, h.p);  // a thread per sampled row
+  CG_LAUNCH_CHECK();
+  uint32_t* hh = static_cast<uint32_t*>(host_stage(sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(hh, h.p, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  return hh[0];
+}
 
 int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, cudaStream_t s) {
   uint64_t cap = 1;

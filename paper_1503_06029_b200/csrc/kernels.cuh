@@ -86,9 +86,12 @@ void radix_sort(K* keys, K* keys_alt, const uint32_t* vals_in, uint32_t* vals, u
 // mode: 0 = 32-bit-prefix sort, per-word LSD if long prefix-tie runs; 1 =
 // prefix sort only (returns false on long runs: nothing sorted); 2 = per-word
 // LSD only.  Returns true when the order is complete.
+// dup_hits (device, mode 1): a duplication sample; >= 8 makes the prefix
+// sort give up at once (the caller then dedupes by hashing first).
 bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
                          cudaStream_t s, SortStats* st, uint32_t* order = nullptr,
-                         bool* no_dups = nullptr, int mode = 0);
+                         bool* no_dups = nullptr, int mode = 0,
+                         const uint32_t* dup_hits = nullptr);
 
 // MSD fast path for W in {1, 2}: LSD passes over the top B bits only (whole
 // keys move), then a shared-memory bitonic sort of each 2^B prefix bucket.
@@ -134,6 +137,9 @@ void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, 
 // (u64[n][W] capacity) by an open-addressed hash set; returns their count.
 // Used when skew overflows the MSD buckets.  Host-synchronising.
 int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, cudaStream_t s);
+// repeated rows among 1024 rows sampled at a fixed stride (0 for distinct
+// inputs); host-synchronising
+uint32_t sample_duplicates(const uint64_t* rows, int64_t n, int W, cudaStream_t s);
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],
 // lcp[n_c] (leading equal bits with the next cell; 0xffff for the last),
 // *n_cells (device u32).

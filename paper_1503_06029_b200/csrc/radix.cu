@@ -1356,7 +1356,12 @@ __global__ void k_tie_fix_prefix(const uint64_t* __restrict__ keys, int W,
                                  const uint64_t* __restrict__ pk, int64_t n,
                                  uint32_t* __restrict__ order, uint32_t* __restrict__ long_run,
                                  int64_t run_cap, uint2* __restrict__ runs,
-                                 uint32_t* __restrict__ nruns) {
+                                 uint32_t* __restrict__ nruns,
+                                 const uint32_t* __restrict__ dup_hits) {
+  if (dup_hits && *dup_hits >= 8u) {  // heavy duplication: the caller hashes first
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(long_run, 1u);
+    return;
+  }
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t k = uint32_t(pk[i] >> 32);
@@ -1479,7 +1484,8 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorted,
-                         cudaStream_t s, SortStats* st, uint32_t* order, bool* no_dups, int mode) {
+                         cudaStream_t s, SortStats* st, uint32_t* order, bool* no_dups, int mode,
+                         const uint32_t* dup_hits) {
   if (no_dups) *no_dups = false;
   auto finish = [&](const uint32_t* idx) {
     if (order) CG_CUDA(cudaMemcpyAsync(order, idx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
@@ -1511,7 +1517,7 @@ bool sort_rows_multiword(const uint64_t* keys, int64_t n, int W, uint64_t* sorte
     DevBuf<uint32_t> nr(1, s);
     CG_CUDA(cudaMemsetAsync(nr.p, 0, 4, s));
     k_tie_fix_prefix<<<grid_for(n, 256), 256, 0, s>>>(keys, W, ko, n, order, flag.p, run_cap, runs.p,
-                                                      nr.p);
+                                                      nr.p, mode == 1 ? dup_hits : nullptr);
     CG_LAUNCH_CHECK();
     uint32_t* h = static_cast<uint32_t*>(host_stage(2 * sizeof(uint32_t)));
     CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));

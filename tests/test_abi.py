@@ -69,7 +69,7 @@ def test_argument_errors_without_device(L):
     assert b"ell" in L.cg_last_error()
     o = cg_opts()
     L.cg_opts_init(ctypes.byref(o))
-    assert o.dict_kind == 2 and o.lcp_prune == 1 and o.bucket_log2 == -1
+    assert o.dict_kind == 4 and o.lcp_prune == 1 and o.bucket_log2 == -1  # CG_DICT_AUTO
     assert L.cg_query(None, None, 1, None, None, None) == CG_EINVAL
     assert L.cg_strerror(-2) == b"input byte not in {0,1} / pad bit set"
     assert L.cg_version() >= 1

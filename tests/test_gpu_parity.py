@@ -455,3 +455,17 @@ def test_long_rows_long_ties_hash_then_sort(cg, ell):
     are dropped by hashing and the distinct rows are sorted word by word."""
     x = synth.clustered_bytes(ell, 40000, ell, n_centers=5, max_flips=3)
     assert_parity(cg, x)
+
+
+def test_auto_dictionary_choice(cg):
+    """CG_DICT_AUTO (the default) takes the hash dictionary for long,
+    heavily duplicated rows (C2: the arrangement with 10x duplication) and the
+    prefix index otherwise; both give the oracle's graph (checked on C2 and
+    C4-like rows) and an index request keeps the prefix index."""
+    d = synth.config("C2")
+    _, _, r = assert_parity(cg, d["bytes"], want_stats=True)
+    assert r.stats["dict_bytes"] != 0
+    x, _ = synth.planted_bytes(4, 3000, 300)
+    assert_parity(cg, x)
+    rr = cg.build(torch.from_numpy(d["bytes"]).cuda(), want_index=True)
+    assert rr.index is not None
