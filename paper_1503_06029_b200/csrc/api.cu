@@ -565,7 +565,14 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   int64_t nc = -1;
   uint32_t in_err = 0;
   bool in_err_read = false;  // the input-error flag already came back with the sort's counts
-  if (msd) {
+  // mid-size inputs with heavy duplication (arrangement samples, P:108;
+  // C3: 54x) overflow the MSD buckets after two radix passes and the bucket
+  // pass (~0.3 ms at 2^20 rows): a 1024-row duplication sample sends them to
+  // the hash dedupe directly.  (Not at >= 2^24 rows, where the sample's
+  // read-back would cost every distinct-input build.)
+  const bool dupy_msd = msd && !sh.cells_only && pre_off == nullptr && n >= (int64_t(1) << 18) &&
+                        n < (int64_t(1) << 24) && sample_duplicates(keys.p, n, W, s) >= 8;
+  if (msd && !dupy_msd) {
     uint64_t* ko = nullptr;
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
