@@ -48,6 +48,12 @@ constexpr uint32_t kScratchChunk = 4096;  // scratch slots a warp reserves at on
 #ifndef PROBE_FR
 #define PROBE_FR 5  // filter loads in flight per round
 #endif
+#ifndef PROBE_UNI
+#define PROBE_UNI 1  // far filter rounds over the warp's union of candidate bits
+#endif
+#ifndef PROBE_FRU
+#define PROBE_FRU 5  // filter loads in flight per warp-uniform round
+#endif
 #ifndef PROBE_STG
 #define PROBE_STG 1  // W in (2, 16]: tile rows staged in shared memory
 #endif
@@ -247,7 +253,8 @@ constexpr int kStgExtra = 4;
 constexpr int kStgRows = kTileCells + kStgExtra;
 size_t probe_stg_smem(int W) { return size_t(kProbeWarps) * kStgRows * (W + 1) * 8; }
 
-template <int WC, bool SUB = false, int FR = PROBE_FR, int NR = 2, int SR = 2, bool STG = false>
+template <int WC, bool SUB = false, int FR = PROBE_FR, int NR = 2, int SR = 2, bool STG = false,
+          int FRU = PROBE_FRU>
 __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     k_probe_global(GlobalDict g, int lcp_prune, int64_t i_lo, int64_t i_hi, int64_t ntiles,
                    uint64_t* __restrict__ out, uint64_t cap, uint32_t* __restrict__ tcnt,
@@ -569,16 +576,44 @@ __global__ void __launch_bounds__(32 * kProbeWarps, STG ? 3 : PROBE_MIN_BLOCKS)
     // in the same top-word bit positions.
     uint32_t surv = 0;
     const int kfar = min(b - 1, kmax);
-    if (kfar >= 0) {
+    // With fextra >= 5 a far flip (key bit k < b) lands on prefix bit
+    // fb - 1 - k >= 5: it changes the filter WORD only, the bit within the
+    // word is the cell's own (y0 & 31), so the test is two shifts.
+    // Warp-uniform rounds (PROBE_UNI): the 32 cells of a tile are consecutive
+    // in canonical order and share their top ~log2(n/32) bits, so their
+    // candidate far bits are mostly the same positions; the warp walks the
+    // union of its lanes' candidate bits once (the loop counter, the bit
+    // extraction and the filter word offset are warp-uniform) and each lane
+    // keeps the bits it needs.  A lane whose bit k is 1 loads its own word
+    // (OR with the flip) and masks it out.  Per-lane rounds ran as many
+    // rounds as the lane with the most zero bits, ~11 instructions per slot.
+    if (PROBE_UNI && g.fextra >= 5 && b > 0) {
+      const uint32_t y0 = uint32_t(v0 >> (64 - fb));
+      const uint32_t zl = kfar >= 0 ? ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar)) : 0u;
+      my_issued += __popc(zl);
+      uint32_t uz = __reduce_or_sync(kFull, zl);
+      const uint32_t wy = y0 >> 5;
+      const int sh5 = 32 - fb + 5;
+      const uint32_t sc = 31u - (y0 & 31u);
+      while (uz) {
+        uint32_t bm[FRU], fw[FRU];
+#pragma unroll
+        for (int u = 0; u < FRU; ++u) {
+          bm[u] = uz & (0u - uz);
+          uz ^= bm[u];
+          fw[u] = __ldg(g.F + (wy | (bm[u] >> sh5)));
+        }
+#pragma unroll
+        for (int u = 0; u < FRU; ++u) surv |= bm[u] & uint32_t(int32_t(fw[u] << sc) >> 31);
+      }
+      surv &= zl;
+    } else if (kfar >= 0) {
       const uint32_t y0 = uint32_t(v0 >> (64 - fb));
       const int fsh = 32 - fb;
       uint32_t z = ~uint32_t(v0 >> 32) & (0xffffffffu << (31 - kfar));
       my_issued += __popc(z);
       // branch-free rounds of FR filter loads in flight; an exhausted slot
       // (bm = 0) re-reads the cell's own filter word and is masked out.
-      // With fextra >= 5 a far flip (key bit k < b) lands on prefix bit
-      // fb - 1 - k >= 5: it changes the filter WORD only, the bit within the
-      // word is the cell's own (y0 & 31), so the test is two shifts
       if (g.fextra >= 5) {
         const uint32_t wy = y0 >> 5;
         const int sh5 = fsh + 5;
