@@ -307,6 +307,15 @@ struct StageTimer {
     CG_CUDA(cudaEventRecord(e, s));
     ev.push_back(e);
   }
+  // drop every mark (a failed sweep attempt is re-run from the pack)
+  void restart() {
+    if (open) nvtxRangePop();
+    open = false;
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    nmark = 0;
+    mark();
+  }
   double us(int a, int b) const {
     if (!on || b >= int(ev.size())) return 0.0;
     float ms = 0.f;
@@ -546,7 +555,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
                             uint32_t* d_flags, StageTimer& tm, cg_stats* st, Built* out,
                             const Shard& sh = Shard(), const uint32_t* top_hist = nullptr,
                             const uint32_t* pre_off = nullptr, int pre_B = 0,
-                            const uint32_t* tile_hist = nullptr) {
+                            const uint32_t* tile_hist = nullptr, const SweepIn* sw = nullptr,
+                            bool* sweep_failed = nullptr) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
@@ -570,15 +580,19 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   // pass (~0.3 ms at 2^20 rows): a 1024-row duplication sample sends them to
   // the hash dedupe directly.  (Not at >= 2^24 rows, where the sample's
   // read-back would cost every distinct-input build.)
-  const bool dupy_msd = msd && !sh.cells_only && pre_off == nullptr && n >= (int64_t(1) << 18) &&
+  const bool dupy_msd = msd && !sw && !sh.cells_only && pre_off == nullptr && n >= (int64_t(1) << 18) &&
                         n < (int64_t(1) << 24) && sample_duplicates(keys.p, n, W, s) >= 8;
   if (msd && !dupy_msd) {
     uint64_t* ko = nullptr;
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
-    done = fused ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off, pre_B,
-                                   tile_hist, d_flags, &in_err, sh.pre_skip)
-                 : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
+    done = (fused || sw) ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off,
+                                           pre_B, tile_hist, d_flags, &in_err, sh.pre_skip, sw)
+                         : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
+    if (sw && !done) {  // a region or bucket slot overflowed: the caller re-packs
+      *sweep_failed = true;
+      return;
+    }
     sorted = ko;
     if (done && fused) {
       nc = ncu;
@@ -883,7 +897,7 @@ static void validate_opts(const cg_opts& o) {
     throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
   if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
   if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};
-  if (o.sort_kind < 0 || o.sort_kind > 2) throw CgError{CG_EINVAL, "sort_kind must be 0, 1 or 2"};
+  if (o.sort_kind < 0 || o.sort_kind > 3) throw CgError{CG_EINVAL, "sort_kind must be 0, 1, 2 or 3"};
   if (o.reserved0 != 0) throw CgError{CG_EINVAL, "reserved0 must be 0"};
 }
 
@@ -971,6 +985,32 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     const bool msd = W <= 2 && o.sort_kind != 1;
     DevBuf<uint64_t> keys(size_t(n) * W, s, msd ? Mem::Persist : Mem::Scratch);
     const int B = msd_prefix_bits(n);
+    // the sweep path (large 64/128-bit rows): the pack kernel does the MSD
+    // sort's first partition, the second needs no look-back
+    bool swept = false;
+    if (vecs && msd && o.sort_kind != 3 && B == 16 && pack_sweep_ok(vecs, n, ell)) {
+      const uint32_t capr = pack_sweep_capr(n);
+      bool failed = false;
+      {
+        DevBuf<uint64_t> regions(size_t(256) * capr * W, s);
+        DevBuf<uint32_t> rc(257, s);  // region counts, overflow flag
+        CG_CUDA(cudaMemsetAsync(rc.p + 256, 0, 4, s));
+        launch_pack_sweep(vecs, n, ell, regions.p, capr, rc.p, flags.p, rc.p + 256, s);
+        tm.mark();  // 1: pack
+        const SweepIn sw{regions.p, capr, rc.p, rc.p + 256};
+        build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(), nullptr, nullptr, B,
+                        nullptr, &sw, &failed);
+      }
+      swept = !failed;
+      if (failed) {  // skewed top bytes: the exact path from a fresh pack
+        tm.restart();
+        CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
+      }
+    }
+    if (swept) {
+      fill_stats(tm, n, o.stats);
+      store_counters(o.stats);
+    } else {
     const int dlo = (64 - B) / 8;
     DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
     // the pack kernel's per-tile counts of the first sort pass's digit (that
@@ -994,6 +1034,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
                     (vecs && msd) ? tile_hist.p : nullptr);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
+    }
     }
   } catch (...) {
     const int rc_ = current_error();

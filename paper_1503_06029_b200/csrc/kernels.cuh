@@ -11,6 +11,22 @@ namespace cgk {
 // dlo..7 of word 0, for the MSD sort (dlo in 5..7).
 // tile_hist (optional, with hist): u32[ceil(n / tile_rows)][256] counts of
 // digit dlo per tile of tile_rows rows (the first one-sweep pass's tiles).
+// The sweep path's input to sort_unique_msd (sw): launch_pack_sweep's regions
+// (u64[256][capr][W]), their row counts rcnt[256] and the overflow flag.
+struct SweepIn {
+  const uint64_t* regions;
+  uint32_t capr;
+  const uint32_t* rcnt;
+  uint32_t* ovf;
+};
+// Pack + the MSD sort's first partition (the "sweep" path, ell = 64 W,
+// W <= 2): rows go to 256 regions of capr rows by the top byte of word 0,
+// region d = regions[d * capr * W ..), rcnt[d] rows (unordered inside a
+// region); *ovf != 0 if some region overflowed (the result is then invalid).
+bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell);
+uint32_t pack_sweep_capr(int64_t n);
+void launch_pack_sweep(const uint8_t* vecs, int64_t n, int ell, uint64_t* regions, uint32_t capr,
+                       uint32_t* rcnt, uint32_t* err, uint32_t* ovf, cudaStream_t s);
 void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32_t* err,
                  cudaStream_t s, uint32_t* hist = nullptr, int dlo = 8,
                  uint32_t* tile_hist = nullptr, int tile_rows = 0);
@@ -126,7 +142,8 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
                      const uint32_t* pre_off = nullptr, int pre_B = 0,
                      const uint32_t* tile_hist = nullptr, const uint32_t* side_dev = nullptr,
-                     uint32_t* side_host = nullptr, int pre_skip = 0);
+                     uint32_t* side_host = nullptr, int pre_skip = 0,
+                     const struct SweepIn* sw = nullptr);
 int msd_tile_rows(int W);
 // popcount (optional) and lcp with the next cell, for a canonical table
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,

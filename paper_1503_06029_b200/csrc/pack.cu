@@ -138,6 +138,116 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
   }
 }
 
+// ---------------------------------------------------------------- pack + first MSD partition
+// The MSD sort's first pass fused into the pack ("sweep"
+// path; ell = 64 W, W <= 2, 16-byte aligned input).  A CTA of kSweepThreads
+// threads packs a tile of kSweepRows rows into shared memory -- fully
+// coalesced 16-byte loads (a warp reads 512 contiguous bytes per
+// instruction), each chunk's 16 bits OR-combined over the 4 lanes that hold
+// one 64-bit word -- then ranks the rows by the top byte of word 0 with
+// shared atomics (the order inside a digit is free: every top-16-bit bucket
+// is sorted completely by the bucket pass), reserves each digit's run in
+// that digit's region with ONE global atomicAdd per (tile, digit) (no
+// look-back, no histogram pass: region d is over-allocated to capr rows),
+// reorders the tile in shared memory and writes the runs.  A region that
+// would overflow sets *ovf and is clipped; the caller then re-packs and
+// takes the exact path.
+constexpr int kSweepThreads = 512;
+constexpr int kSweepRPT = 8;  // rows per thread in the rank phase
+constexpr int kSweepRows = kSweepThreads * kSweepRPT;
+
+template <int W>
+__global__ void __launch_bounds__(kSweepThreads, 2) k_pack_sweep(
+    const uint8_t* __restrict__ vecs, int64_t n, uint64_t* __restrict__ regions, uint32_t capr,
+    uint32_t* __restrict__ rcnt, uint32_t* __restrict__ err, uint32_t* __restrict__ ovf) {
+  constexpr int C = 4 * W;  // 16-byte chunks per row (ell = 64 W bytes)
+  constexpr int TR = kSweepRows, NT = kSweepThreads;
+  constexpr int STEPS = TR * C / NT;  // chunk loads per thread
+  constexpr int U = 8;                // loads in flight per thread
+  static_assert(STEPS % U == 0, "sweep tile");
+  extern __shared__ __align__(16) uint64_t sk[];  // [TR][W]
+  __shared__ uint32_t hc[256], dex[256], lim[256], s_scan[33];
+  __shared__ uint64_t gb[256];
+  const int tid = threadIdx.x;
+  const int64_t r0 = int64_t(blockIdx.x) * TR;
+  const int rows = int(min(int64_t(TR), n - r0));
+  const int nch = rows * C;
+  if (tid < 256) hc[tid] = 0u;
+  const uint4* src = reinterpret_cast<const uint4*>(vecs + r0 * (64 * W));
+  uint64_t bad = 0;
+  const int j = tid & (C - 1);        // chunk of the row this thread reads (NT % C == 0)
+  const int sh = 48 - 16 * (j & 3);   // its 16 bits inside the word
+  for (int s0 = 0; s0 < STEPS; s0 += U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = (s0 + u) * NT + tid;
+      v[u] = c < nch ? __ldcs(src + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = (s0 + u) * NT + tid;
+      const uint64_t lo = (uint64_t(v[u].y) << 32) | v[u].x;
+      const uint64_t hi = (uint64_t(v[u].w) << 32) | v[u].z;
+      bad |= (lo | hi) & kHi7;
+      uint64_t p = (uint64_t(bits8_msb(lo)) << (sh + 8)) | (uint64_t(bits8_msb(hi)) << sh);
+      p |= __shfl_xor_sync(kFull, p, 1);
+      p |= __shfl_xor_sync(kFull, p, 2);
+      if ((tid & 3) == 0 && c < nch) sk[(c / C) * W + (j >> 2)] = p;
+    }
+  }
+  __syncthreads();
+  uint64_t key[kSweepRPT][W];
+  uint32_t rk[kSweepRPT];
+#pragma unroll
+  for (int k = 0; k < kSweepRPT; ++k) {
+    const int r = k * NT + tid;
+    rk[k] = 0u;
+#pragma unroll
+    for (int w = 0; w < W; ++w) key[k][w] = r < rows ? sk[r * W + w] : 0ull;
+    if (r < rows) rk[k] = atomicAdd(&hc[uint32_t(key[k][0] >> 56)], 1u);
+  }
+  __syncthreads();
+  // digit d = tid (< 256): tile count, local start, region reservation
+  const uint32_t c = tid < 256 ? hc[tid] : 0u;
+  uint32_t tot;
+  const uint32_t ex = block_excl_scan(c, s_scan, &tot);
+  if (tid < 256) {
+    uint32_t base = 0;
+    if (c) {
+      base = atomicAdd(&rcnt[tid], c);
+      if (uint64_t(base) + c > capr) atomicOr(ovf, 1u);
+    }
+    dex[tid] = ex;
+    gb[tid] = uint64_t(tid) * capr + base - ex;  // region row of local position ex + q = gb + ex + q
+    lim[tid] = ex + (base < capr ? capr - base : 0u);  // local positions below lim fit
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kSweepRPT; ++k) {
+    const int r = k * NT + tid;
+    if (r < rows) {
+      const uint32_t pos = dex[uint32_t(key[k][0] >> 56)] + rk[k];
+#pragma unroll
+      for (int w = 0; w < W; ++w) sk[pos * W + w] = key[k][w];
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < rows; q += NT) {
+    const uint32_t d = uint32_t(sk[q * W] >> 56);
+    if (uint32_t(q) < lim[d]) {
+      const uint64_t g = gb[d] + uint64_t(q);
+      if (W == 2) {
+        *reinterpret_cast<ulonglong2*>(regions + 2 * g) =
+            *reinterpret_cast<const ulonglong2*>(sk + 2 * q);
+      } else {
+        regions[g] = sk[q];
+      }
+    }
+  }
+  if (bad) atomicOr(err, 1u);
+}
+
 __global__ void k_check_pad(const uint64_t* __restrict__ words, int64_t n, int W, uint64_t pad,
                             uint32_t* __restrict__ err) {
   uint64_t bad = 0;
@@ -166,6 +276,33 @@ void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32
     k_pack<8><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
   } else {
     k_pack<1><<<unsigned(blocks), threads, 0, s>>>(vecs, n, ell, W, keys, err, hist, dlo, tile_hist, tile_rows);
+  }
+  CG_LAUNCH_CHECK();
+}
+
+bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell) {
+  return (ell == 64 || ell == 128) && (reinterpret_cast<uintptr_t>(vecs) % 16) == 0 &&
+         n >= (int64_t(1) << 24) && n < (int64_t(1) << 32);
+}
+
+uint32_t pack_sweep_capr(int64_t n) {
+  // mean region + 1/16 + two tiles: uniform top bytes never come close
+  const int64_t mean = (n + 255) / 256;
+  return uint32_t(mean + mean / 16 + 2 * kSweepRows);
+}
+
+void launch_pack_sweep(const uint8_t* vecs, int64_t n, int ell, uint64_t* regions, uint32_t capr,
+                       uint32_t* rcnt, uint32_t* err, uint32_t* ovf, cudaStream_t s) {
+  const int W = ell / 64;
+  const int64_t tiles = (n + kSweepRows - 1) / kSweepRows;
+  const size_t smem = size_t(kSweepRows) * W * 8;
+  CG_CUDA(cudaMemsetAsync(rcnt, 0, 256 * sizeof(uint32_t), s));
+  if (W == 2) {
+    CG_CUDA(cudaFuncSetAttribute(k_pack_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_pack_sweep<2><<<unsigned(tiles), kSweepThreads, smem, s>>>(vecs, n, regions, capr, rcnt, err, ovf);
+  } else {
+    CG_CUDA(cudaFuncSetAttribute(k_pack_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_pack_sweep<1><<<unsigned(tiles), kSweepThreads, smem, s>>>(vecs, n, regions, capr, rcnt, err, ovf);
   }
   CG_LAUNCH_CHECK();
 }

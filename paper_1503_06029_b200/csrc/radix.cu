@@ -226,6 +226,88 @@ __global__ void __launch_bounds__(kSortThreads, OS_MINB)
   }
 }
 
+// Second partition of the sweep path (after k_pack_sweep): region x (top
+// byte x) is split by the next byte into the buckets (x, d) of the top 16
+// bits.  The tile structure of k_onesweep, but the order inside a bucket is
+// free (the bucket pass sorts each bucket completely), so ranks come from
+// shared atomics and each (tile, bucket) run is reserved in the bucket's
+// slot of cap16 rows with one global atomicAdd -- no look-back.  Block
+// x * tpr + t takes tile t of region x.
+template <class K>
+__global__ void __launch_bounds__(kSortThreads, OS_MINB)
+    k_region_sweep(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
+                   uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
+                   uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf) {
+  constexpr int IPT = TileCfg<K, false>::IPT;
+  constexpr int TILE = TileCfg<K, false>::TILE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* skeys = reinterpret_cast<K*>(smem_raw);
+  __shared__ uint32_t wcnt[kSortWarps][kRadix];
+  __shared__ uint32_t s_dexcl[kRadix], s_lim[kRadix], s_gbase[kRadix];
+  __shared__ uint32_t s_scan[33];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t x = blockIdx.x / tpr, t = blockIdx.x % tpr;
+  const uint32_t cnt = min(rcnt[x], capr);
+  const uint32_t beg = t * uint32_t(TILE);
+  if (beg >= cnt) return;  // (block-uniform)
+  const int nt = int(min(uint32_t(TILE), cnt - beg));
+  for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const K* kin = regions + size_t(x) * capr + beg;
+  const int wb = w * 32 * IPT;
+  K key[IPT];
+  uint32_t rank[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int g = wb + i * 32 + lane;
+    key[i] = g < nt ? kin[g] : K{};
+  }
+#pragma unroll
+  for (int i = 0; i < IPT; ++i)
+    if (wb + i * 32 + lane < nt) rank[i] = atomicAdd(&wcnt[w][digit_of(key[i], 48)], 1u);
+  __syncthreads();
+  uint32_t total = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww) {
+    const uint32_t c = wcnt[ww][tid];
+    wcnt[ww][tid] = total;
+    total += c;
+  }
+  uint32_t tile_n;
+  const uint32_t dex = block_excl_scan(total, s_scan, &tile_n);
+  uint32_t base = 0;
+  const uint32_t q = (x << 8) | uint32_t(tid);
+  if (total) {
+    base = atomicAdd(&cnt16[q], total);
+    if (uint64_t(base) + total > cap16) atomicOr(ovf, 1u);
+  }
+  s_dexcl[tid] = dex;
+  s_gbase[tid] = q * cap16 + base - dex;  // slot row of local position dex + r: s_gbase + dex + r
+  s_lim[tid] = dex + (base < cap16 ? cap16 - base : 0u);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if (wb + i * 32 + lane < nt) {
+      const uint32_t d = digit_of(key[i], 48);
+      skeys[s_dexcl[d] + wcnt[w][d] + rank[i]] = key[i];
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < nt; j += kSortThreads) {
+    const K k = skeys[j];
+    const uint32_t d = digit_of(k, 48);
+    if (uint32_t(j) < s_lim[d]) slots[s_gbase[d] + uint32_t(j)] = k;
+  }
+}
+
+// off[q] = min(cnt16[q], cap) (then scanned), off[nb] = 0
+__global__ void k_clip_counts(const uint32_t* __restrict__ cnt, int64_t nb, uint32_t cap,
+                              uint32_t* __restrict__ off) {
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q <= nb;
+       q += int64_t(gridDim.x) * blockDim.x)
+    off[q] = q < nb ? min(cnt[q], cap) : 0u;
+}
+
 __global__ void k_iota(uint32_t* v, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
@@ -758,7 +840,7 @@ template <class K, int MAXC, bool PREF>
 __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
-                  uint32_t* __restrict__ nlist) {
+                  uint32_t* __restrict__ nlist, const K* __restrict__ src, uint32_t scap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // PREF: the next bucket is prefetched (cp.async) into a second buffer;
   // otherwise one buffer and more resident CTAs hide the load latency
@@ -796,6 +878,12 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     }
     __syncthreads();
   }
+  // the bucket's input rows: in place (src == nullptr) or, on the sweep
+  // path, bucket bk's slot of scap rows in src; the output always goes to
+  // keys + off[bk]
+  auto rsrc = [&](int64_t bk, uint32_t lo) -> const K* {
+    return src ? src + size_t(bk) * scap : keys + lo;
+  };
   auto prefetch = [&](int64_t bk, K* dst, uint64_t* bar) {
     if (BULK) {
       if (tid == 0) {
@@ -809,7 +897,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
           // those writes before the async-proxy (TMA) writes
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive_expect_tx(bar, S * uint32_t(sizeof(K)));
-          bulk_g2s(dst, keys + lo, S * uint32_t(sizeof(K)), bar);
+          bulk_g2s(dst, rsrc(bk, lo), S * uint32_t(sizeof(K)), bar);
         } else {
           mbar_arrive(bar);  // nothing to move: complete the phase
         }
@@ -820,7 +908,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
       const uint32_t lo = off[bk];
       const int S = int(off[bk + 1] - lo);
       if (S <= CAP)
-        for (int i = tid; i < S; i += kBktThreads) cp_async_key(dst + i, keys + lo + i);
+        for (int i = tid; i < S; i += kBktThreads) cp_async_key(dst + i, rsrc(bk, lo) + i);
     }
     cp_async_commit();
   };
@@ -837,14 +925,22 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     __syncthreads();
     const uint32_t lo = off[bk], hi = off[bk + 1];
     const int S = int(hi - lo);
+    // a listed bucket is finished in place by the byte-pass kernel: on the
+    // sweep path its rows are first copied to their output range
+    auto list_bucket = [&]() {
+      if (src)
+        for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = rsrc(bk, lo)[i];
+      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
+      __syncthreads();
+    };
     if (S <= 1) {
       if (ucnt && tid == 0) ucnt[bk] = uint32_t(S);
+      if (src && S == 1 && tid == 0) keys[lo] = s[0];
       __syncthreads();
       continue;
     }
     if (S > CAP) {
-      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
-      __syncthreads();
+      list_bucket();
       continue;
     }
     // ---- 1. bits that vary inside the bucket
@@ -855,7 +951,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
-        kr[c] = keys[lo + (i < S ? i : 0)];
+        kr[c] = rsrc(bk, lo)[i < S ? i : 0];
         if (i < S) s[i] = kr[c];
       }
     }
@@ -941,8 +1037,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     }
     if (tid == 0) h[kBins] = uint32_t(S);
     if (__syncthreads_or(too_long)) {
-      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
-      __syncthreads();
+      list_bucket();
       continue;
     }
     // ---- 3. scatter, then rank inside the digit
@@ -979,8 +1074,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     __syncthreads();
     const uint32_t nmany = s_nmany;
     if (nmany > mcap) {  // (skewed digits) the byte-pass kernel takes the bucket
-      if (tid == 0) blist[atomicAdd(nlist, 1u)] = uint32_t(bk);
-      __syncthreads();
+      list_bucket();
       continue;
     }
     if (nmany) {
@@ -1069,7 +1163,8 @@ int grid_for(int64_t n, int threads, int per_sm = 8) {
 // larger than its capacity) go through the stable byte-pass kernel.
 template <class K>
 void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
-                        uint32_t* ucnt, cudaStream_t s) {
+                        uint32_t* ucnt, cudaStream_t s, const K* src = nullptr,
+                        uint32_t scap = 0) {
   const int64_t avg = (n + nb - 1) / nb;
   const int cap = avg <= 1024 ? 2048 : 4096;
   DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
@@ -1084,7 +1179,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
     auto go = [&](auto kern) {
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p);
+      kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p, src, scap);
     };
     if (rcap <= 1280) go(k_bucket_rank<K, 5, true>);
     else if (rcap <= 1536) go(k_bucket_rank<K, 6, true>);
@@ -1626,12 +1721,15 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
                       SortStats* st, const uint32_t* top_hist, const uint32_t* pre_off = nullptr,
                       int pre_B = 0, const uint32_t* tile_hist = nullptr,
                       const uint32_t* side_dev = nullptr, uint32_t* side_host = nullptr,
-                      int pre_skip = 0) {
+                      int pre_skip = 0, const SweepIn* sw = nullptr) {
   // pre_off: keys are already grouped by their top pre_B bits (scatter pack),
-  // pre_off[b] = first row of bucket b -- no global pass needed
-  const int B = pre_off ? pre_B : msd_prefix_bits(n);
+  // pre_off[b] = first row of bucket b -- no global pass needed.
+  // sw (the sweep path): the rows are in k_pack_sweep's 256 top-byte regions;
+  // k_region_sweep splits them into the 2^16 bucket slots and the bucket
+  // pass reads each slot and writes its bucket, sorted, to keys + off[b]
+  const int B = sw ? 16 : (pre_off ? pre_B : msd_prefix_bits(n));
   K* ko = keys;
-  if (!pre_off)
+  if (!pre_off && !sw)
     radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
                     s, st, top_hist, tile_hist);
   const int64_t nb = int64_t(1) << B;
@@ -1640,16 +1738,44 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   DevBuf<uint32_t> ucnt(size_t(nb), s), uoff(size_t(nb), s);
   DevBuf<uint32_t> flag(1, s);
   CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
-  if (!pre_off) {
+  DevBuf<K> slots;
+  uint32_t cap16 = 0;
+  if (sw) {
+    // slot capacity: mean + max(mean / 4, 8 sigma) (uniform buckets of ~2^10
+    // rows: 1312); a fuller bucket sets the overflow flag (caller re-runs)
+    const int64_t mean = (n + nb - 1) / nb;
+    int64_t sig8 = 8;
+    while (sig8 * sig8 < 64 * mean) ++sig8;
+    cap16 = uint32_t(mean + std::max(mean / 4, sig8) + 32);
+    slots.alloc(size_t(nb) * cap16, s);
+    DevBuf<uint32_t> cnt16(size_t(nb), s);
+    CG_CUDA(cudaMemsetAsync(cnt16.p, 0, cnt16.n * 4, s));
+    constexpr int TILE = TileCfg<K, false>::TILE;
+    const uint32_t tpr = (sw->capr + TILE - 1) / TILE;
+    CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(TileCfg<K, false>::SMEM)));
+    k_region_sweep<K><<<unsigned(256 * tpr), kSortThreads, TileCfg<K, false>::SMEM, s>>>(
+        reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16, cnt16.p,
+        sw->ovf);
+    CG_LAUNCH_CHECK();
+    k_clip_counts<<<grid_for(nb + 1, 256), 256, 0, s>>>(cnt16.p, nb, cap16, offb.p);
+    CG_LAUNCH_CHECK();
+    launch_scan_u32(offb.p, nb + 1, s);
+    if (st) st->passes += 1;  // the region sweep (the first partition ran in the pack)
+  } else if (!pre_off) {
     k_bucket_bounds_search<K><<<unsigned((nb + 256) / 256), 256, 0, s>>>(ko, n, B, offb.p);
     CG_LAUNCH_CHECK();
   }
   // the bucket kernels skip the key bytes every key of a bucket shares: the
   // top pre_skip + B bits
-  launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s);
+  launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s, sw ? slots.p : nullptr,
+                        cap16);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
-  uint32_t* h = static_cast<uint32_t*>(host_stage(4 * sizeof(uint32_t)));
+  uint32_t* h = static_cast<uint32_t*>(host_stage(5 * sizeof(uint32_t)));
+  h[4] = 0;
+  if (sw) CG_CUDA(cudaMemcpyAsync(h + 4, sw->ovf, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaMemcpyAsync(h + 1, uoff.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaMemcpyAsync(h + 2, ucnt.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
@@ -1658,7 +1784,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   CG_CUDA(cudaStreamSynchronize(s));
   if (side_dev && side_host) *side_host = h[3];
   *cells = ko;
-  if (h[0]) return false;
+  if (h[0] || h[4]) return false;
   const int64_t total = int64_t(h[1]) + int64_t(h[2]);
   *nc = total;
   if (total != n) {  // duplicates removed: close the gaps between buckets
@@ -1680,11 +1806,12 @@ int msd_tile_rows(int W) {
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
                      int64_t* nc, cudaStream_t s, SortStats* st, const uint32_t* top_hist,
                      const uint32_t* pre_off, int pre_B, const uint32_t* tile_hist,
-                     const uint32_t* side_dev, uint32_t* side_host, int pre_skip) {
+                     const uint32_t* side_dev, uint32_t* side_host, int pre_skip,
+                     const SweepIn* sw) {
   if (W == 1) {
     uint64_t* o = nullptr;
     const bool ok = sort_unique_impl<uint64_t>(keys, alt, n, &o, nc, s, st, top_hist, pre_off,
-                                               pre_B, tile_hist, side_dev, side_host, pre_skip);
+                                               pre_B, tile_hist, side_dev, side_host, pre_skip, sw);
     *cells = o;
     return ok;
   }
@@ -1693,7 +1820,7 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
     const bool ok = sort_unique_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(keys),
                                                  reinterpret_cast<ulonglong2*>(alt), n, &o, nc, s,
                                                  st, top_hist, pre_off, pre_B, tile_hist, side_dev,
-                                                 side_host, pre_skip);
+                                                 side_host, pre_skip, sw);
     *cells = reinterpret_cast<uint64_t*>(o);
     return ok;
   }

@@ -1,0 +1,149 @@
+"""GPU parity of the sweep path (>= 2^24 rows of ell = 64 or 128 bytes): the
+pack kernel does the MSD sort's first partition into over-allocated top-byte
+regions, the region sweep fills the top-16-bit bucket slots, the bucket pass
+sorts each slot into its output range.
+
+Inputs are too large for the oracle's std::set in seconds, so the checks use
+what the generator fixes by construction (pin P7): with random 64/128-bit
+bases every row is a cell and the distance-1 pairs are exactly the planted
+pairs.  The canonical table is the generator's words in numpy lexsort order.
+Also covered: duplicates (dedupe + compaction), a ragged tail, skewed top
+bytes that overflow a region or a bucket slot (the build re-runs on the
+exact path), and the input-byte check."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1503_06029_b200 import build_lib
+
+    build_lib.build()
+    import paper_1503_06029_b200 as cg
+
+    cg.lib()
+    return cg
+
+
+def _expected(words, pair_of):
+    """Canonical table (lexsort, word 0 most significant) and the planted
+    pairs as canonical (i < j) edges in (i, j) order."""
+    W = words.shape[1]
+    order = np.lexsort(tuple(words[:, w] for w in range(W - 1, -1, -1)))
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.size)
+    o2 = np.argsort(pair_of, kind="stable")
+    a, b = rank[o2[0::2]], rank[o2[1::2]]
+    e = np.stack([np.minimum(a, b), np.maximum(a, b)], 1).astype(np.uint32)
+    e = e[np.argsort(e[:, 0], kind="stable")]
+    return words[order], e
+
+
+def _build(cg, words, ell, **kw):
+    wt = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
+    x = synth.unpack_words_torch(wt, ell)
+    del wt
+    res = cg.build(x, want_stats=True, **kw)
+    torch.cuda.synchronize()
+    del x
+    return (res.cells.cpu().numpy().view(np.uint64), res.edges.cpu().numpy().view(np.uint32),
+            res.stats)
+
+
+def _check(cells, edges, want_c, want_e):
+    assert cells.shape == want_c.shape
+    np.testing.assert_array_equal(cells, want_c)
+    assert edges.shape == want_e.shape
+    np.testing.assert_array_equal(edges, want_e)
+
+
+def _planted(seed, n, ell, top_byte=None, second_byte=None):
+    """Planted pairs; optionally every row's top byte (and second byte) forced
+    to a constant, the planted bit then drawn below them (skewed prefixes)."""
+    words, pair_of = synth.planted_words(seed, n // 2, ell)
+    if top_byte is None:
+        return words, pair_of
+    rng = np.random.default_rng(seed + 100)
+    W = words.shape[1]
+    half = n // 2
+    base = rng.integers(0, 2**64, size=(half, W), dtype=np.uint64)
+    keep = 16 if second_byte is not None else 8
+    fixed = np.uint64(top_byte) << np.uint64(56)
+    if second_byte is not None:
+        fixed |= np.uint64(second_byte) << np.uint64(48)
+    base[:, 0] = (base[:, 0] & np.uint64((1 << (64 - keep)) - 1)) | fixed
+    k = rng.integers(keep, ell, size=half)
+    part = base.copy()
+    part[np.arange(half), k // 64] ^= np.uint64(1) << (np.uint64(63) - (k % 64).astype(np.uint64))
+    w = np.concatenate([base, part])
+    po = np.concatenate([np.arange(half), np.arange(half)]).astype(np.uint64)
+    perm = rng.permutation(n)
+    return np.ascontiguousarray(w[perm]), po[perm]
+
+
+@pytest.mark.parametrize("ell", [128, 64])
+def test_sweep_planted(cg, ell):
+    words, pair_of = _planted(7, 1 << 24, ell)
+    want_c, want_e = _expected(words, pair_of)
+    c, e, st = _build(cg, words, ell)
+    _check(c, e, want_c, want_e)
+    assert st["sort_passes"] == 1  # the sweep path ran (one region sweep)
+    c, e, st = _build(cg, words, ell, sort_kind="nosweep")
+    _check(c, e, want_c, want_e)
+    assert st["sort_passes"] == 2  # two one-sweep passes
+
+
+def test_sweep_duplicates_and_ragged_tail(cg):
+    """2^23 planted rows, a shuffled second copy and 12345 more copies: every
+    bucket has duplicates to drop and the last tile is ragged."""
+    words, pair_of = _planted(8, 1 << 23, 128)
+    want_c, want_e = _expected(words, pair_of)
+    rng = np.random.default_rng(9)
+    extra = words[rng.integers(0, words.shape[0], size=12345)]
+    allw = np.concatenate([words, words[rng.permutation(words.shape[0])], extra])
+    c, e, st = _build(cg, allw, 128)
+    _check(c, e, want_c, want_e)
+    assert st["n_in"] == allw.shape[0] and st["sort_passes"] == 1
+
+
+@pytest.mark.parametrize("second", [None, 0x3C])
+def test_sweep_overflow_falls_back(cg, second):
+    """second=None: every row has the top byte 0xA5, so one region receives
+    every row (region overflow).  second=0x3C: a uniform top byte and a
+    constant second byte, so each region's rows all land in one bucket slot
+    (slot overflow).  Both builds re-run on the exact path."""
+    if second is None:
+        words, pair_of = _planted(10, 1 << 24, 128, top_byte=0xA5)
+    else:
+        words, pair_of = _planted(11, 1 << 24, 128, top_byte=0, second_byte=second)
+        # uniform top byte, constant second byte
+        rng = np.random.default_rng(12)
+        words[:, 0] = (words[:, 0] & np.uint64((1 << 56) - 1)) | (
+            rng.integers(0, 256, size=words.shape[0], dtype=np.uint64) << np.uint64(56))
+        # the partner must keep its base's top byte: redo the pairing by value
+        order = np.argsort(pair_of, kind="stable")
+        words[order[1::2], 0] = (words[order[1::2], 0] & np.uint64((1 << 56) - 1)) | (
+            words[order[0::2], 0] & ~np.uint64((1 << 56) - 1))
+    want_c, want_e = _expected(words, pair_of)
+    c, e, st = _build(cg, words, 128)
+    _check(c, e, want_c, want_e)
+    assert st["sort_passes"] != 1  # not finished on the sweep path
+
+
+def test_sweep_input_byte_check(cg):
+    words, _ = _planted(13, 1 << 24, 128)
+    wt = torch.from_numpy(words.view(np.int64)).cuda()
+    x = synth.unpack_words_torch(wt, 128)
+    x[(1 << 24) - 3, 77] = 2
+    with pytest.raises(cg.CgError) as ei:
+        cg.build(x)
+    assert ei.value.code == -2
