@@ -152,18 +152,30 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ vecs, 
 // reorders the tile in shared memory and writes the runs.  A region that
 // would overflow sets *ovf and is clipped; the caller then re-packs and
 // takes the exact path.
-constexpr int kSweepThreads = 512;
-constexpr int kSweepRPT = 8;  // rows per thread in the rank phase
+#ifndef SWEEP_NT
+#define SWEEP_NT 256  // threads per CTA (A/B at C5: 512 x 2 CTAs 1.66 ms, 256 x 4 1.54, 256 x 3 1.71)
+#endif
+#ifndef SWEEP_RPT
+#define SWEEP_RPT 8  // rows per thread in the rank phase
+#endif
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 4  // resident CTAs per SM (register bound: 64 registers)
+#endif
+#ifndef SWEEP_U
+#define SWEEP_U 8  // 16-byte loads in flight per thread
+#endif
+constexpr int kSweepThreads = SWEEP_NT;
+constexpr int kSweepRPT = SWEEP_RPT;
 constexpr int kSweepRows = kSweepThreads * kSweepRPT;
 
 template <int W>
-__global__ void __launch_bounds__(kSweepThreads, 2) k_pack_sweep(
+__global__ void __launch_bounds__(kSweepThreads, SWEEP_MINB) k_pack_sweep(
     const uint8_t* __restrict__ vecs, int64_t n, uint64_t* __restrict__ regions, uint32_t capr,
     uint32_t* __restrict__ rcnt, uint32_t* __restrict__ err, uint32_t* __restrict__ ovf) {
   constexpr int C = 4 * W;  // 16-byte chunks per row (ell = 64 W bytes)
   constexpr int TR = kSweepRows, NT = kSweepThreads;
   constexpr int STEPS = TR * C / NT;  // chunk loads per thread
-  constexpr int U = 8;                // loads in flight per thread
+  constexpr int U = SWEEP_U;          // loads in flight per thread
   static_assert(STEPS % U == 0, "sweep tile");
   extern __shared__ __align__(16) uint64_t sk[];  // [TR][W]
   __shared__ uint32_t hc[256], dex[256], lim[256], s_scan[33];
