@@ -233,13 +233,25 @@ __global__ void __launch_bounds__(kSortThreads, OS_MINB)
 // shared atomics and each (tile, bucket) run is reserved in the bucket's
 // slot of cap16 rows with one global atomicAdd -- no look-back.  Block
 // x * tpr + t takes tile t of region x.
+#ifndef RS_IPT
+#define RS_IPT 12  // region sweep: 16-byte keys per thread and tile
+#endif
+#ifndef RS_MINB
+#define RS_MINB 3  // region sweep: resident CTAs per SM
+#endif
 template <class K>
-__global__ void __launch_bounds__(kSortThreads, OS_MINB)
+struct RsCfg {
+  static constexpr int IPT = sizeof(K) == 16 ? RS_IPT : 2 * RS_IPT;
+  static constexpr int TILE = kSortThreads * IPT;
+  static constexpr size_t SMEM = size_t(TILE) * sizeof(K);
+};
+template <class K>
+__global__ void __launch_bounds__(kSortThreads, RS_MINB)
     k_region_sweep(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
                    uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
                    uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf) {
-  constexpr int IPT = TileCfg<K, false>::IPT;
-  constexpr int TILE = TileCfg<K, false>::TILE;
+  constexpr int IPT = RsCfg<K>::IPT;
+  constexpr int TILE = RsCfg<K>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* skeys = reinterpret_cast<K*>(smem_raw);
   __shared__ uint32_t wcnt[kSortWarps][kRadix];
@@ -1750,12 +1762,12 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
     slots.alloc(size_t(nb) * cap16, s);
     DevBuf<uint32_t> cnt16(size_t(nb), s);
     CG_CUDA(cudaMemsetAsync(cnt16.p, 0, cnt16.n * 4, s));
-    constexpr int TILE = TileCfg<K, false>::TILE;
+    constexpr int TILE = RsCfg<K>::TILE;
     const uint32_t tpr = (sw->capr + TILE - 1) / TILE;
     CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(TileCfg<K, false>::SMEM)));
-    k_region_sweep<K><<<unsigned(256 * tpr), kSortThreads, TileCfg<K, false>::SMEM, s>>>(
+                                 int(RsCfg<K>::SMEM)));
+    k_region_sweep<K><<<unsigned(256 * tpr), kSortThreads, RsCfg<K>::SMEM, s>>>(
         reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16, cnt16.p,
         sw->ovf);
     CG_LAUNCH_CHECK();
