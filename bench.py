@@ -133,10 +133,13 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
     K = 8 * W
     nc, m = st["n_cells"], st["n_edges"]
     dict_b = st.get("dict_bytes", 0)
-    # MSD path (W <= 2): 2 top-digit one-sweep passes + the bucket pass, each
-    # reads and writes every key; W > 2: word-0 gather, 8 passes over
-    # (u64 word 0, u32 index) pairs, one row gather (tie fixes not counted)
-    sort_key_bytes = 6 * K if W <= 2 else 8 + 8 * 2 * 12 + (K + 4) + K
+    # MSD path (W <= 2): the top-digit passes (sort_passes: 2 one-sweep
+    # passes, or 1 region sweep on the sweep path, whose first partition ran
+    # inside the pack) + the bucket pass, each reads and writes every key;
+    # W > 2: word-0 gather, 8 passes over (u64 word 0, u32 index) pairs, one
+    # row gather (tie fixes not counted)
+    passes = int(st.get("sort_passes", 2)) if W <= 2 else 0
+    sort_key_bytes = (passes + 1) * 2 * K if W <= 2 else 8 + 8 * 2 * 12 + (K + 4) + K
     # the probe kernel's work unit is a tile of 32 cells (probe_global.cu
     # kTileCells); per tile it writes a u32 count and a u64 block position
     tiles = (nc + 31) // 32
