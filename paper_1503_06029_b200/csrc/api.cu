@@ -405,9 +405,18 @@ struct GlobalOut {
   uint32_t* F = nullptr;
 };
 
+// PreIndex: T/F already written by the sweep path's bucket pass for b = pre_b
+// (b + 5-bit filter); used when the dictionary here has that shape.
+struct PreIndex {
+  DevBuf<uint32_t>* T = nullptr;
+  DevBuf<uint32_t>* F = nullptr;
+  int b = -1;
+};
+
 static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* src_pos,
                          const uint32_t* idx, int64_t n_src, int W, int ell, const cg_opts& o,
-                         bool keep_index, StageTimer& tm, GlobalOut* go) {
+                         bool keep_index, StageTimer& tm, GlobalOut* go,
+                         const PreIndex& pre = PreIndex()) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int64_t nc = nrows;
   {
@@ -426,21 +435,26 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     const bool hash = o.dict_kind == CG_DICT_HASH;
     int lb = 0;
     while (hash && (int64_t(1) << lb) * 2 < nc) ++lb;
-    DevBuf<uint32_t> T(hash ? 1 : (size_t(1) << b) + 1, s, gix);
-    DevBuf<uint32_t> F(hash ? 1 : std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
+    const bool fused = pre.T && pre.T->p && !hash && b == pre.b && fextra == 5;
+    DevBuf<uint32_t> T(hash || fused ? 1 : (size_t(1) << b) + 1, s, gix);
+    DevBuf<uint32_t> F(hash || fused ? 1 : std::max<size_t>(1, (size_t(1) << (b + fextra)) / 32), s, gix);
+    uint32_t* Tp = fused ? pre.T->p : T.p;
+    uint32_t* Fp = fused ? pre.F->p : F.p;
     DevBuf<uint64_t> Z(hash ? size_t(ell) : 1, s), slots(hash ? (size_t(4) << lb) : 1, s),
         hv(hash ? size_t(nc) : 1, s);
     int64_t dict_bytes = 0;
     if (hash) {
       build_hash_dict(keys, nc, W, ell, lb, Z.p, slots.p, hv.p, s);
       dict_bytes = int64_t(slots.n + hv.n + Z.n) * 8;
+    } else if (fused) {  // written by the bucket pass (sweep path)
+      dict_bytes = int64_t(pre.T->n) * 4 + int64_t(pre.F->n) * 4;
     } else {
       CG_CUDA(cudaMemsetAsync(F.p, 0, F.n * 4, s));
       dict_bytes = int64_t(T.n) * 4 + int64_t(F.n) * 4;
       build_global_index(keys, nc, W, b, fextra, T.p, F.p, s);
     }
     tm.mark();  // 5: dict
-    GlobalDict g{keys, nullptr, T.p, F.p, b, fextra, W, ell, nc};
+    GlobalDict g{keys, nullptr, Tp, Fp, b, fextra, W, ell, nc};
     g.src_pos = src_pos;
     g.idx = idx;
     if (hash) {
@@ -541,8 +555,8 @@ static void global_probe(const uint64_t* keys, int64_t nrows, const uint32_t* sr
     go->b = b;
     go->fextra = fextra;
     if (keep_index) {
-      go->T = T.release();
-      go->F = F.release();
+      go->T = fused ? pre.T->release() : T.release();
+      go->F = fused ? pre.F->release() : F.release();
     }
   }
 }
@@ -582,12 +596,34 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   // read-back would cost every distinct-input build.)
   const bool dupy_msd = msd && !sw && !sh.cells_only && pre_off == nullptr && n >= (int64_t(1) << 18) &&
                         n < (int64_t(1) << 24) && sample_duplicates(keys.p, n, W, s) >= 8;
+  // the sweep path's bucket pass can write the global dictionary's index
+  // (T, F) of the table it produces: shaped for b from n (= nc without
+  // duplicates, the case it is for; global_probe falls back to the index
+  // pass when b(nc) differs)
+  DevBuf<uint32_t> preT, preF;
+  PreIndex pre;
+  SweepIn swx = sw ? *sw : SweepIn{};
+  if (sw && !sh.cells_only && (o.dict_kind == CG_DICT_GLOBAL || o.dict_kind == CG_DICT_AUTO) &&
+      (o.filter_extra < 0 || o.filter_extra == 5) && o.bucket_log2 <= 0) {
+    int bp = 0;
+    while (bp < 28 && (uint64_t(n) >> (bp + 1)) >= 1) ++bp;
+    if (bp >= 16 && bp <= 26) {
+      const Mem gix = o.index_out ? Mem::Persist : Mem::Scratch;
+      preT.alloc((size_t(1) << bp) + 1, s, gix);
+      preF.alloc(size_t(1) << bp, s, gix);
+      pre = PreIndex{&preT, &preF, bp};
+      swx.T = preT.p;
+      swx.F = preF.p;
+      swx.b = bp;
+    }
+  }
   if (msd && !dupy_msd) {
     uint64_t* ko = nullptr;
     int64_t ncu = 0;
     const bool fused = !keys.scratch && !alt.scratch;
     done = (fused || sw) ? sort_unique_msd(keys.p, alt.p, n, W, &ko, &ncu, s, &sst, top_hist, pre_off,
-                                           pre_B, tile_hist, d_flags, &in_err, sh.pre_skip, sw)
+                                           pre_B, tile_hist, d_flags, &in_err, sh.pre_skip,
+                                           sw ? &swx : nullptr)
                          : sort_rows_msd(keys.p, alt.p, n, W, &ko, s, &sst, top_hist);
     if (sw && !done) {  // a region or bucket slot overflowed: the caller re-packs
       *sweep_failed = true;
@@ -705,7 +741,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
     if (od.dict_kind == CG_DICT_AUTO)
       od.dict_kind = (W > 2 && !o.index_out && nc * 4 <= n) ? CG_DICT_HASH : CG_DICT_GLOBAL;
     GlobalOut go;
-    global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, od, o.index_out != nullptr, tm, &go);
+    global_probe(cellbuf.p, nc, nullptr, nullptr, nc, W, ell, od, o.index_out != nullptr, tm, &go,
+                 pre);
     const uint64_t m = uint64_t(go.m);
     uint64_t* eout = go.edges;
     const int b = go.b, fextra = go.fextra;

@@ -13,11 +13,17 @@ namespace cgk {
 // digit dlo per tile of tile_rows rows (the first one-sweep pass's tiles).
 // The sweep path's input to sort_unique_msd (sw): launch_pack_sweep's regions
 // (u64[256][capr][W]), their row counts rcnt[256] and the overflow flag.
+// T/F (optional, b in [16, 26]): the bucket pass also writes the prefix index
+// T[2^b + 1] and the b + 5-bit filter F[2^b] of the sorted unique table
+// (the global dictionary of probe_global.cu) -- no separate index pass.
 struct SweepIn {
   const uint64_t* regions;
   uint32_t capr;
   const uint32_t* rcnt;
   uint32_t* ovf;
+  uint32_t* T = nullptr;
+  uint32_t* F = nullptr;
+  int b = 0;
 };
 // Pack + the MSD sort's first partition (the "sweep" path, ell = 64 W,
 // W <= 2): rows go to 256 regions of capr rows by the top byte of word 0,

@@ -852,7 +852,8 @@ template <class K, int MAXC, bool PREF>
 __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
-                  uint32_t* __restrict__ nlist, const K* __restrict__ src, uint32_t scap) {
+                  uint32_t* __restrict__ nlist, const K* __restrict__ src, uint32_t scap,
+                  uint32_t* __restrict__ Tix, uint32_t* __restrict__ Fix, int ib) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // PREF: the next bucket is prefetched (cp.async) into a second buffer;
   // otherwise one buffer and more resident CTAs hide the load latency
@@ -870,7 +871,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     return d >= uint32_t(kBins) ? uint32_t(kBins) : (d % kPer) * kBktThreads + d / kPer;
   };
   __shared__ uint32_t s_nmany;
-  __shared__ uint32_t h[kBins + 1];
+  __shared__ __align__(16) uint32_t h[kBins + 1];
   __shared__ uint32_t s_scan[33];
   __shared__ uint64_t s_red[2][kBktWarps][2];
   __shared__ uint32_t s_wc[MAXC * kBktWarps];
@@ -939,6 +940,56 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     const int S = int(hi - lo);
     // a listed bucket is finished in place by the byte-pass kernel: on the
     // sweep path its rows are first copied to their output range
+    // Fused prefix index (sweep path): bucket bk owns the
+    // 2^(ib-16) entries of T and words of F (b + 5-bit filter) under its top
+    // 16 bits; its distinct cells are counted per ib-bit prefix and OR'ed
+    // into the filter words in shared memory (h is free at those points),
+    // then T (bucket start + exclusive count) and F are written once --
+    // no separate pass over the table, no global atomics, no memset of F.
+    const int ixs = Tix ? ib - 16 : 0, ixn = 1 << ixs;
+    uint32_t* ixc = h;           // [ixn] cells per ib-bit prefix
+    uint32_t* ixf = h + 1024;    // [ixn] filter words
+    auto ix_zero = [&]() {
+      for (int q = tid; q < ixn; q += kBktThreads) ixc[q] = ixf[q] = 0u;
+    };
+    auto ix_add = [&](const K& k) {
+      const uint64_t t = KT<K>::top(k);
+      const uint32_t x = uint32_t(t >> (64 - ib)) & uint32_t(ixn - 1);
+      atomicAdd(&ixc[x], 1u);
+      atomicOr(&ixf[x], 1u << (uint32_t(t >> (64 - ib - 5)) & 31u));
+    };
+    auto ix_write = [&](int64_t b2, uint32_t base) {  // after a barrier
+      constexpr int PER = 1024 / kBktThreads;
+      uint32_t cv[PER], loc = 0;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int q = tid * PER + u;
+        cv[u] = q < ixn ? ixc[q] : 0u;
+        loc += cv[u];
+      }
+      uint32_t tot;
+      uint32_t run = block_excl_scan(loc, s_scan, &tot);
+      const size_t g0 = size_t(b2) << ixs;
+      static_assert(PER == 4, "one 16-byte store per array and thread");
+      if (tid * PER < ixn) {  // (ixn >= 4 when ixs >= 2; else one entry per thread)
+        uint4 tv, fv;
+        tv.x = base + run;
+        tv.y = tv.x + cv[0];
+        tv.z = tv.y + cv[1];
+        tv.w = tv.z + cv[2];
+        if (ixn >= 4) {
+          fv = *reinterpret_cast<const uint4*>(ixf + tid * PER);
+          *reinterpret_cast<uint4*>(Tix + g0 + tid * PER) = tv;
+          *reinterpret_cast<uint4*>(Fix + g0 + tid * PER) = fv;
+        } else {
+          const uint32_t t4[4] = {tv.x, tv.y, tv.z, tv.w};
+          for (int u = 0; u < PER && tid * PER + u < ixn; ++u) {
+            Tix[g0 + tid * PER + u] = t4[u];
+            Fix[g0 + tid * PER + u] = ixf[tid * PER + u];
+          }
+        }
+      }
+    };
     auto list_bucket = [&]() {
       if (src)
         for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = rsrc(bk, lo)[i];
@@ -948,6 +999,13 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     if (S <= 1) {
       if (ucnt && tid == 0) ucnt[bk] = uint32_t(S);
       if (src && S == 1 && tid == 0) keys[lo] = s[0];
+      if (Tix) {  // the bucket's slice of the prefix index: at most one cell
+        ix_zero();
+        __syncthreads();
+        if (S == 1 && tid == 0) ix_add(s[0]);
+        __syncthreads();
+        ix_write(bk, lo);
+      }
       __syncthreads();
       continue;
     }
@@ -1015,6 +1073,14 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
         }
       } else {
         for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[i];
+      }
+      if (Tix) {  // one distinct cell
+        __syncthreads();
+        ix_zero();
+        __syncthreads();
+        if (tid == 0) ix_add(s[0]);
+        __syncthreads();
+        ix_write(bk, lo);
       }
       __syncthreads();
       continue;
@@ -1120,6 +1186,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     } else {
       uint32_t bl[MAXC];
       K sv[MAXC];
+      if (Tix) ix_zero();  // (h is free after the permutation)
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int i = c * kBktThreads + tid;
@@ -1129,6 +1196,11 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
         if (lane == 0) s_wc[c * kBktWarps + wid] = __popc(bl[c]);
       }
       __syncthreads();
+      if (Tix) {
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c)
+          if ((bl[c] >> lane) & 1u) ix_add(sv[c]);
+      }
       if (tid < 32) {
         constexpr int NWC = MAXC * kBktWarps;
         constexpr int PER = (NWC + 31) / 32;
@@ -1158,11 +1230,70 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
         if ((bl[c] >> lane) & 1u)
           keys[lo + s_wc[c * kBktWarps + wid] + __popc(bl[c] & lt)] = sv[c];
       }
+      if (Tix) ix_write(bk, lo);  // (the atomics above precede the last barrier)
     }
     __syncthreads();
   }
   cp_async_wait0();
 }
+
+// Index slices (see k_bucket_rank's fused prefix index) of the buckets listed
+// to the byte-pass kernel, from their finished (deduplicated) rows.
+template <class K>
+__global__ void __launch_bounds__(256)
+    k_bucket_slices(const K* __restrict__ keys, const uint32_t* __restrict__ off,
+                    const uint32_t* __restrict__ ucnt, const uint32_t* __restrict__ blist,
+                    const uint32_t* __restrict__ nlist, uint32_t* __restrict__ Tix,
+                    uint32_t* __restrict__ Fix, int ib) {
+  __shared__ uint32_t ixc[1024], ixf[1024], s_scan[33];
+  const int tid = threadIdx.x, ixs = ib - 16, ixn = 1 << ixs;
+  const uint32_t nl = *nlist;
+  for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+    const uint32_t bk = blist[q], lo = off[bk], u = ucnt[bk];
+    for (int r = tid; r < ixn; r += 256) ixc[r] = ixf[r] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < u; i += 256) {
+      const uint64_t t = KT<K>::top(keys[lo + i]);
+      const uint32_t x = uint32_t(t >> (64 - ib)) & uint32_t(ixn - 1);
+      atomicAdd(&ixc[x], 1u);
+      atomicOr(&ixf[x], 1u << (uint32_t(t >> (64 - ib - 5)) & 31u));
+    }
+    __syncthreads();
+    uint32_t cv[4], loc = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = tid * 4 + v;
+      cv[v] = r < ixn ? ixc[r] : 0u;
+      loc += cv[v];
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan(loc, s_scan, &tot);
+    const size_t g0 = size_t(bk) << ixs;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = tid * 4 + v;
+      if (r < ixn) {
+        Tix[g0 + r] = lo + run;
+        Fix[g0 + r] = ixf[r];
+      }
+      run += cv[v];
+    }
+    __syncthreads();
+  }
+}
+
+// duplicates were dropped: the buckets moved from off[] to uoff[]
+__global__ void k_fix_index(uint32_t* __restrict__ T, int ib, const uint32_t* __restrict__ off,
+                            const uint32_t* __restrict__ uoff) {
+  const int64_t n = int64_t(1) << ib;
+  for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t bk = x >> (ib - 16);
+    T[x] -= off[bk] - uoff[bk];
+  }
+}
+
+__global__ void k_ix_end(uint32_t* p, uint32_t v) { *p = v; }
 
 int grid_for(int64_t n, int threads, int per_sm = 8) {
   int64_t b = (n + threads - 1) / threads;
@@ -1176,7 +1307,8 @@ int grid_for(int64_t n, int threads, int per_sm = 8) {
 template <class K>
 void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
                         uint32_t* ucnt, cudaStream_t s, const K* src = nullptr,
-                        uint32_t scap = 0) {
+                        uint32_t scap = 0, uint32_t* Tix = nullptr, uint32_t* Fix = nullptr,
+                        int ib = 0) {
   const int64_t avg = (n + nb - 1) / nb;
   const int cap = avg <= 1024 ? 2048 : 4096;
   DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
@@ -1191,7 +1323,8 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
     auto go = [&](auto kern) {
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p, src, scap);
+      kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p, src, scap, Tix,
+                                           Fix, ib);
     };
     if (rcap <= 1280) go(k_bucket_rank<K, 5, true>);
     else if (rcap <= 1536) go(k_bucket_rank<K, 6, true>);
@@ -1209,6 +1342,11 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
     k_bucket_sort<K, 16><<<grid, kBktThreads, smem, s>>>(ko, off, nb, cap, B, flag, ucnt, blist.p, nlist.p);
   }
   CG_LAUNCH_CHECK();
+  if (Tix) {  // index slices of the buckets the byte-pass kernel finished
+    k_bucket_slices<K><<<unsigned(num_sms() * 2), 256, 0, s>>>(ko, off, ucnt, blist.p, nlist.p,
+                                                               Tix, Fix, ib);
+    CG_LAUNCH_CHECK();
+  }
 }
 
 // bases[d][b] = exclusive scan of hist[d][0..256) (one block per digit)
@@ -1781,8 +1919,9 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   }
   // the bucket kernels skip the key bytes every key of a bucket shares: the
   // top pre_skip + B bits
+  uint32_t* Tix = sw ? sw->T : nullptr;
   launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s, sw ? slots.p : nullptr,
-                        cap16);
+                        cap16, Tix, Tix ? sw->F : nullptr, Tix ? sw->b : 0);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
   uint32_t* h = static_cast<uint32_t*>(host_stage(5 * sizeof(uint32_t)));
@@ -1799,6 +1938,14 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   if (h[0] || h[4]) return false;
   const int64_t total = int64_t(h[1]) + int64_t(h[2]);
   *nc = total;
+  if (Tix) {  // the fused prefix index: final positions and the end sentinel
+    if (total != n) {
+      k_fix_index<<<grid_for(int64_t(1) << sw->b, 256), 256, 0, s>>>(Tix, sw->b, offp, uoff.p);
+      CG_LAUNCH_CHECK();
+    }
+    k_ix_end<<<1, 1, 0, s>>>(Tix + (size_t(1) << sw->b), uint32_t(total));
+    CG_LAUNCH_CHECK();
+  }
   if (total != n) {  // duplicates removed: close the gaps between buckets
     K* dst = (ko == keys) ? alt : keys;
     const int64_t blocks = std::min<int64_t>((nb * 32 + 255) / 256, int64_t(num_sms()) * 16);
