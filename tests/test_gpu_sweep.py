@@ -102,14 +102,23 @@ def test_sweep_planted(cg, ell):
     assert st["sort_passes"] == 2  # two one-sweep passes
 
 
-def test_sweep_duplicates_and_ragged_tail(cg):
-    """2^23 planted rows, a shuffled second copy and 12345 more copies: every
-    bucket has duplicates to drop and the last tile is ragged."""
-    words, pair_of = _planted(8, 1 << 23, 128)
+@pytest.mark.parametrize("distinct_log2,copies", [(23, None), (24, 1 << 21)])
+def test_sweep_duplicates_and_ragged_tail(cg, distinct_log2, copies):
+    """Duplicates dropped by the bucket pass and the buckets compacted.
+    (23, None): 2^23 planted rows, a shuffled second copy and 12345 more
+    copies -- every bucket has duplicates, the last tile is ragged, and the
+    table (2^23 cells) is too small for the index shaped from n (the index
+    pass runs).  (24, 2^21): 2^24 + 2^22 planted rows plus 2^21 + 12345
+    copies -- the fused index of the bucket pass is kept and shifted to the
+    compacted positions (k_fix_index)."""
+    n0 = (1 << distinct_log2) + (0 if copies is None else 1 << 22)
+    words, pair_of = _planted(8, n0, 128)
     want_c, want_e = _expected(words, pair_of)
     rng = np.random.default_rng(9)
     extra = words[rng.integers(0, words.shape[0], size=12345)]
-    allw = np.concatenate([words, words[rng.permutation(words.shape[0])], extra])
+    dup = words[rng.permutation(words.shape[0])] if copies is None else \
+        words[rng.integers(0, words.shape[0], size=copies)]
+    allw = np.concatenate([words, dup, extra])
     c, e, st = _build(cg, allw, 128)
     _check(c, e, want_c, want_e)
     assert st["n_in"] == allw.shape[0] and st["sort_passes"] == 1
