@@ -124,7 +124,8 @@ typedef struct {
                            prefix/LSD sorts beyond, full LSD fallback; >= 2^24 rows of
                            ell = 64 or 128 bytes: the sweep path, the pack kernel doing the
                            first MSD partition), 1 = full LSD only, 2 = auto without the
-                           one-CTA small path, 3 = auto without the sweep path */
+                           one-CTA small path, 3 = auto without the sweep path, 4 = auto
+                           with the sweep path at any size (2^18 < n <= 2^26) */
   cg_index** index_out; /* if non-NULL, receives the dictionary (release with cg_index_free) */
   cg_stats* stats;      /* if non-NULL, stage times and counters */
   int32_t filter_extra; /* prefix filter resolution: b + filter_extra prefix bits per filter

@@ -274,7 +274,7 @@ class BuildResult:
     index: Index | None = None
 
 
-SORT_KINDS = {"auto": 0, "lsd": 1, "nosmall": 2, "nosweep": 3}
+SORT_KINDS = {"auto": 0, "lsd": 1, "nosmall": 2, "nosweep": 3, "sweep": 4}
 
 
 def _opts(stream, dict_kind, lcp_prune, bucket_log2, want_index, want_stats, sort_kind="auto",

@@ -934,7 +934,7 @@ static void validate_opts(const cg_opts& o) {
     throw CgError{CG_ENOTIMPL, "dict_kind not implemented"};
   if (o.filter_extra < -1 || o.filter_extra > 8) throw CgError{CG_EINVAL, "filter_extra must be in [-1, 8]"};
   if (o.edge_cap < 0) throw CgError{CG_EINVAL, "edge_cap must be >= 0"};
-  if (o.sort_kind < 0 || o.sort_kind > 3) throw CgError{CG_EINVAL, "sort_kind must be 0, 1, 2 or 3"};
+  if (o.sort_kind < 0 || o.sort_kind > 4) throw CgError{CG_EINVAL, "sort_kind must be in [0, 4]"};
   if (o.reserved0 != 0) throw CgError{CG_EINVAL, "reserved0 must be 0"};
 }
 
@@ -1025,7 +1025,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     // the sweep path (large 64/128-bit rows): the pack kernel does the MSD
     // sort's first partition, the second needs no look-back
     bool swept = false;
-    if (vecs && msd && o.sort_kind != 3 && B == 16 && pack_sweep_ok(vecs, n, ell)) {
+    if (vecs && msd && o.sort_kind != 3 && B == 16 && pack_sweep_ok(vecs, n, ell, o.sort_kind == 4)) {
       const uint32_t capr = pack_sweep_capr(n);
       bool failed = false;
       {

@@ -399,7 +399,7 @@ def test_filter_resolution(cg, fextra, dict_kind):
 
 def test_bad_options_rejected(cg):
     x = torch.zeros((10, 8), dtype=torch.uint8, device="cuda")
-    for kw in (dict(filter_extra=9), dict(filter_extra=-2), dict(edge_cap=-1)):
+    for kw in (dict(filter_extra=9), dict(filter_extra=-2), dict(edge_cap=-1), dict(sort_kind=5)):
         with pytest.raises(cg.CgError) as ei:
             cg.build(x, **kw)
         assert ei.value.code == -1

@@ -156,3 +156,31 @@ def test_sweep_input_byte_check(cg):
     with pytest.raises(cg.CgError) as ei:
         cg.build(x)
     assert ei.value.code == -2
+
+
+# ---------------------------------------------------------------- forced sweep vs the oracle
+# sort_kind="sweep" takes the sweep path at any size with 2^18 < n <= 2^26, so
+# the oracle (ORACLE-A, std::set + flip lookup) can check it element by element.
+@pytest.mark.parametrize("case", ["planted128_ragged", "planted64_dups", "clustered128"])
+def test_sweep_forced_vs_oracle(cg, case):
+    import oracle
+
+    if case == "planted128_ragged":
+        x, _ = synth.planted_bytes(21, (1 << 18) + 77, 128)
+    elif case == "planted64_dups":
+        x0, _ = synth.planted_bytes(22, 1 << 18, 64)
+        rng = np.random.default_rng(23)
+        x = np.concatenate([x0, x0[rng.integers(0, x0.shape[0], size=150001)]])
+    else:  # few centres: skewed top bytes (region overflow -> the exact path)
+        x = synth.clustered_bytes(24, 300000, 128, n_centers=8, max_flips=3)
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    res = cg.build(xt, want_stats=True, sort_kind="sweep")
+    torch.cuda.synchronize()
+    cells = res.cells.cpu().numpy().view(np.uint64)
+    edges = res.edges.cpu().numpy().view(np.uint32)
+    rc, oc, oe = oracle.build(x)
+    assert rc == 0
+    _check(cells, edges, oc, oe)
+    if case != "clustered128":
+        assert res.stats["sort_passes"] == 1  # finished on the sweep path
+

@@ -26,6 +26,14 @@ for x in cases:
             r.index.query(q)
         torch.cuda.synchronize()
         del r
+# the sweep path (pack partition, region sweep, slot-reading bucket pass with
+# the fused prefix index), forced at a size the sanitizers finish
+xs, _ = synth.planted_bytes(5, (1 << 17) + 500, 128)
+xs = np.concatenate([xs, xs[:3000]])
+r = cg.build(torch.from_numpy(xs).cuda(), sort_kind="sweep", want_stats=True)
+torch.cuda.synchronize()
+assert r.stats["sort_passes"] == 1, r.stats["sort_passes"]
+del r
 print("sanitize build paths ok")
 
 # rows f1-f4 on small inputs
