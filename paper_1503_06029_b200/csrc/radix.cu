@@ -287,15 +287,12 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
   }
   uint32_t tile_n;
   const uint32_t dex = block_excl_scan(total, s_scan, &tile_n);
+  // the reservation's result is first used after the shared-memory scatter:
+  // its L2 round trip overlaps the scatter
   uint32_t base = 0;
   const uint32_t q = (x << 8) | uint32_t(tid);
-  if (total) {
-    base = atomicAdd(&cnt16[q], total);
-    if (uint64_t(base) + total > cap16) atomicOr(ovf, 1u);
-  }
+  if (total) base = atomicAdd(&cnt16[q], total);
   s_dexcl[tid] = dex;
-  s_gbase[tid] = q * cap16 + base - dex;  // slot row of local position dex + r: s_gbase + dex + r
-  s_lim[tid] = dex + (base < cap16 ? cap16 - base : 0u);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
@@ -304,6 +301,9 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
       skeys[s_dexcl[d] + wcnt[w][d] + rank[i]] = key[i];
     }
   }
+  if (total && uint64_t(base) + total > cap16) atomicOr(ovf, 1u);
+  s_gbase[tid] = q * cap16 + base - dex;  // slot row of local position dex + r: s_gbase + dex + r
+  s_lim[tid] = dex + (base < cap16 ? cap16 - base : 0u);
   __syncthreads();
   for (int j = tid; j < nt; j += kSortThreads) {
     const K k = skeys[j];
