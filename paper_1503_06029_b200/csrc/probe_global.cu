@@ -1095,6 +1095,7 @@ void launch_spill_place(const GlobalDict& g, const uint64_t* sorted, int64_t m, 
 // memory -- and writes one contiguous run as (i, j) u32 pairs.  Overflow
 // tiles (pos = ~0) are written by the spill path and skipped here.
 constexpr int kCopyTiles = 256;
+constexpr int kCopyMap = 16384;  // (bytes of shared memory for the element -> tile map)
 
 __global__ void __launch_bounds__(256)
     k_tile_copy(const uint64_t* __restrict__ scratch, const uint64_t* __restrict__ off,
@@ -1102,6 +1103,7 @@ __global__ void __launch_bounds__(256)
                 uint64_t* __restrict__ out) {
   __shared__ uint32_t s_pre[kCopyTiles + 1];
   __shared__ uint64_t s_pos[kCopyTiles];
+  __shared__ uint8_t s_tile[kCopyMap];  // destination element -> its tile (E <= kCopyMap)
   for (int64_t t0 = int64_t(blockIdx.x) * kCopyTiles; t0 < ntiles;
        t0 += int64_t(gridDim.x) * kCopyTiles) {
     const int nt = int(ntiles - t0 < kCopyTiles ? ntiles - t0 : int64_t(kCopyTiles));
@@ -1115,6 +1117,14 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) s_pre[nt] = uint32_t(off[t0 + nt - 1] - base) + cntv[t0 + nt - 1];
     __syncthreads();
     const uint32_t E = s_pre[nt];
+    // each tile marks its destination elements (one shared byte each, no
+    // per-element binary search) when the 256 tiles hold <= kCopyMap edges
+    const bool map = E <= uint32_t(kCopyMap);
+    if (map) {
+      for (int q = threadIdx.x; q < nt; q += blockDim.x)
+        for (uint32_t e = s_pre[q]; e < s_pre[q + 1]; ++e) s_tile[e] = uint8_t(q);
+      __syncthreads();
+    }
     // 4 edges per thread and step: all four loads in flight before the stores
     constexpr int U = 4;
     for (uint32_t e0 = threadIdx.x; e0 < E; e0 += U * blockDim.x) {
@@ -1126,11 +1136,13 @@ __global__ void __launch_bounds__(256)
         src[u] = ~0ull;
         if (e < E) {
           int lo = 0, hi = nt - 1;  // last tile with s_pre <= e
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pre[mid] <= e) lo = mid;
-            else hi = mid - 1;
-          }
+          if (map) lo = s_tile[e];
+          else
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (s_pre[mid] <= e) lo = mid;
+              else hi = mid - 1;
+            }
           const uint64_t p = s_pos[lo];
           if (p != ~0ull) src[u] = p + (e - s_pre[lo]);
         }

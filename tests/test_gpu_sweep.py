@@ -184,3 +184,30 @@ def test_sweep_forced_vs_oracle(cg, case):
     if case != "clustered128":
         assert res.stats["sort_passes"] == 1  # finished on the sweep path
 
+
+
+def test_sweep_index_kept_for_query(cg):
+    """want_index on the sweep path: the prefix index the bucket pass wrote is
+    handed to the caller; cg_query answers every cell and random rows like
+    the oracle (self index and the neighbour list per flipped bit)."""
+    import oracle
+    from helpers import words_from_rows
+
+    x0, _ = synth.planted_bytes(31, (1 << 18) + 5, 128)
+    rng = np.random.default_rng(32)
+    x = np.concatenate([x0, x0[rng.integers(0, x0.shape[0], size=4099)]])
+    res = cg.build(torch.from_numpy(x).cuda(), want_index=True, want_stats=True, sort_kind="sweep")
+    torch.cuda.synchronize()
+    assert res.stats["sort_passes"] == 1
+    cells = res.cells.cpu().numpy().view(np.uint64)
+    idx = res.index
+    assert idx is not None and idx.n_cells == cells.shape[0]
+    extra = synth.random_bytes(33, 3000, 128)
+    sel = cells[rng.integers(0, cells.shape[0], size=20000)]
+    q = np.concatenate([sel, words_from_rows(extra)])
+    s, nb = idx.query(torch.from_numpy(q.view(np.int64)).cuda())
+    torch.cuda.synchronize()
+    rc, os_, onb = oracle.query(cells, 128, q)
+    assert rc == 0
+    np.testing.assert_array_equal(s.cpu().numpy(), os_)
+    np.testing.assert_array_equal(nb.cpu().numpy(), onb)
