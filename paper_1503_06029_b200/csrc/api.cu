@@ -607,7 +607,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
       (o.filter_extra < 0 || o.filter_extra == 5) && o.bucket_log2 <= 0) {
     int bp = 0;
     while (bp < 28 && (uint64_t(n) >> (bp + 1)) >= 1) ++bp;
-    if (bp >= 16 && bp <= 26) {
+    if (bp - (8 + swx.B2) >= 0 && bp - (8 + swx.B2) <= 10) {  // <= 1024 entries per bucket
       const Mem gix = o.index_out ? Mem::Persist : Mem::Scratch;
       preT.alloc((size_t(1) << bp) + 1, s, gix);
       preF.alloc(size_t(1) << bp, s, gix);
@@ -1025,7 +1025,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     // the sweep path (large 64/128-bit rows): the pack kernel does the MSD
     // sort's first partition, the second needs no look-back
     bool swept = false;
-    if (vecs && msd && o.sort_kind != 3 && B == 16 && pack_sweep_ok(vecs, n, ell, o.sort_kind == 4)) {
+    if (vecs && msd && o.sort_kind != 3 && sweep_bits(n) > 0 &&
+        pack_sweep_ok(vecs, n, ell, o.sort_kind == 4)) {
       const uint32_t capr = pack_sweep_capr(n);
       bool failed = false;
       {
@@ -1034,7 +1035,8 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
         CG_CUDA(cudaMemsetAsync(rc.p + 256, 0, 4, s));
         launch_pack_sweep(vecs, n, ell, regions.p, capr, rc.p, flags.p, rc.p + 256, s);
         tm.mark();  // 1: pack
-        const SweepIn sw{regions.p, capr, rc.p, rc.p + 256};
+        SweepIn sw{regions.p, capr, rc.p, rc.p + 256};
+        sw.B2 = sweep_bits(n);
         build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(), nullptr, nullptr, B,
                         nullptr, &sw, &failed);
       }

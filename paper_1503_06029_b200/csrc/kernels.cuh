@@ -24,7 +24,11 @@ struct SweepIn {
   uint32_t* T = nullptr;
   uint32_t* F = nullptr;
   int b = 0;
+  int B2 = 8;  // the region sweep's digit: buckets are the top 8 + B2 bits
 };
+// B2 for n rows (~2^10 rows per top-(8 + B2)-bit bucket), 0 = no sweep path
+// (n <= 2^18 or n > 2^26)
+int sweep_bits(int64_t n);
 // Pack + the MSD sort's first partition (the "sweep" path, ell = 64 W,
 // W <= 2): rows go to 256 regions of capr rows by the top byte of word 0,
 // region d = regions[d * capr * W ..), rcnt[d] rows (unordered inside a

@@ -297,6 +297,13 @@ bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell, bool force) {
          (force || n >= (int64_t(1) << 24)) && n < (int64_t(1) << 32);
 }
 
+int sweep_bits(int64_t n) {
+  if (n <= (int64_t(1) << 18) || n > (int64_t(1) << 26)) return 0;
+  int c = 0;
+  while ((int64_t(1) << c) < n) ++c;  // ceil(log2 n)
+  return std::min(8, std::max(1, c - 18));
+}
+
 uint32_t pack_sweep_capr(int64_t n) {
   // mean region + 1/16 + two tiles: uniform top bytes never come close
   const int64_t mean = (n + 255) / 256;

@@ -245,11 +245,16 @@ struct RsCfg {
   static constexpr int TILE = kSortThreads * IPT;
   static constexpr size_t SMEM = size_t(TILE) * sizeof(K);
 };
+// the region sweep's digit: the B2 bits after the top byte
+template <class K>
+__device__ __forceinline__ uint32_t rs_digit(const K& k, int B2) {
+  return uint32_t(KT<K>::top(k) >> (56 - B2)) & ((1u << B2) - 1u);
+}
 template <class K>
 __global__ void __launch_bounds__(kSortThreads, RS_MINB)
     k_region_sweep(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
                    uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
-                   uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf) {
+                   uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2) {
   constexpr int IPT = RsCfg<K>::IPT;
   constexpr int TILE = RsCfg<K>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
   }
 #pragma unroll
   for (int i = 0; i < IPT; ++i)
-    if (wb + i * 32 + lane < nt) rank[i] = atomicAdd(&wcnt[w][digit_of(key[i], 48)], 1u);
+    if (wb + i * 32 + lane < nt) rank[i] = atomicAdd(&wcnt[w][rs_digit(key[i], B2)], 1u);
   __syncthreads();
   uint32_t total = 0;
 #pragma unroll
@@ -290,14 +295,14 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
   // the reservation's result is first used after the shared-memory scatter:
   // its L2 round trip overlaps the scatter
   uint32_t base = 0;
-  const uint32_t q = (x << 8) | uint32_t(tid);
+  const uint32_t q = (x << B2) | uint32_t(tid);
   if (total) base = atomicAdd(&cnt16[q], total);
   s_dexcl[tid] = dex;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     if (wb + i * 32 + lane < nt) {
-      const uint32_t d = digit_of(key[i], 48);
+      const uint32_t d = rs_digit(key[i], B2);
       skeys[s_dexcl[d] + wcnt[w][d] + rank[i]] = key[i];
     }
   }
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
   __syncthreads();
   for (int j = tid; j < nt; j += kSortThreads) {
     const K k = skeys[j];
-    const uint32_t d = digit_of(k, 48);
+    const uint32_t d = rs_digit(k, B2);
     if (uint32_t(j) < s_lim[d]) slots[s_gbase[d] + uint32_t(j)] = k;
   }
 }
@@ -853,7 +858,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
                   uint32_t* __restrict__ nlist, const K* __restrict__ src, uint32_t scap,
-                  uint32_t* __restrict__ Tix, uint32_t* __restrict__ Fix, int ib) {
+                  uint32_t* __restrict__ Tix, uint32_t* __restrict__ Fix, int ib, int ibits) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // PREF: the next bucket is prefetched (cp.async) into a second buffer;
   // otherwise one buffer and more resident CTAs hide the load latency
@@ -941,12 +946,12 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     // a listed bucket is finished in place by the byte-pass kernel: on the
     // sweep path its rows are first copied to their output range
     // Fused prefix index (sweep path): bucket bk owns the
-    // 2^(ib-16) entries of T and words of F (b + 5-bit filter) under its top
-    // 16 bits; its distinct cells are counted per ib-bit prefix and OR'ed
+    // 2^(ib - ibits) <= 1024 entries of T and words of F (b + 5-bit filter)
+    // under its top ibits bits; its distinct cells are counted per ib-bit prefix and OR'ed
     // into the filter words in shared memory (h is free at those points),
     // then T (bucket start + exclusive count) and F are written once --
     // no separate pass over the table, no global atomics, no memset of F.
-    const int ixs = Tix ? ib - 16 : 0, ixn = 1 << ixs;
+    const int ixs = Tix ? ib - ibits : 0, ixn = 1 << ixs;
     uint32_t* ixc = h;           // [ixn] cells per ib-bit prefix
     uint32_t* ixf = h + 1024;    // [ixn] filter words
     auto ix_zero = [&]() {
@@ -1244,12 +1249,16 @@ __global__ void __launch_bounds__(256)
     k_bucket_slices(const K* __restrict__ keys, const uint32_t* __restrict__ off,
                     const uint32_t* __restrict__ ucnt, const uint32_t* __restrict__ blist,
                     const uint32_t* __restrict__ nlist, uint32_t* __restrict__ Tix,
-                    uint32_t* __restrict__ Fix, int ib) {
+                    uint32_t* __restrict__ Fix, int ib, int ibits,
+                    const uint32_t* __restrict__ failed) {
   __shared__ uint32_t ixc[1024], ixf[1024], s_scan[33];
-  const int tid = threadIdx.x, ixs = ib - 16, ixn = 1 << ixs;
+  const int tid = threadIdx.x, ixs = ib - ibits, ixn = 1 << ixs;
+  // a bucket the byte-pass kernel could not finish has no ucnt: the whole
+  // sort is redone by the caller, the index with it
+  if (*failed) return;
   const uint32_t nl = *nlist;
   for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
-    const uint32_t bk = blist[q], lo = off[bk], u = ucnt[bk];
+    const uint32_t bk = blist[q], lo = off[bk], u = min(ucnt[bk], off[bk + 1] - lo);
     for (int r = tid; r < ixn; r += 256) ixc[r] = ixf[r] = 0u;
     __syncthreads();
     for (uint32_t i = tid; i < u; i += 256) {
@@ -1283,12 +1292,12 @@ __global__ void __launch_bounds__(256)
 }
 
 // duplicates were dropped: the buckets moved from off[] to uoff[]
-__global__ void k_fix_index(uint32_t* __restrict__ T, int ib, const uint32_t* __restrict__ off,
-                            const uint32_t* __restrict__ uoff) {
+__global__ void k_fix_index(uint32_t* __restrict__ T, int ib, int ibits,
+                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ uoff) {
   const int64_t n = int64_t(1) << ib;
   for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
        x += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t bk = x >> (ib - 16);
+    const int64_t bk = x >> (ib - ibits);
     T[x] -= off[bk] - uoff[bk];
   }
 }
@@ -1308,7 +1317,7 @@ template <class K>
 void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
                         uint32_t* ucnt, cudaStream_t s, const K* src = nullptr,
                         uint32_t scap = 0, uint32_t* Tix = nullptr, uint32_t* Fix = nullptr,
-                        int ib = 0) {
+                        int ib = 0, int ibits = 0) {
   const int64_t avg = (n + nb - 1) / nb;
   const int cap = avg <= 1024 ? 2048 : 4096;
   DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
@@ -1324,7 +1333,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p, src, scap, Tix,
-                                           Fix, ib);
+                                           Fix, ib, ibits);
     };
     if (rcap <= 1280) go(k_bucket_rank<K, 5, true>);
     else if (rcap <= 1536) go(k_bucket_rank<K, 6, true>);
@@ -1344,7 +1353,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
   CG_LAUNCH_CHECK();
   if (Tix) {  // index slices of the buckets the byte-pass kernel finished
     k_bucket_slices<K><<<unsigned(num_sms() * 2), 256, 0, s>>>(ko, off, ucnt, blist.p, nlist.p,
-                                                               Tix, Fix, ib);
+                                                               Tix, Fix, ib, ibits, flag);
     CG_LAUNCH_CHECK();
   }
 }
@@ -1877,7 +1886,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   // sw (the sweep path): the rows are in k_pack_sweep's 256 top-byte regions;
   // k_region_sweep splits them into the 2^16 bucket slots and the bucket
   // pass reads each slot and writes its bucket, sorted, to keys + off[b]
-  const int B = sw ? 16 : (pre_off ? pre_B : msd_prefix_bits(n));
+  const int B = sw ? 8 + sw->B2 : (pre_off ? pre_B : msd_prefix_bits(n));
   K* ko = keys;
   if (!pre_off && !sw)
     radix_passes<K>(keys, alt, nullptr, nullptr, nullptr, false, n, (64 - B) / 8, 8, &ko, nullptr,
@@ -1907,7 +1916,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
                                  int(RsCfg<K>::SMEM)));
     k_region_sweep<K><<<unsigned(256 * tpr), kSortThreads, RsCfg<K>::SMEM, s>>>(
         reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16, cnt16.p,
-        sw->ovf);
+        sw->ovf, sw->B2);
     CG_LAUNCH_CHECK();
     k_clip_counts<<<grid_for(nb + 1, 256), 256, 0, s>>>(cnt16.p, nb, cap16, offb.p);
     CG_LAUNCH_CHECK();
@@ -1921,7 +1930,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   // top pre_skip + B bits
   uint32_t* Tix = sw ? sw->T : nullptr;
   launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s, sw ? slots.p : nullptr,
-                        cap16, Tix, Tix ? sw->F : nullptr, Tix ? sw->b : 0);
+                        cap16, Tix, Tix ? sw->F : nullptr, Tix ? sw->b : 0, B);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
   uint32_t* h = static_cast<uint32_t*>(host_stage(5 * sizeof(uint32_t)));
@@ -1940,7 +1949,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   *nc = total;
   if (Tix) {  // the fused prefix index: final positions and the end sentinel
     if (total != n) {
-      k_fix_index<<<grid_for(int64_t(1) << sw->b, 256), 256, 0, s>>>(Tix, sw->b, offp, uoff.p);
+      k_fix_index<<<grid_for(int64_t(1) << sw->b, 256), 256, 0, s>>>(Tix, sw->b, B, offp, uoff.p);
       CG_LAUNCH_CHECK();
     }
     k_ix_end<<<1, 1, 0, s>>>(Tix + (size_t(1) << sw->b), uint32_t(total));
