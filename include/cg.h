@@ -121,11 +121,12 @@ typedef struct {
   int32_t bucket_log2;  /* prefix index: target log2(cells per bucket); -1 = default (2) */
   int32_t sort_kind;    /* 0 = auto (n <= 2048 and ell <= 256: the whole build in one CTA;
                            else MSD prefix buckets + shared-memory sort for ell <= 128,
-                           prefix/LSD sorts beyond, full LSD fallback; >= 2^24 rows of
-                           ell = 64 or 128 bytes: the sweep path, the pack kernel doing the
-                           first MSD partition), 1 = full LSD only, 2 = auto without the
-                           one-CTA small path, 3 = auto without the sweep path, 4 = auto
-                           with the sweep path at any size (2^18 < n <= 2^26) */
+                           prefix/LSD sorts beyond, full LSD fallback; 2^18 < n <= 2^26
+                           rows of ell = 64 or 128 bytes: the sweep path, the pack kernel
+                           doing the first MSD partition -- below 2^24 rows unless a
+                           1024-row sample shows heavy duplication), 1 = full LSD only,
+                           2 = auto without the one-CTA small path, 3 = auto without the
+                           sweep path, 4 = auto with the sweep path whatever the sample */
   cg_index** index_out; /* if non-NULL, receives the dictionary (release with cg_index_free) */
   cg_stats* stats;      /* if non-NULL, stage times and counters */
   int32_t filter_extra; /* prefix filter resolution: b + filter_extra prefix bits per filter

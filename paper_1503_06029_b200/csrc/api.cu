@@ -570,7 +570,7 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
                             const Shard& sh = Shard(), const uint32_t* top_hist = nullptr,
                             const uint32_t* pre_off = nullptr, int pre_B = 0,
                             const uint32_t* tile_hist = nullptr, const SweepIn* sw = nullptr,
-                            bool* sweep_failed = nullptr) {
+                            bool* sweep_failed = nullptr, int dup_hint = -1) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
   const int W = (ell + 63) / 64;
   SortStats sst;
@@ -595,7 +595,8 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   // the hash dedupe directly.  (Not at >= 2^24 rows, where the sample's
   // read-back would cost every distinct-input build.)
   const bool dupy_msd = msd && !sw && !sh.cells_only && pre_off == nullptr && n >= (int64_t(1) << 18) &&
-                        n < (int64_t(1) << 24) && sample_duplicates(keys.p, n, W, s) >= 8;
+                        n < (int64_t(1) << 24) &&
+                        (dup_hint >= 0 ? dup_hint : int(sample_duplicates(keys.p, n, W, s))) >= 8;
   // the sweep path's bucket pass can write the global dictionary's index
   // (T, F) of the table it produces: shaped for b from n (= nc without
   // duplicates, the case it is for; global_probe falls back to the index
@@ -899,6 +900,45 @@ static void build_from_keys(DevBuf<uint64_t>& keys, int64_t n, int ell, const cg
   }
 }
 
+// The sweep path: pack + first MSD partition into top-byte
+// regions, then build_from_keys with the region sweep.  Mid-size inputs
+// (< 2^24 rows) first sample their duplication on the input bytes (1024
+// rows): heavy duplication (arrangement samples) skews the top bytes
+// and is left to the exact path's hash dedupe (*dup_hint carries the
+// sample there).  false = not taken, or a region/slot overflowed (the stage
+// timer and flags are reset; the caller packs again on the exact path).
+static bool try_sweep(const uint8_t* vecs, int64_t n, int ell, const cg_opts& o,
+                      DevBuf<uint64_t>& keys, uint32_t* flags, StageTimer& tm, cg_stats* st,
+                      Built* b, const Shard& sh, int* dup_hint) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(o.stream);
+  const int W = (ell + 63) / 64;
+  const int B2 = sweep_bits(n);
+  if (o.sort_kind == 1 || o.sort_kind == 3 || W > 2 || B2 == 0 || !pack_sweep_ok(vecs, n, ell))
+    return false;
+  if (o.sort_kind != 4 && n < (int64_t(1) << 24)) {
+    *dup_hint = int(sample_duplicates(reinterpret_cast<const uint64_t*>(vecs), n, ell / 8, s));
+    if (*dup_hint >= 8) return false;
+  }
+  const uint32_t capr = pack_sweep_capr(n);
+  bool failed = false;
+  {
+    DevBuf<uint64_t> regions(size_t(256) * capr * W, s);
+    DevBuf<uint32_t> rc(257, s);  // region counts, overflow flag
+    CG_CUDA(cudaMemsetAsync(rc.p + 256, 0, 4, s));
+    launch_pack_sweep(vecs, n, ell, regions.p, capr, rc.p, flags, rc.p + 256, s);
+    tm.mark();  // 1: pack
+    SweepIn sw{regions.p, capr, rc.p, rc.p + 256};
+    sw.B2 = B2;
+    build_from_keys(keys, n, ell, o, flags, tm, st, b, sh, nullptr, nullptr, 8 + B2, nullptr, &sw,
+                    &failed);
+  }
+  if (failed) {  // skewed top bytes: the exact path from a fresh pack
+    tm.restart();
+    CG_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(uint32_t), s));
+  }
+  return !failed;
+}
+
 static void fill_stats(const StageTimer& tm, int64_t n, cg_stats* st) {
   if (!st) return;
   st->n_in = n;
@@ -1022,30 +1062,12 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     const bool msd = W <= 2 && o.sort_kind != 1;
     DevBuf<uint64_t> keys(size_t(n) * W, s, msd ? Mem::Persist : Mem::Scratch);
     const int B = msd_prefix_bits(n);
-    // the sweep path (large 64/128-bit rows): the pack kernel does the MSD
-    // sort's first partition, the second needs no look-back
-    bool swept = false;
-    if (vecs && msd && o.sort_kind != 3 && sweep_bits(n) > 0 &&
-        pack_sweep_ok(vecs, n, ell, o.sort_kind == 4)) {
-      const uint32_t capr = pack_sweep_capr(n);
-      bool failed = false;
-      {
-        DevBuf<uint64_t> regions(size_t(256) * capr * W, s);
-        DevBuf<uint32_t> rc(257, s);  // region counts, overflow flag
-        CG_CUDA(cudaMemsetAsync(rc.p + 256, 0, 4, s));
-        launch_pack_sweep(vecs, n, ell, regions.p, capr, rc.p, flags.p, rc.p + 256, s);
-        tm.mark();  // 1: pack
-        SweepIn sw{regions.p, capr, rc.p, rc.p + 256};
-        sw.B2 = sweep_bits(n);
-        build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(), nullptr, nullptr, B,
-                        nullptr, &sw, &failed);
-      }
-      swept = !failed;
-      if (failed) {  // skewed top bytes: the exact path from a fresh pack
-        tm.restart();
-        CG_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(uint32_t), s));
-      }
-    }
+    // the sweep path (64/128-bit rows, 2^18 < n <= 2^26): the pack kernel
+    // does the MSD sort's first partition, the second needs no look-back
+    //
+    int dup_hint = -1;
+    const bool swept = vecs && msd && try_sweep(vecs, n, ell, o, keys, flags.p, tm, o.stats, &b,
+                                                Shard(), &dup_hint);
     if (swept) {
       fill_stats(tm, n, o.stats);
       store_counters(o.stats);
@@ -1070,7 +1092,7 @@ static int build_entry(const uint8_t* vecs, const uint64_t* words, int64_t n, in
     tm.mark();  // 1: pack
     build_from_keys(keys, n, ell, o, flags.p, tm, o.stats, &b, Shard(),
                     ((vecs || pin) && msd) ? top_hist.p : nullptr, nullptr, B,
-                    (vecs && msd) ? tile_hist.p : nullptr);
+                    (vecs && msd) ? tile_hist.p : nullptr, nullptr, nullptr, dup_hint);
     fill_stats(tm, n, o.stats);
     store_counters(o.stats);
     }
@@ -1542,14 +1564,18 @@ int cg_dist_local(const uint8_t* vecs, int64_t n_local, int32_t ell, const cg_op
     const int dlo = (64 - B) / 8;
     DevBuf<uint32_t> top_hist(size_t(8 - dlo) * 256, s);
     DevBuf<uint32_t> tile_hist(msd ? size_t((n_local + msd_tile_rows(W) - 1) / msd_tile_rows(W)) * 256 : 1, s);
-    if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
-    launch_pack(vecs, n_local, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo,
-                msd ? tile_hist.p : nullptr, msd_tile_rows(W));
-    tm.mark();
     Shard sh;
     sh.cells_only = true;
-    build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh, msd ? top_hist.p : nullptr,
-                    nullptr, B, msd ? tile_hist.p : nullptr);
+    int dup_hint = -1;
+    if (!(msd && try_sweep(vecs, n_local, ell, o, keys, flags.p, tm, o.stats, &b, sh, &dup_hint))) {
+      if (msd) CG_CUDA(cudaMemsetAsync(top_hist.p, 0, top_hist.n * 4, s));
+      launch_pack(vecs, n_local, ell, keys.p, flags.p, s, msd ? top_hist.p : nullptr, dlo,
+                  msd ? tile_hist.p : nullptr, msd_tile_rows(W));
+      tm.mark();
+      build_from_keys(keys, n_local, ell, o, flags.p, tm, o.stats, &b, sh,
+                      msd ? top_hist.p : nullptr, nullptr, B, msd ? tile_hist.p : nullptr, nullptr,
+                      nullptr, dup_hint);
+    }
     // the run's split into 2^chunk_bits prefix chunks (the pipelined exchange)
     const int C = 1 << chunk_bits;
     if (chunk_bits == 0) {

@@ -33,8 +33,8 @@ int sweep_bits(int64_t n);
 // W <= 2): rows go to 256 regions of capr rows by the top byte of word 0,
 // region d = regions[d * capr * W ..), rcnt[d] rows (unordered inside a
 // region); *ovf != 0 if some region overflowed (the result is then invalid).
-// force: any size (sort_kind 4, tests); else >= 2^24 rows
-bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell, bool force = false);
+// ell = 64 or 128, 16-byte aligned rows (the size rule is sweep_bits)
+bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell);
 uint32_t pack_sweep_capr(int64_t n);
 void launch_pack_sweep(const uint8_t* vecs, int64_t n, int ell, uint64_t* regions, uint32_t capr,
                        uint32_t* rcnt, uint32_t* err, uint32_t* ovf, cudaStream_t s);

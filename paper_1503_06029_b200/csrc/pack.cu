@@ -292,9 +292,9 @@ void launch_pack(const uint8_t* vecs, int64_t n, int ell, uint64_t* keys, uint32
   CG_LAUNCH_CHECK();
 }
 
-bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell, bool force) {
+bool pack_sweep_ok(const uint8_t* vecs, int64_t n, int ell) {
   return (ell == 64 || ell == 128) && (reinterpret_cast<uintptr_t>(vecs) % 16) == 0 &&
-         (force || n >= (int64_t(1) << 24)) && n < (int64_t(1) << 32);
+         n < (int64_t(1) << 32);
 }
 
 int sweep_bits(int64_t n) {
