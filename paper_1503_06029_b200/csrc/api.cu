@@ -1670,6 +1670,15 @@ int cg_dist_merge_chunk(const uint64_t* pieces, const int64_t* counts, int32_t G
         at += counts[g];
       }
     }
+    // MSD: the bucket pass writes the merged chunk straight into the table
+    // (no 1 GB copy of a staged result per rank at C5)
+    if (msd) {
+      int64_t ncm = 0;
+      if (merge_sorted_into(keys.p, boff.p, total, W, B, chunk_bits, dst, &ncm, s)) {
+        *n_table += ncm;
+        return CG_OK;
+      }
+    }
     Shard sh;
     sh.cells_only = true;
     sh.pre_skip = chunk_bits;

@@ -155,6 +155,13 @@ bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t**
                      const uint32_t* tile_hist = nullptr, const uint32_t* side_dev = nullptr,
                      uint32_t* side_host = nullptr, int pre_skip = 0,
                      const struct SweepIn* sw = nullptr);
+// The distributed merge's bucket pass writing straight into the table: rows
+// gathered[0..n) grouped into 2^B buckets (off[2^B + 1], the common top
+// pre_skip bits skipped), each bucket sorted and deduplicated into
+// dst + off[b], then compacted in dst; *nc distinct rows.  false = a bucket
+// the shared-memory passes could not take (gathered is left intact).
+bool merge_sorted_into(uint64_t* gathered, const uint32_t* off, int64_t n, int W, int B,
+                       int pre_skip, uint64_t* dst, int64_t* nc, cudaStream_t s);
 int msd_tile_rows(int W);
 // popcount (optional) and lcp with the next cell, for a canonical table
 void launch_cell_meta(const uint64_t* cells, int64_t nc, int W, uint32_t* popc, uint16_t* lcp,

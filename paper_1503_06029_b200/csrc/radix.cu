@@ -899,8 +899,9 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
   // the bucket's input rows: in place (src == nullptr) or, on the sweep
   // path, bucket bk's slot of scap rows in src; the output always goes to
   // keys + off[bk]
+  // (scap = 0: src has the output's bucket offsets -- the distributed merge)
   auto rsrc = [&](int64_t bk, uint32_t lo) -> const K* {
-    return src ? src + size_t(bk) * scap : keys + lo;
+    return src ? (scap ? src + size_t(bk) * scap : src + lo) : keys + lo;
   };
   auto prefetch = [&](int64_t bk, K* dst, uint64_t* bar) {
     if (BULK) {
@@ -1969,6 +1970,44 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
 
 int msd_tile_rows(int W) {
   return W == 1 ? TileCfg<uint64_t, false>::TILE : TileCfg<ulonglong2, false>::TILE;
+}
+
+namespace {
+template <class K>
+bool merge_into_impl(K* gathered, const uint32_t* off, int64_t n, int B, int pre_skip, K* dst,
+                     int64_t* nc, cudaStream_t s) {
+  const int64_t nb = int64_t(1) << B;
+  DevBuf<uint32_t> ucnt(size_t(nb), s), uoff(size_t(nb), s), flag(1, s);
+  CG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(uint32_t), s));
+  launch_bucket_sort<K>(dst, off, n, nb, B + pre_skip, flag.p, ucnt.p, s, gathered, 0u);
+  CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
+  launch_scan_u32(uoff.p, nb, s);
+  uint32_t* h = static_cast<uint32_t*>(host_stage(3 * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(h + 1, uoff.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(h + 2, ucnt.p + nb - 1, 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  if (h[0]) return false;
+  const int64_t total = int64_t(h[1]) + int64_t(h[2]);
+  if (total != n) {  // cross-run duplicates dropped: close the gaps (gathered is free now)
+    const int64_t blocks = std::min<int64_t>((nb * 32 + 255) / 256, int64_t(num_sms()) * 16);
+    k_compact_buckets<K><<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, s>>>(dst, off, ucnt.p,
+                                                                                uoff.p, nb, gathered);
+    CG_LAUNCH_CHECK();
+    CG_CUDA(cudaMemcpyAsync(dst, gathered, size_t(total) * sizeof(K), cudaMemcpyDeviceToDevice, s));
+  }
+  *nc = total;
+  return true;
+}
+}  // namespace
+
+bool merge_sorted_into(uint64_t* gathered, const uint32_t* off, int64_t n, int W, int B,
+                       int pre_skip, uint64_t* dst, int64_t* nc, cudaStream_t s) {
+  if (W == 1) return merge_into_impl<uint64_t>(gathered, off, n, B, pre_skip, dst, nc, s);
+  if (W == 2)
+    return merge_into_impl<ulonglong2>(reinterpret_cast<ulonglong2*>(gathered), off, n, B, pre_skip,
+                                       reinterpret_cast<ulonglong2*>(dst), nc, s);
+  return false;
 }
 
 bool sort_unique_msd(uint64_t* keys, uint64_t* alt, int64_t n, int W, uint64_t** cells,
