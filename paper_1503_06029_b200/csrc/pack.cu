@@ -13,6 +13,7 @@
 // (x * 0x8040201008040201 >> 56 places byte j at bit 7-j: the 64 partial
 // products land on distinct bit positions, so there are no carries), and
 // writes the word.  Consecutive threads read consecutive 64-byte spans.
+// k_pack_sweep (the sweep path) also does the MSD sort's first partition.
 #include "kernels.cuh"
 
 namespace cgk {

@@ -31,6 +31,16 @@
 //
 // (3) the multi-word LSD (W > 2): per word (least significant first) a
 //   stable sort of (word, u32 row index) pairs, then a row gather.
+//
+// (4) the sweep path (W <= 2, ell = 64/128, 2^18 < n <= 2^26; DESIGN
+//   section 6): the pack kernel (pack.cu: k_pack_sweep) already moved the
+//   rows into 256 over-allocated top-byte regions; k_region_sweep splits
+//   each region by the next B2 bits into slots of ~2^10 rows (one atomicAdd
+//   per tile and slot, no look-back: the order inside a slot is free), and
+//   k_bucket_rank reads each slot and writes its bucket sorted, deduplicated
+//   and -- for the global dictionary -- with its slices of the prefix index
+//   T and filter F.  A region or slot overflow (skewed top bits) makes the
+//   caller re-run the exact path.
 #include <algorithm>
 #include <vector>
 
