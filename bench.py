@@ -143,12 +143,15 @@ def alg_bytes(st: dict, n: int, ell: int) -> dict:
     # the probe kernel's work unit is a tile of 32 cells (probe_global.cu
     # kTileCells); per tile it writes a u32 count and a u64 block position
     tiles = (nc + 31) // 32
+    # sweep path: the bucket pass writes T and F itself (the dict stage has
+    # no kernel of its own, only the index writes move into the sort)
+    fused_dict = W <= 2 and passes == 1 and dict_b > 0 and st.get("us_dict", 1e9) < 50.0
     return {
         "pack": n * (ell + K),
-        "sort": n * sort_key_bytes,
+        "sort": n * sort_key_bytes + (dict_b if fused_dict else 0),
         "dedupe": 0,
         "layers": 0,
-        "dict": nc * K + dict_b,
+        "dict": 0 if fused_dict else nc * K + dict_b,
         "probe": nc * K + dict_b + m * 8 + tiles * 12,
         "edges": m * 16,
     }
