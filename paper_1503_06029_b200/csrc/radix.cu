@@ -260,11 +260,12 @@ template <class K>
 __device__ __forceinline__ uint32_t rs_digit(const K& k, int B2) {
   return uint32_t(KT<K>::top(k) >> (56 - B2)) & ((1u << B2) - 1u);
 }
-template <class K>
+template <class K, int B2T>  // B2T: the digit width at compile time (8 at 2^26 rows), 0 = B2
 __global__ void __launch_bounds__(kSortThreads, RS_MINB)
     k_region_sweep(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
                    uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
-                   uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2) {
+                   uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2arg) {
+  const int B2 = B2T ? B2T : B2arg;
   constexpr int IPT = RsCfg<K>::IPT;
   constexpr int TILE = RsCfg<K>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1922,12 +1923,16 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
     CG_CUDA(cudaMemsetAsync(cnt16.p, 0, cnt16.n * 4, s));
     constexpr int TILE = RsCfg<K>::TILE;
     const uint32_t tpr = (sw->capr + TILE - 1) / TILE;
-    CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CG_CUDA(cudaFuncSetAttribute(k_region_sweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(RsCfg<K>::SMEM)));
-    k_region_sweep<K><<<unsigned(256 * tpr), kSortThreads, RsCfg<K>::SMEM, s>>>(
-        reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16, cnt16.p,
-        sw->ovf, sw->B2);
+    auto go = [&](auto kern) {
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RsCfg<K>::SMEM)));
+      kern<<<unsigned(256 * tpr), kSortThreads, RsCfg<K>::SMEM, s>>>(
+          reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16,
+          cnt16.p, sw->ovf, sw->B2);
+    };
+    if (sw->B2 == 8) go(k_region_sweep<K, 8>);
+    else go(k_region_sweep<K, 0>);
     CG_LAUNCH_CHECK();
     k_clip_counts<<<grid_for(nb + 1, 256), 256, 0, s>>>(cnt16.p, nb, cap16, offb.p);
     CG_LAUNCH_CHECK();
