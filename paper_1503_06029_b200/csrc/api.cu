@@ -922,7 +922,7 @@ static bool try_sweep(const uint8_t* vecs, int64_t n, int ell, const cg_opts& o,
   const uint32_t capr = pack_sweep_capr(n);
   bool failed = false;
   {
-    DevBuf<uint64_t> regions(size_t(256) * capr * W, s);
+    DevBuf<uint64_t> regions(size_t(256) * capr * W + 2, s);  // (+16 B: bulk-copy tail)
     DevBuf<uint32_t> rc(257, s);  // region counts, overflow flag
     CG_CUDA(cudaMemsetAsync(rc.p + 256, 0, 4, s));
     launch_pack_sweep(vecs, n, ell, regions.p, capr, rc.p, flags, rc.p + 256, s);

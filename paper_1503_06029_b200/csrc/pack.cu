@@ -308,7 +308,7 @@ int sweep_bits(int64_t n) {
 uint32_t pack_sweep_capr(int64_t n) {
   // mean region + 1/16 + two tiles: uniform top bytes never come close
   const int64_t mean = (n + 255) / 256;
-  return uint32_t(mean + mean / 16 + 2 * kSweepRows);
+  return uint32_t((mean + mean / 16 + 2 * kSweepRows + 1) & ~int64_t(1));  // even (16-byte rows)
 }
 
 void launch_pack_sweep(const uint8_t* vecs, int64_t n, int ell, uint64_t* regions, uint32_t capr,

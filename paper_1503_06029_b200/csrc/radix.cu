@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(kSortThreads, OS_MINB)
 #ifndef RS_MINB
 #define RS_MINB 3  // region sweep: resident CTAs per SM
 #endif
+#ifndef RS_PERSIST
+#define RS_PERSIST 1  // region sweep as a persistent kernel with TMA prefetch of the next tile
+#endif
 template <class K>
 struct RsCfg {
   static constexpr int IPT = sizeof(K) == 16 ? RS_IPT : 2 * RS_IPT;
@@ -1254,6 +1257,123 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
   cp_async_wait0();
 }
 
+// The region sweep as a persistent kernel (RS_PERSIST): two CTAs per SM walk
+// the tiles with the next tile's rows already on their way -- one TMA bulk
+// copy (cp.async.bulk global->shared, mbarrier completion) per tile issued a
+// whole tile ahead -- so the loads overlap the ranking, the reservation
+// atomics and the writes of the current tile; the tile's buffer is then
+// reused for its own reorder.
+template <class K, int B2T>
+__global__ void __launch_bounds__(kSortThreads, 2)
+    k_region_sweep_p(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
+                     uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
+                     uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2arg) {
+  const int B2 = B2T ? B2T : B2arg;
+  constexpr int IPT = RsCfg<K>::IPT;
+  constexpr int TILE = RsCfg<K>::TILE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* const buf0 = reinterpret_cast<K*>(smem_raw);
+  K* const buf1 = buf0 + TILE;
+  __shared__ uint32_t wcnt[kSortWarps][kRadix];
+  __shared__ uint32_t s_dexcl[kRadix], s_lim[kRadix], s_gbase[kRadix];
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint64_t s_bar[2];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t ntot = 256u * tpr;
+  auto info = [&](uint32_t id, uint32_t& x, uint32_t& beg, int& nt) -> bool {
+    x = id / tpr;
+    const uint32_t cnt = min(rcnt[x], capr);
+    beg = (id % tpr) * uint32_t(TILE);
+    if (beg >= cnt) return false;
+    nt = int(min(uint32_t(TILE), cnt - beg));
+    return true;
+  };
+  auto next_tile = [&](uint32_t id) -> uint32_t {
+    uint32_t x, b;
+    int nt;
+    for (; id < ntot; id += gridDim.x)
+      if (info(id, x, b, nt)) return id;
+    return ntot;
+  };
+  auto issue = [&](uint32_t id, K* dst, uint64_t* bar) {  // thread 0
+    uint32_t x, beg;
+    int nt;
+    if (id < ntot && info(id, x, beg, nt)) {
+      // bulk copies move multiples of 16 bytes from 16-byte aligned
+      // addresses: 8-byte keys round up to an even count (capr is even and
+      // the regions buffer has a 16-byte tail, so the extra key is readable)
+      const uint32_t bytes = (uint32_t(nt) * uint32_t(sizeof(K)) + 15u) & ~15u;
+      // the buffer was last written by the threads (generic proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(bar, bytes);
+      bulk_g2s(dst, regions + size_t(x) * capr + beg, bytes, bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t cur = next_tile(blockIdx.x);
+  if (tid == 0) issue(cur, buf0, &s_bar[0]);
+  for (int it = 0; cur < ntot; ++it) {
+    K* const sb = (it & 1) ? buf1 : buf0;
+    const uint32_t nxt = next_tile(cur + gridDim.x);
+    if (tid == 0) issue(nxt, (it & 1) ? buf0 : buf1, &s_bar[(it + 1) & 1]);
+    for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&wcnt[0][0])[i] = 0;
+    uint32_t x, beg;
+    int nt;
+    info(cur, x, beg, nt);
+    mbar_wait(&s_bar[it & 1], uint32_t(it >> 1) & 1u);
+    __syncthreads();
+    const int wb = w * 32 * IPT;
+    K key[IPT];
+    uint32_t rank[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int g = wb + i * 32 + lane;
+      key[i] = g < nt ? sb[g] : K{};
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if (wb + i * 32 + lane < nt) rank[i] = atomicAdd(&wcnt[w][rs_digit(key[i], B2)], 1u);
+    __syncthreads();
+    uint32_t total = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = wcnt[ww][tid];
+      wcnt[ww][tid] = total;
+      total += c;
+    }
+    uint32_t tile_n;
+    const uint32_t dex = block_excl_scan(total, s_scan, &tile_n);
+    uint32_t base = 0;
+    const uint32_t q = (x << B2) | uint32_t(tid);
+    if (total) base = atomicAdd(&cnt16[q], total);
+    s_dexcl[tid] = dex;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if (wb + i * 32 + lane < nt) {
+        const uint32_t d = rs_digit(key[i], B2);
+        sb[s_dexcl[d] + wcnt[w][d] + rank[i]] = key[i];
+      }
+    }
+    if (total && uint64_t(base) + total > cap16) atomicOr(ovf, 1u);
+    s_gbase[tid] = q * cap16 + base - dex;
+    s_lim[tid] = dex + (base < cap16 ? cap16 - base : 0u);
+    __syncthreads();
+    for (int j = tid; j < nt; j += kSortThreads) {
+      const K k = sb[j];
+      const uint32_t d = rs_digit(k, B2);
+      if (uint32_t(j) < s_lim[d]) slots[s_gbase[d] + uint32_t(j)] = k;
+    }
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
 // Index slices (see k_bucket_rank's fused prefix index) of the buckets listed
 // to the byte-pass kernel, from their finished (deduplicated) rows.
 template <class K>
@@ -1931,8 +2051,23 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
           reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16,
           cnt16.p, sw->ovf, sw->B2);
     };
-    if (sw->B2 == 8) go(k_region_sweep<K, 8>);
-    else go(k_region_sweep<K, 0>);
+    if (RS_PERSIST) {
+      auto gop = [&](auto kern) {
+        const size_t sm = 2 * RsCfg<K>::SMEM;
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        const int grid = int(std::min<int64_t>(int64_t(256) * tpr, int64_t(num_sms()) * 2));
+        kern<<<unsigned(grid), kSortThreads, sm, s>>>(
+            reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16,
+            cnt16.p, sw->ovf, sw->B2);
+      };
+      if (sw->B2 == 8) gop(k_region_sweep_p<K, 8>);
+      else gop(k_region_sweep_p<K, 0>);
+    } else if (sw->B2 == 8) {
+      go(k_region_sweep<K, 8>);
+    } else {
+      go(k_region_sweep<K, 0>);
+    }
     CG_LAUNCH_CHECK();
     k_clip_counts<<<grid_for(nb + 1, 256), 256, 0, s>>>(cnt16.p, nb, cap16, offb.p);
     CG_LAUNCH_CHECK();
