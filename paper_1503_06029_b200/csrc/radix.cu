@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
   auto hx = [](uint32_t d) -> uint32_t {
     return d >= uint32_t(kBins) ? uint32_t(kBins) : (d % kPer) * kBktThreads + d / kPer;
   };
-  __shared__ uint32_t s_nmany;
+  __shared__ uint32_t s_nmany, s_eq;
   __shared__ __align__(16) uint32_t h[kBins + 1];
   __shared__ uint32_t s_scan[33];
   __shared__ uint64_t s_red[2][kBktWarps][2];
@@ -1068,7 +1068,7 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     }
 #pragma unroll
     for (int q = 0; q < kPer; ++q) h[q * kBktThreads + tid] = 0u;
-    if (tid == 0) s_nmany = 0u;
+    if (tid == 0) s_nmany = s_eq = 0u;
     __syncthreads();
     uint64_t dif[2] = {0ull, 0ull};
 #pragma unroll
@@ -1158,12 +1158,18 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     // together (one list entry per thread: no lanes idle behind a long loop);
     // their positions come back through pos_of[]
     uint32_t ps[MAXC];
+    int anyeq = 0;  // two equal keys seen (equal keys share a digit): the dedupe has work
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       const int i = c * kBktThreads + tid;
       const uint32_t pq = min(bs[c] + (rk[c] ^ 1u), uint32_t(CAP - 1));
       const int j = nxt[pq];
-      ps[c] = bs[c] + (ct[c] == 2u ? key_before(s[j], j, kr[c], i) : 0u);
+      ps[c] = bs[c];
+      if (ct[c] == 2u) {
+        const K kj = s[j];
+        ps[c] += key_before(kj, j, kr[c], i);
+        anyeq |= int(key_eq(kj, kr[c]));
+      }
       if (ct[c] > 2u) {
         const uint32_t q = atomicAdd(&s_nmany, 1u);
         if (q < mcap) mlist[q] = uint32_t(i) | (dg[c] << 16);
@@ -1182,11 +1188,15 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
         const uint32_t d = e >> 16, b0 = h[hx(d)], cn = h[hx(d + 1)] - b0;
         const K ki = s[i];
         uint32_t r = 0;
+        uint32_t eq = 0;
         for (uint32_t m = 0; m < cn; ++m) {
           const int j = nxt[b0 + m];
-          r += (j != i) && key_before(s[j], j, ki, i);
+          const K kj = s[j];
+          r += (j != i) && key_before(kj, j, ki, i);
+          eq |= uint32_t(j != i) & uint32_t(key_eq(kj, ki));
         }
         pos_of[i] = uint16_t(b0 + r);
+        if (eq) s_eq = 1u;
       }
       __syncthreads();
 #pragma unroll
@@ -1198,10 +1208,26 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c)
       if (ct[c] != 0u) s[ps[c]] = kr[c];
-    __syncthreads();
+    const bool nodup = !__syncthreads_or(anyeq) && s_eq == 0u;
     // ---- 4. write (deduplicated and compacted when ucnt is given); the
-    // sorted keys are read contiguously
-    if (!ucnt) {
+    // sorted keys are read contiguously.  No two keys compared equal (the
+    // common case): every key is a cell, no dedupe pass over the buffer
+    if (ucnt && nodup) {
+      if (Tix) {
+        ix_zero();
+        __syncthreads();
+      }
+      for (int i = tid; i < S; i += kBktThreads) {
+        const K k = s[i];
+        keys[lo + i] = k;
+        if (Tix) ix_add(k);
+      }
+      if (tid == 0) ucnt[bk] = uint32_t(S);
+      if (Tix) {
+        __syncthreads();
+        ix_write(bk, lo);
+      }
+    } else if (!ucnt) {
       for (int i = tid; i < S; i += kBktThreads) keys[lo + i] = s[i];
     } else {
       uint32_t bl[MAXC];
