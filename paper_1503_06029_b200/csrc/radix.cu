@@ -1289,8 +1289,11 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
 // whole tile ahead -- so the loads overlap the ranking, the reservation
 // atomics and the writes of the current tile; the tile's buffer is then
 // reused for its own reorder.
+#ifndef RS_PMINB
+#define RS_PMINB 2  // persistent region sweep: CTAs per SM
+#endif
 template <class K, int B2T>
-__global__ void __launch_bounds__(kSortThreads, 2)
+__global__ void __launch_bounds__(kSortThreads, RS_PMINB)
     k_region_sweep_p(const K* __restrict__ regions, uint32_t capr, const uint32_t* __restrict__ rcnt,
                      uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
                      uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2arg) {
@@ -2082,7 +2085,7 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
         const size_t sm = 2 * RsCfg<K>::SMEM;
         CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        const int grid = int(std::min<int64_t>(int64_t(256) * tpr, int64_t(num_sms()) * 2));
+        const int grid = int(std::min<int64_t>(int64_t(256) * tpr, int64_t(num_sms()) * RS_PMINB));
         kern<<<unsigned(grid), kSortThreads, sm, s>>>(
             reinterpret_cast<const K*>(sw->regions), sw->capr, sw->rcnt, tpr, slots.p, cap16,
             cnt16.p, sw->ovf, sw->B2);
