@@ -915,11 +915,14 @@ static bool try_sweep(const uint8_t* vecs, int64_t n, int ell, const cg_opts& o,
   const int B2 = sweep_bits(n);
   if (o.sort_kind == 1 || o.sort_kind == 3 || W > 2 || B2 == 0 || !pack_sweep_ok(vecs, n, ell))
     return false;
-  if (o.sort_kind != 4 && n < (int64_t(1) << 24)) {
-    *dup_hint = int(sample_duplicates(reinterpret_cast<const uint64_t*>(vecs), n, ell / 8, s));
-    if (*dup_hint >= 8) return false;
-  }
   const uint32_t capr = pack_sweep_capr(n);
+  if (o.sort_kind != 4 && n < (int64_t(1) << 24)) {
+    // the sample also estimates the fullest top-byte region: skewed bits
+    // (arrangement signatures) would overflow the regions and waste a pack
+    double top = 0.0;
+    *dup_hint = int(sample_duplicates_and_top(vecs, n, ell, s, &top));
+    if (*dup_hint >= 8 || top * double(n) > 0.85 * double(capr)) return false;
+  }
   bool failed = false;
   {
     DevBuf<uint64_t> regions(size_t(256) * capr * W + 2, s);  // (+16 B: bulk-copy tail)

@@ -320,6 +320,43 @@ __global__ void __launch_bounds__(kDupSample)
 
 }  // namespace
 
+// Top-byte histogram of up to kTopSample rows of a byte matrix at a fixed
+// stride (the first 8 bytes of a row are the top byte of its packed key):
+// the sweep path's region-skew estimate.
+constexpr int kTopSample = 65536;
+__global__ void __launch_bounds__(256) k_top_sample(const uint8_t* __restrict__ vecs, int64_t n,
+                                                    int ell, int64_t stride, int S,
+                                                    uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0u;
+  __syncthreads();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < S; q += gridDim.x * blockDim.x) {
+    const uint64_t x = *reinterpret_cast<const uint64_t*>(vecs + int64_t(q) * stride * ell);
+    atomicAdd(&h[uint32_t((x * 0x8040201008040201ull) >> 56)], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+uint32_t sample_duplicates_and_top(const uint8_t* vecs, int64_t n, int ell, cudaStream_t s,
+                                   double* max_top_share) {
+  DevBuf<uint32_t> h(1 + 256, s);
+  CG_CUDA(cudaMemsetAsync(h.p, 0, h.n * 4, s));
+  k_dup_sample<<<1, kDupSample, 0, s>>>(reinterpret_cast<const uint64_t*>(vecs), n, ell / 8, h.p);
+  CG_LAUNCH_CHECK();
+  const int S = int(std::min<int64_t>(n, kTopSample));
+  const int64_t stride = std::max<int64_t>(1, n / S);
+  k_top_sample<<<64, 256, 0, s>>>(vecs, n, ell, stride, S, h.p + 1);
+  CG_LAUNCH_CHECK();
+  uint32_t* hh = static_cast<uint32_t*>(host_stage(257 * sizeof(uint32_t)));
+  CG_CUDA(cudaMemcpyAsync(hh, h.p, 257 * 4, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  uint32_t mx = 0;
+  for (int b = 0; b < 256; ++b) mx = std::max(mx, hh[1 + b]);
+  *max_top_share = double(mx) / double(S);
+  return hh[0];
+}
+
 uint32_t sample_duplicates(const uint64_t* rows, int64_t n, int W, cudaStream_t s) {
   DevBuf<uint32_t> h(1, s);
   k_dup_sample<<<1, kDupSample, 0, s>>>(rows, n, W, h.p);  // a thread per sampled row

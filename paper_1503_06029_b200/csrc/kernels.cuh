@@ -175,6 +175,10 @@ int64_t hash_unique_rows(const uint64_t* rows, int64_t n, int W, uint64_t* out, 
 // repeated rows among 1024 rows sampled at a fixed stride (0 for distinct
 // inputs); host-synchronising
 uint32_t sample_duplicates(const uint64_t* rows, int64_t n, int W, cudaStream_t s);
+// the same duplication sample on a byte matrix (ell = 64/128, 8-byte aligned
+// rows), plus the largest top-byte share among up to 65536 sampled rows
+uint32_t sample_duplicates_and_top(const uint8_t* vecs, int64_t n, int ell, cudaStream_t s,
+                                   double* max_top_share);
 // sorted rows u64[n][W] -> cells u64[n_c][W] (strictly increasing), popc[n_c],
 // lcp[n_c] (leading equal bits with the next cell; 0xffff for the last),
 // *n_cells (device u32).

@@ -307,8 +307,11 @@ int sweep_bits(int64_t n) {
 
 uint32_t pack_sweep_capr(int64_t n) {
   // mean region + 1/16 + two tiles: uniform top bytes never come close
+  // mean + 1/16 (+ 1/2 below 2^24 rows, where a sample screens skewed inputs
+  // first and memory is no concern) + two tiles; even (16-byte bulk copies)
   const int64_t mean = (n + 255) / 256;
-  return uint32_t((mean + mean / 16 + 2 * kSweepRows + 1) & ~int64_t(1));  // even (16-byte rows)
+  const int64_t slack = n < (int64_t(1) << 24) ? mean / 2 : mean / 16;
+  return uint32_t((mean + slack + 2 * kSweepRows + 1) & ~int64_t(1));
 }
 
 void launch_pack_sweep(const uint8_t* vecs, int64_t n, int ell, uint64_t* regions, uint32_t capr,

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kSortThreads, RS_MINB)
                    uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
                    uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2arg) {
   const int B2 = B2T ? B2T : B2arg;
+  if (*ovf) return;  // a region overflowed in the pack: the caller re-runs the exact path
   constexpr int IPT = RsCfg<K>::IPT;
   constexpr int TILE = RsCfg<K>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -872,7 +873,10 @@ __global__ void __launch_bounds__(kBktThreads, PREF ? (MAXC <= 5 ? 4 : 3) : 4)
     k_bucket_rank(K* __restrict__ keys, const uint32_t* __restrict__ off, int64_t nbuckets, int CAP,
                   uint32_t* __restrict__ ucnt, uint32_t* __restrict__ blist,
                   uint32_t* __restrict__ nlist, const K* __restrict__ src, uint32_t scap,
-                  uint32_t* __restrict__ Tix, uint32_t* __restrict__ Fix, int ib, int ibits) {
+                  uint32_t* __restrict__ Tix, uint32_t* __restrict__ Fix, int ib, int ibits,
+                  const uint32_t* __restrict__ abort_flag) {
+  // (sweep path) a region or slot overflowed: the caller re-runs the exact path
+  if (abort_flag && *abort_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // PREF: the next bucket is prefetched (cp.async) into a second buffer;
   // otherwise one buffer and more resident CTAs hide the load latency
@@ -1298,6 +1302,7 @@ __global__ void __launch_bounds__(kSortThreads, RS_PMINB)
                      uint32_t tpr, K* __restrict__ slots, uint32_t cap16,
                      uint32_t* __restrict__ cnt16, uint32_t* __restrict__ ovf, int B2arg) {
   const int B2 = B2T ? B2T : B2arg;
+  if (*ovf) return;  // a region overflowed in the pack: the caller re-runs the exact path
   constexpr int IPT = RsCfg<K>::IPT;
   constexpr int TILE = RsCfg<K>::TILE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1478,7 +1483,7 @@ template <class K>
 void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B, uint32_t* flag,
                         uint32_t* ucnt, cudaStream_t s, const K* src = nullptr,
                         uint32_t scap = 0, uint32_t* Tix = nullptr, uint32_t* Fix = nullptr,
-                        int ib = 0, int ibits = 0) {
+                        int ib = 0, int ibits = 0, const uint32_t* abort_flag = nullptr) {
   const int64_t avg = (n + nb - 1) / nb;
   const int cap = avg <= 1024 ? 2048 : 4096;
   DevBuf<uint32_t> blist(size_t(nb), s), nlist(1, s);
@@ -1494,7 +1499,7 @@ void launch_bucket_sort(K* ko, const uint32_t* off, int64_t n, int64_t nb, int B
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<grid, kBktThreads, smem, s>>>(ko, off, nb, rcap, ucnt, blist.p, nlist.p, src, scap, Tix,
-                                           Fix, ib, ibits);
+                                           Fix, ib, ibits, abort_flag);
     };
     if (rcap <= 1280) go(k_bucket_rank<K, 5, true>);
     else if (rcap <= 1536) go(k_bucket_rank<K, 6, true>);
@@ -2110,7 +2115,8 @@ bool sort_unique_impl(K* keys, K* alt, int64_t n, K** cells, int64_t* nc, cudaSt
   // top pre_skip + B bits
   uint32_t* Tix = sw ? sw->T : nullptr;
   launch_bucket_sort<K>(ko, offp, n, nb, B + pre_skip, flag.p, ucnt.p, s, sw ? slots.p : nullptr,
-                        cap16, Tix, Tix ? sw->F : nullptr, Tix ? sw->b : 0, B);
+                        cap16, Tix, Tix ? sw->F : nullptr, Tix ? sw->b : 0, B,
+                        sw ? sw->ovf : nullptr);
   CG_CUDA(cudaMemcpyAsync(uoff.p, ucnt.p, size_t(nb) * 4, cudaMemcpyDeviceToDevice, s));
   launch_scan_u32(uoff.p, nb, s);
   uint32_t* h = static_cast<uint32_t*>(host_stage(5 * sizeof(uint32_t)));

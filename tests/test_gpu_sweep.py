@@ -211,3 +211,31 @@ def test_sweep_index_kept_for_query(cg):
     assert rc == 0
     np.testing.assert_array_equal(s.cpu().numpy(), os_)
     np.testing.assert_array_equal(nb.cpu().numpy(), onb)
+
+
+@pytest.mark.parametrize("seed,n,ell,dup,p_one", [(41, 300_001, 128, 0.2, 0.5),
+                                                  (42, 400_000, 64, 0.0, 0.45),
+                                                  (43, 262_145, 128, 0.5, 0.3),
+                                                  (44, 500_000, 64, 0.1, 0.5)])
+def test_sweep_default_random_vs_oracle(cg, seed, n, ell, dup, p_one):
+    """Default options at mid sizes (the sweep path unless the byte sample
+    sees heavy duplication or a region/slot overflows on skewed bits: then
+    the exact path) against the oracle, element by element."""
+    import oracle
+
+    x = synth.random_bytes(seed, n, ell, dup_frac=dup, p_one=p_one)
+    # plant Hamming-1 partners so the edge list is not empty
+    rng = np.random.default_rng(seed + 1)
+    src = rng.integers(0, n, size=n // 20)
+    y = x[src].copy()
+    y[np.arange(y.shape[0]), rng.integers(0, ell, size=y.shape[0])] ^= 1
+    x = np.concatenate([x, y])
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    res = cg.build(xt, want_stats=True)
+    torch.cuda.synchronize()
+    cells = res.cells.cpu().numpy().view(np.uint64)
+    edges = res.edges.cpu().numpy().view(np.uint32)
+    rc, oc, oe = oracle.build(x)
+    assert rc == 0
+    _check(cells, edges, oc, oe)
+    assert edges.shape[0] > 0
