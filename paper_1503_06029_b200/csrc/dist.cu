@@ -16,6 +16,9 @@ namespace cgk {
 namespace {
 
 constexpr int kWeightStride = 8;  // cells sampled per weighted cell
+#ifndef SEL_KB
+#define SEL_KB 4  // rows in flight per lane (k_select_rows)
+#endif
 constexpr int kSelThreads = 256;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSelPerWarp = 512;  // cells per warp and tile (16 rounds of 32)
@@ -87,8 +90,9 @@ __global__ void __launch_bounds__(256)
 // U[u] = cells[i], idx[u] = i for the kept cells; src_pos[s] = u for the
 // sources.  Stable compaction: warp ballots + block scan + decoupled
 // look-back (two counters); tiles of kSelTile cells by atomic ticket.
+template <int WT>  // WT: words per row at compile time (1, 2), 0 = W
 __global__ void __launch_bounds__(kSelThreads)
-    k_select_rows(const uint64_t* __restrict__ cells, int64_t nc, int W, int blk_log2,
+    k_select_rows(const uint64_t* __restrict__ cells, int64_t nc, int Wr, int blk_log2,
                   int64_t nblk, int64_t c_lo, int64_t c_hi, int t_lo, int t_hi,
                   uint64_t* __restrict__ U, uint32_t* __restrict__ idx,
                   uint32_t* __restrict__ src_pos, uint64_t* st_keep, uint64_t* st_src,
@@ -97,18 +101,24 @@ __global__ void __launch_bounds__(kSelThreads)
   __shared__ uint32_t s_wk[kSelWarps], s_ws[kSelWarps];
   __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int W = WT ? WT : Wr;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t w0 = tile * kSelTile + int64_t(wid) * kSelPerWarp;
   uint32_t ck = 0, cs = 0;
-  constexpr int kB = 4;  // rows in flight per lane
+  constexpr int kB = SEL_KB;  // rows in flight per lane
   for (int it0 = 0; it0 < kSelPerWarp / 32; it0 += kB) {
     int pc[kB];
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
       const int64_t i = w0 + (it0 + u) * 32 + lane;
-      pc[u] = i < nc ? row_popc(cells + i * W, W) : -1;
+      if (WT == 2) {
+        const ulonglong2 r = i < nc ? reinterpret_cast<const ulonglong2*>(cells)[i] : ulonglong2{};
+        pc[u] = i < nc ? __popcll(r.x) + __popcll(r.y) : -1;
+      } else {
+        pc[u] = i < nc ? row_popc(cells + i * W, W) : -1;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
@@ -165,7 +175,10 @@ __global__ void __launch_bounds__(kSelThreads)
     const uint32_t mk = s_bal[wid][it][0], ms = s_bal[wid][it][1];
     if ((mk >> lane) & 1u) {
       const uint32_t u = bk + __popc(mk & lt);
-      for (int w = 0; w < W; ++w) U[int64_t(u) * W + w] = cells[i * W + w];
+      if (WT == 2)
+        reinterpret_cast<ulonglong2*>(U)[u] = reinterpret_cast<const ulonglong2*>(cells)[i];
+      else
+        for (int w = 0; w < W; ++w) U[int64_t(u) * W + w] = cells[i * W + w];
       idx[u] = uint32_t(i);
       if ((ms >> lane) & 1u) src_pos[bs + __popc(ms & lt)] = u;
     }
@@ -272,7 +285,8 @@ void select_rows(const uint64_t* cells, int64_t nc, int W, int blk_log2, int64_t
   CG_CUDA(cudaMemsetAsync(st.p, 0, st.n * 8, s));
   CG_CUDA(cudaMemsetAsync(ticket.p, 0, 4, s));
   CG_CUDA(cudaMemsetAsync(tot.p, 0, 16, s));
-  k_select_rows<<<unsigned(tiles), kSelThreads, 0, s>>>(cells, nc, W, blk_log2, nblk, c_lo, c_hi,
+  auto sel = W == 2 ? k_select_rows<2> : (W == 1 ? k_select_rows<1> : k_select_rows<0>);
+  sel<<<unsigned(tiles), kSelThreads, 0, s>>>(cells, nc, W, blk_log2, nblk, c_lo, c_hi,
                                                         t_lo, t_hi, U, idx, src_pos, st.p,
                                                         st.p + tiles, ticket.p, tot.p);
   CG_LAUNCH_CHECK();
